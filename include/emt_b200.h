@@ -1,0 +1,150 @@
+/* emt_b200.h — C ABI of the B200 EMT step-loop engine (libemtb200.so).
+ *
+ * Drop-in for the reference executor boundary:
+ *
+ *   WaveformSet interpret(const ScheduleProgram&, const Eigen::VectorXd& initial,
+ *                         int steps, const ExecOptions& = {});
+ *     /root/reference/proj/include/emtgrid/exec.hpp:29-30, proj/src/exec.cpp:350-383
+ *   WaveformSet execute_parallel(const ScheduleProgram&, const Eigen::VectorXd&, int workers,
+ *                                int steps, const ExecOptions& = {});
+ *     /root/reference/proj/include/emtgrid/exec.hpp:36-37, proj/src/exec.cpp:385-500
+ *   dispatched from execute_task, proj/src/pipeline.cpp:20-33
+ *
+ * The schedule crosses the boundary in the reference's own canonical text
+ * form (ScheduleProgram::serialize, proj/src/schedule.cpp:335-411; grammar in
+ * proj/docs/schedule_format.md). The initial arena is `extent*width` doubles,
+ * slot-major with lanes innermost (proj/docs/schedule_format.md:32-34), exactly
+ * the reference's Eigen::VectorXd. Waveforms come back in WaveformSet order:
+ * `steps` rows of `channels*width` doubles, column = channel*width + lane
+ * (proj/include/emtgrid/waveform.hpp:12-37).
+ *
+ * Plain pointers and sizes only. Every call is synchronous unless it says
+ * otherwise. An engine is confined to one host thread at a time.
+ */
+#ifndef EMT_B200_H
+#define EMT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status = 0 on success, else 1 + emtgrid::ErrorCode
+ * (proj/include/emtgrid/common.hpp:11-33), plus engine-specific codes >= 64. */
+typedef enum emt_status {
+    EMT_OK = 0,
+    EMT_MALFORMED_DOCUMENT = 1,
+    EMT_NON_FINITE_STATE = 7,   /* |v| > divergence limit, proj/src/exec.cpp:229-237 */
+    EMT_SINGULAR_MATRIX = 8,    /* pivot check, proj/src/sparse.cpp:135-143 */
+    EMT_DIMENSION_MISMATCH = 10,/* initial.size() != extent*width, proj/src/exec.cpp:340-346 */
+    EMT_CAPACITY_EXCEEDED = 13, /* arena does not fit the device plan */
+    EMT_UNKNOWN_KIND = 14,      /* unregistered kernel code, proj/src/exec.cpp:37-41 */
+    EMT_NON_POSITIVE_INPUT = 20,/* steps < 0, width < 1, ... */
+    EMT_CUDA_ERROR = 64,        /* CUDA runtime failure (message has the detail) */
+    EMT_INVALID_HANDLE = 65,
+} emt_status;
+
+typedef struct emt_engine emt_engine;
+
+/* Where and how an engine runs. Zero-initialise for defaults. */
+typedef struct emt_config {
+    int32_t device;          /* CUDA device ordinal */
+    int32_t lane_begin;      /* first scenario lane this engine owns (multi-GPU shard) */
+    int32_t lane_count;      /* lanes owned; 0 = all lanes from lane_begin */
+    int32_t lanes_per_block; /* 0 = auto (one CTA per SM when the batch allows) */
+    int32_t threads_per_lane;/* 0 = auto (32: one warp per scenario lane) */
+    int32_t reserved[3];
+} emt_config;
+
+/* ExecOptions (proj/include/emtgrid/exec.hpp:17-25). */
+typedef struct emt_exec_options {
+    double divergence_limit; /* <= 0 selects kDivergenceLimit = 1e12 (kernels.hpp:24) */
+    int32_t warmup_steps;    /* steps excluded from measured_seconds */
+    int32_t reserved;
+} emt_exec_options;
+
+/* ExecStats (proj/include/emtgrid/exec.hpp:10-15) plus device counters. */
+typedef struct emt_exec_stats {
+    int32_t factor_count;    /* refactorization passes; == reference lane-0 fcount */
+    int32_t measured_steps;
+    double measured_seconds; /* device time of the step loop after warm-up (CUDA events) */
+    int32_t kernel_launches; /* step-loop kernel launches issued */
+    int32_t switch_events;   /* (step, lane, switch) state changes seen */
+} emt_exec_stats;
+
+/* One switch state change: the process id of the switch's Norton update
+ * (== its canonical component index) changed state at `step` in `lane`. */
+typedef struct emt_switch_event {
+    int32_t step;
+    int32_t lane;
+    int32_t process;
+} emt_switch_event;
+
+/* ---- one-shot drop-in for interpret() ------------------------------------ */
+
+/* Parses `schedule_text`, runs `steps` passes from `initial` on `cfg->device`
+ * and writes the waveform rows. `waves` holds steps*channels*width doubles
+ * (may be NULL), `time` holds `steps` doubles (may be NULL). On error the
+ * status mirrors the reference exception and emt_last_error() carries
+ * "<where>: <message>". */
+emt_status emt_interpret(const char* schedule_text, const double* initial, int64_t initial_len,
+                         int32_t steps, const emt_exec_options* options, const emt_config* cfg,
+                         double* waves, double* time, emt_exec_stats* stats);
+
+/* Thread-local detail of the last failing call on this thread. */
+const char* emt_last_error(void);
+
+/* ---- engine object: resident batch, resumable stepping -------------------- */
+
+/* `const_table` (optional, may be NULL): consts*width doubles, slot-major,
+ * replacing the CONST rows of the text (lets callers widen a base schedule to
+ * `width` scenario lanes without re-serialising it); `width` must then be
+ * given, else it is read from the schedule header. */
+emt_status emt_engine_create(const char* schedule_text, const double* const_table, int32_t width,
+                             const double* initial, int64_t initial_len, const emt_config* cfg,
+                             emt_engine** out);
+void emt_engine_destroy(emt_engine* engine);
+
+/* Shape: lanes owned by this engine, channels, arena extent, const extent,
+ * META steps, nodes, L nnz, U nnz, layers. Any pointer may be NULL. */
+emt_status emt_engine_shape(const emt_engine* engine, int32_t* lanes, int32_t* channels,
+                            int32_t* extent, int32_t* consts, int32_t* steps, int32_t* nodes,
+                            int32_t* l_nnz, int32_t* u_nnz, int32_t* layers);
+
+/* Reserves device waveform storage for `capacity_steps` recorded passes and
+ * rewinds the recorder. Called implicitly by emt_engine_run. */
+emt_status emt_engine_reserve(emt_engine* engine, int32_t capacity_steps);
+
+/* Advances the device-resident batch by `steps` passes starting at absolute
+ * pass index engine->step (t = (step+1)*dt, proj/src/exec.cpp:366), appending
+ * waveform rows to device storage. Asynchronous on the engine's stream when
+ * `sync` is 0; errors raised inside the kernel surface on the next
+ * synchronising call (emt_engine_sync / read / stats). */
+emt_status emt_engine_advance(emt_engine* engine, int32_t steps, int32_t sync);
+emt_status emt_engine_sync(emt_engine* engine);
+
+/* Host copies of recorded rows [row0, row0+rows) (WaveformSet layout, this
+ * engine's lanes only) and their times. */
+emt_status emt_engine_read_waves(emt_engine* engine, int32_t row0, int32_t rows, double* waves,
+                                 double* time);
+/* Current arena (extent*lanes doubles, slot-major) — a STATE v1 snapshot body. */
+emt_status emt_engine_read_state(emt_engine* engine, double* arena);
+/* Recorded switch events so far (up to max); returns total in *count. */
+emt_status emt_engine_read_events(emt_engine* engine, emt_switch_event* events, int32_t max,
+                                  int32_t* count);
+emt_status emt_engine_stats(emt_engine* engine, emt_exec_stats* stats);
+
+/* Raw device pointer of the waveform store (rows x channels x lanes doubles)
+ * and the CUDA stream the engine launches on (cudaStream_t as void*). */
+void* emt_engine_device_waves(emt_engine* engine);
+void* emt_engine_stream(emt_engine* engine);
+
+/* Library build string (arch, flags). */
+const char* emt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMT_B200_H */

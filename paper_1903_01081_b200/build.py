@@ -1,0 +1,55 @@
+"""In-tree build of libemtb200.so for sm_100a (nvcc cross-compiles without a GPU).
+
+The shared object is written next to this file so that it travels with the
+repository snapshot to the GPU box; nothing is JIT-compiled at import time.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libemtb200.so")
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_schedule.cpp")]
+HEADERS = [os.path.join(HERE, "csrc", "host_schedule.hpp"), os.path.join(ROOT, "include", "emt_b200.h")]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo",
+    "-fmad=false",            # no FMA contraction: the reference builds with -ffp-contract=off
+    "-std=c++17",
+    "-ccbin", "/usr/bin/g++",  # system libstdc++ (dynamic), same as the Python process
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return LIB
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SOURCES]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.check_call(cmd)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

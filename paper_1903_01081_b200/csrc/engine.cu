@@ -1,0 +1,863 @@
+// B200 EMT step-loop engine: persistent sm_100a kernel + C ABI (include/emt_b200.h).
+//
+// Design: one warp owns one scenario lane for the whole run.
+// The lane's arena (the reference's slot layout, proj/docs/schedule_format.md)
+// and its constant-table column live in shared memory; the warp walks the
+// schedule's layers in order (proj/src/exec.cpp:364-374), its 32 threads
+// taking the layer's processes in parallel (write sets are disjoint per layer,
+// proj/src/schedule.cpp:229-254), with __syncwarp between layers. The
+// factorize / solve singletons run warp-cooperatively: sparse LU rows in the
+// reference's up-looking order and level-scheduled triangular sweeps that keep
+// every row's subtraction sequence, so results are bit-identical to the
+// reference's lu_factor / lu_solve (proj/src/sparse.cpp:79-172). Compiled with
+// -fmad=false: no FMA contraction, like the reference's -ffp-contract=off.
+// Scenario lanes are independent, so there is no grid-wide synchronisation:
+// a launch advances every lane by N passes and streams waveform rows to HBM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/emt_b200.h"
+#include "host_schedule.hpp"
+
+namespace emtb200 {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr double kDefaultDivergence = 1e12;  // kDivergenceLimit, kernels.hpp:24
+
+// Per-lane error record in global memory: code (1+ErrorCode), step, index.
+struct LaneError {
+    int code, step, index, layer;
+};
+
+struct DevPlan {
+    int W;          // lanes owned by this engine
+    int lpb;        // lanes (warps) per block
+    int use_smem;   // arena + consts in shared memory (else lane-major global scratch)
+    int lane_stride;  // doubles per lane in the working area
+    int ext_pad;      // consts start inside the lane's area
+    int extent, consts, nch, nlatch, layers, nodes, comps, dim, nnz, nwatch;
+    int v_base, mat, l, u, scratch, fcount;
+    int n_fwd, n_bwd;
+    double dt, div_limit;
+
+    const int* layer_begin;  // layers+1, into the regular process list
+    const int* layer_flags;  // bit0 factorize, bit1 solve
+    const int4* procA;       // code, out, out2, state
+    const int4* procB;       // par, par_len, in_base, in_count
+    const int* proc_id;
+    const int* port_slot;
+    const double* port_sign;
+    const int* ch_slot;
+    const int* latch_live;
+    const int* latch_shadow;
+    const int* row_ptr;
+    const int* col_idx;
+    const int* ment_ptr;
+    const int* ment_slot;
+    const double* ment_sign;
+    const int* gat_ptr;
+    const int* gat_slot;
+    const int* fin;  // 5 per component
+    const int* watch;
+    const int* l_row_ptr;
+    const int* l_col;
+    const int* u_row_ptr;
+    const int* u_col;
+    const int* fwd_ptr;
+    const int* fwd_rows;
+    const int* bwd_ptr;
+    const int* bwd_rows;
+
+    double* arena;         // extent x W (slot-major, lanes innermost): resident state between launches
+    const double* ctab;    // consts x W
+    double* work;          // lane-major scratch when !use_smem: W x lane_stride
+    double* waves;         // rows x nch x W
+    unsigned char* refactored;  // per recorded row: some lane refactorized
+    LaneError* lane_err;        // per lane
+    int* events;                // triples step, lane, process
+    int* n_events;
+    int max_events;
+};
+
+__device__ __forceinline__ double rd(const double* A, int slot) { return slot < 0 ? 0.0 : A[slot]; }
+
+// kern::source_value (proj/include/emtgrid/kernels.hpp:68-70)
+__device__ __forceinline__ double source_value(double mag, double omega, double phase, double t) {
+    return omega == 0.0 ? mag : mag * cos(omega * t + phase);
+}
+
+// One non-singleton process for this lane: Engine::run_proc, proj/src/exec.cpp:77-311.
+__device__ __forceinline__ void run_regular(const DevPlan& P, double* __restrict__ A, const double* __restrict__ C,
+                                            int k, double t, int step, int lane) {
+    const int4 a = __ldg(&P.procA[k]);  // code, out, out2, state
+    const int4 b = __ldg(&P.procB[k]);  // par, par_len, in_base, in_count
+    const int* in = P.port_slot + b.z;
+    const double* sg = P.port_sign + b.z;
+    const double* par = C + b.x;
+    double* st = A + a.w;
+    switch (a.x) {
+        case kNortonResistor:
+            A[a.y] = par[0];
+            A[a.z] = 0.0;
+            break;
+        case kNortonInductor: {  // h = i_prev + g*v_prev (kernels.hpp:71-73)
+            const double vs = rd(A, __ldg(in + 1)) - rd(A, __ldg(in + 0));
+            const double g = par[0];
+            A[a.y] = g;
+            A[a.z] = rd(A, __ldg(in + 2)) + g * vs;
+            break;
+        }
+        case kNortonCapacitor: {  // h = -i_prev - g*v_prev (kernels.hpp:74-76)
+            const double vs = rd(A, __ldg(in + 1)) - rd(A, __ldg(in + 0));
+            const double g = par[0];
+            A[a.y] = g;
+            A[a.z] = -rd(A, __ldg(in + 2)) - g * vs;
+            break;
+        }
+        case kNortonSeriesRL: {  // h = decay*i_prev + g*v_prev (kernels.hpp:77-79)
+            const double vs = rd(A, __ldg(in + 1)) - rd(A, __ldg(in + 0));
+            const double g = par[0];
+            A[a.y] = g;
+            A[a.z] = par[1] * rd(A, __ldg(in + 2)) + g * vs;
+            break;
+        }
+        case kNortonVoltageSource: {
+            const double g = par[0];
+            A[a.y] = g;
+            A[a.z] = g * source_value(par[1], par[2], par[3], t);
+            break;
+        }
+        case kNortonCurrentSource:
+            A[a.y] = 0.0;
+            A[a.z] = source_value(par[0], par[1], par[2], t);
+            break;
+        case kNortonControlledSource:
+            A[a.y] = 0.0;
+            A[a.z] = par[0] * (b.w > 3 ? rd(A, __ldg(in + 3)) : 0.0);
+            break;
+        case kNortonSwitch: {  // proj/src/exec.cpp:151-165; state = [now, changed]
+            int now = par[2] != 0.0 ? 1 : 0;
+            for (int j = 3; j < b.y; ++j)
+                if (t >= par[j]) now ^= 1;
+            const double changed = static_cast<double>(now) != st[0] ? 1.0 : 0.0;
+            st[1] = changed;
+            st[0] = static_cast<double>(now);
+            A[a.y] = now != 0 ? par[0] : par[1];
+            A[a.z] = 0.0;
+            if (changed != 0.0 && P.events != nullptr) {
+                const int slot = atomicAdd(P.n_events, 1);
+                if (slot < P.max_events) {
+                    P.events[3 * slot + 0] = step;
+                    P.events[3 * slot + 1] = lane;
+                    P.events[3 * slot + 2] = __ldg(&P.proc_id[k]);
+                }
+            }
+            break;
+        }
+        case kInjectionPair: {
+            const double h = rd(A, __ldg(in + 0));
+            A[a.y] = h;
+            A[a.y + 1] = -h;
+            break;
+        }
+        case kCtlGain:
+            A[a.y] = par[0] * (__ldg(sg + 0) * rd(A, __ldg(in + 0)));
+            break;
+        case kCtlSum: {  // signs applied before sequential accumulation (exec.cpp:245-253)
+            double acc = 0.0;
+            for (int j = 0; j < b.w; ++j) acc += __ldg(sg + j) * rd(A, __ldg(in + j));
+            A[a.y] = acc;
+            break;
+        }
+        case kCtlIntegrator: {  // y = y_prev + dt/2 (u + u_prev) (kernels.hpp:80-82)
+            const double u = __ldg(sg + 0) * rd(A, __ldg(in + 0));
+            const double y = st[0] + par[0] * (u + st[1]);
+            st[0] = y;
+            st[1] = u;
+            A[a.y] = y;
+            break;
+        }
+        case kCtlFirstOrderLag: {  // kernels.hpp:83-85
+            const double u = __ldg(sg + 0) * rd(A, __ldg(in + 0));
+            const double y = par[0] * st[0] + par[1] * (u + st[1]);
+            st[0] = y;
+            st[1] = u;
+            A[a.y] = y;
+            break;
+        }
+        case kCtlLimiter: {  // kernels.hpp:86-88
+            const double u = __ldg(sg + 0) * rd(A, __ldg(in + 0));
+            const double lo = par[0], hi = par[1];
+            A[a.y] = u < lo ? lo : (u > hi ? hi : u);
+            break;
+        }
+        case kCtlPiController: {  // exec.cpp:283-292
+            const double u = __ldg(sg + 0) * rd(A, __ldg(in + 0));
+            st[0] = st[0] + par[1] * (u + st[1]);
+            st[1] = u;
+            A[a.y] = par[0] * u + st[0];
+            break;
+        }
+        case kCtlComparator:
+            A[a.y] = __ldg(sg + 0) * rd(A, __ldg(in + 0)) >= __ldg(sg + 1) * rd(A, __ldg(in + 1)) ? 1.0 : 0.0;
+            break;
+        case kCtlConstant:
+            A[a.y] = par[0];
+            break;
+        case kCtlDelay:
+            A[a.y] = __ldg(sg + 0) * rd(A, __ldg(in + 0));
+            break;
+        default:
+            break;
+    }
+}
+
+__device__ __forceinline__ void lane_fail(const DevPlan& P, int lane, int code, int step, int index, int layer,
+                                          int tl) {
+    if (tl == 0) {
+        LaneError e{code, step, index, layer};
+        P.lane_err[lane] = e;
+    }
+}
+
+// FactorizeSystem for one lane (exec.cpp:175-204 + lu_factor, sparse.cpp:79-145).
+// Refactorizing only lanes whose watch slots are set gives the same factors
+// the reference computes for every lane (unchanged lanes re-derive identical
+// values); the per-row `refactored` flag reproduces its global factor_count.
+__device__ int warp_factorize(const DevPlan& P, double* __restrict__ A, int tl, int lane, int step, int row,
+                              int layer) {
+    bool set = false;
+    for (int q = tl; q < P.nwatch; q += 32) set |= (A[__ldg(&P.watch[q])] != 0.0);
+    if (!__any_sync(kFull, set)) return 0;
+
+    double* G = A + P.mat;
+    for (int k = tl; k < P.nnz; k += 32) {
+        double d = 0.0;
+        for (int q = __ldg(&P.ment_ptr[k]); q < __ldg(&P.ment_ptr[k + 1]); ++q)
+            d += __ldg(&P.ment_sign[q]) * A[__ldg(&P.ment_slot[q])];
+        G[k] = d;
+    }
+    __syncwarp();
+    double m = 0.0;  // max |A| of the lane, sparse.cpp:84-90
+    for (int k = tl; k < P.nnz; k += 32) {
+        const double x = fabs(G[k]);
+        m = m < x ? x : m;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(kFull, m, off);
+        m = m < o ? o : m;
+    }
+    double* S = A + P.scratch;
+    double* Lv = A + P.l;
+    double* Uv = A + P.u;
+    for (int i = 0; i < P.dim; ++i) {
+        const int lb = __ldg(&P.l_row_ptr[i]), le = __ldg(&P.l_row_ptr[i + 1]);
+        const int ub = __ldg(&P.u_row_ptr[i]), ue = __ldg(&P.u_row_ptr[i + 1]);
+        for (int k = lb + tl; k < le; k += 32) S[__ldg(&P.l_col[k])] = 0.0;
+        for (int k = ub + tl; k < ue; k += 32) S[__ldg(&P.u_col[k])] = 0.0;
+        __syncwarp();
+        for (int k = __ldg(&P.row_ptr[i]) + tl; k < __ldg(&P.row_ptr[i + 1]); k += 32)
+            S[__ldg(&P.col_idx[k])] = G[k];
+        __syncwarp();
+        for (int k = lb; k < le; ++k) {
+            const int col = __ldg(&P.l_col[k]);
+            const int cb = __ldg(&P.u_row_ptr[col]), ce = __ldg(&P.u_row_ptr[col + 1]);
+            const double lik = S[col] / Uv[cb];
+            if (tl == 0) Lv[k] = lik;
+            for (int j = cb + 1 + tl; j < ce; j += 32) S[__ldg(&P.u_col[j])] -= lik * Uv[j];
+            __syncwarp();
+        }
+        for (int k = ub + tl; k < ue; k += 32) Uv[k] = S[__ldg(&P.u_col[k])];
+        __syncwarp();
+        if (!(fabs(Uv[ub]) > 1e-12 * m)) {
+            lane_fail(P, lane, 8 /*SingularMatrix*/, step, i, layer, tl);
+            return 1;
+        }
+    }
+    for (int q = tl; q < P.nwatch; q += 32) A[__ldg(&P.watch[q])] = 0.0;
+    if (tl == 0) {
+        A[P.fcount] += 1.0;
+        P.refactored[row] = 1;
+    }
+    __syncwarp();
+    return 0;
+}
+
+// SolveSystem for one lane (exec.cpp:205-239 + lu_solve, sparse.cpp:147-172).
+__device__ int warp_solve(const DevPlan& P, double* __restrict__ A, int tl, int lane, int step, int layer) {
+    double* v = A + P.v_base;
+    for (int node = tl; node < P.nodes; node += 32) {  // canonical gather order, exec.cpp:207-214
+        double acc = 0.0;
+        for (int q = __ldg(&P.gat_ptr[node]); q < __ldg(&P.gat_ptr[node + 1]); ++q) acc += A[__ldg(&P.gat_slot[q])];
+        v[node] = acc;
+    }
+    __syncwarp();
+    if (P.nodes > 0) {
+        const double* Lv = A + P.l;
+        const double* Uv = A + P.u;
+        for (int lv = 0; lv < P.n_fwd; ++lv) {
+            for (int r = __ldg(&P.fwd_ptr[lv]) + tl; r < __ldg(&P.fwd_ptr[lv + 1]); r += 32) {
+                const int i = __ldg(&P.fwd_rows[r]);
+                double x = v[i];
+                for (int k = __ldg(&P.l_row_ptr[i]); k < __ldg(&P.l_row_ptr[i + 1]); ++k)
+                    x -= Lv[k] * v[__ldg(&P.l_col[k])];
+                v[i] = x;
+            }
+            __syncwarp();
+        }
+        for (int lv = 0; lv < P.n_bwd; ++lv) {
+            for (int r = __ldg(&P.bwd_ptr[lv]) + tl; r < __ldg(&P.bwd_ptr[lv + 1]); r += 32) {
+                const int i = __ldg(&P.bwd_rows[r]);
+                const int ub = __ldg(&P.u_row_ptr[i]);
+                double x = v[i];
+                for (int k = ub + 1; k < __ldg(&P.u_row_ptr[i + 1]); ++k) x -= Uv[k] * v[__ldg(&P.u_col[k])];
+                x /= Uv[ub];
+                v[i] = x;
+            }
+            __syncwarp();
+        }
+    }
+    for (int c = tl; c < P.comps; c += 32) {  // i = g (v_b - v_a) + h, exec.cpp:220-228
+        const int* f = P.fin + 5 * c;
+        const double vs = rd(A, __ldg(f + 4)) - rd(A, __ldg(f + 3));
+        A[__ldg(f + 0)] = A[__ldg(f + 1)] * vs + A[__ldg(f + 2)];
+    }
+    int bad = INT_MAX;  // first diverged node index, exec.cpp:229-237
+    for (int node = tl; node < P.nodes; node += 32)
+        if (!(fabs(v[node]) <= P.div_limit)) bad = min(bad, node);
+    for (int off = 16; off > 0; off >>= 1) bad = min(bad, __shfl_xor_sync(kFull, bad, off));
+    __syncwarp();
+    if (bad != INT_MAX) {
+        lane_fail(P, lane, 7 /*NonFiniteState*/, step, bad, layer, tl);
+        return 1;
+    }
+    return 0;
+}
+
+__global__ void __launch_bounds__(1024, 1)
+emt_step_kernel(const DevPlan P, const int step0, const int nsteps, const int row0) {
+    extern __shared__ double smem[];
+    const int wid = threadIdx.x >> 5;
+    const int tl = threadIdx.x & 31;
+    const int lane = blockIdx.x * P.lpb + wid;
+    if (lane >= P.W) return;
+    if (P.lane_err[lane].code != 0) return;  // lane already failed: frozen
+
+    double* A = P.use_smem ? smem + static_cast<size_t>(wid) * P.lane_stride
+                           : P.work + static_cast<size_t>(lane) * P.lane_stride;
+    double* C = A + P.ext_pad;
+    for (int s = tl; s < P.extent; s += 32) A[s] = P.arena[static_cast<size_t>(s) * P.W + lane];
+    for (int s = tl; s < P.consts; s += 32) C[s] = P.ctab[static_cast<size_t>(s) * P.W + lane];
+    __syncwarp();
+
+    int err = 0;
+    int it = 0;
+    for (; it < nsteps; ++it) {
+        const int step = step0 + it;
+        const int row = row0 + it;
+        const double t = static_cast<double>(step + 1) * P.dt;  // exec.cpp:366
+        for (int layer = 0; layer < P.layers; ++layer) {
+            const int e = __ldg(&P.layer_begin[layer + 1]);
+            for (int k = __ldg(&P.layer_begin[layer]) + tl; k < e; k += 32) run_regular(P, A, C, k, t, step, lane);
+            const int fl = __ldg(&P.layer_flags[layer]);
+            if (fl != 0) {
+                __syncwarp();
+                if (fl & 1) err = warp_factorize(P, A, tl, lane, step, row, layer);
+                if (!err && (fl & 2)) err = warp_solve(P, A, tl, lane, step, layer);
+                if (err) break;
+            }
+            __syncwarp();
+        }
+        if (err) break;
+        // record (exec.cpp:313-321) then latch (exec.cpp:323-329)
+        double* wrow = P.waves + static_cast<size_t>(row) * P.nch * P.W;
+        for (int ch = tl; ch < P.nch; ch += 32) wrow[static_cast<size_t>(ch) * P.W + lane] = rd(A, __ldg(&P.ch_slot[ch]));
+        for (int q = tl; q < P.nlatch; q += 32) A[__ldg(&P.latch_shadow[q])] = A[__ldg(&P.latch_live[q])];
+        __syncwarp();
+    }
+    for (int s = tl; s < P.extent; s += 32) P.arena[static_cast<size_t>(s) * P.W + lane] = A[s];
+}
+
+// ----------------------------------------------------------------- host side
+
+thread_local std::string g_last_error;
+
+emt_status set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return static_cast<emt_status>(code);
+}
+
+#define CUDA_TRY(expr)                                                                              \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            return set_error(EMT_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+    } while (0)
+
+}  // namespace emtb200
+
+using namespace emtb200;
+
+struct emt_engine {
+    Schedule sched;
+    int device = 0;
+    int lane_begin = 0;
+    int W = 1;  // lanes owned
+    cudaStream_t stream = nullptr;
+    DevPlan plan{};
+    std::vector<void*> allocations;
+    size_t smem_bytes = 0;
+    int grid = 1;
+    int block = 32;
+    int step = 0;       // absolute next pass index
+    int rows = 0;       // recorded rows
+    int capacity = 0;   // rows the waveform store can hold
+    double* d_waves = nullptr;
+    unsigned char* d_refactored = nullptr;
+    int launches = 0;
+    int failed = 0;
+    int max_events = 1 << 16;
+    double divergence_limit = kDefaultDivergence;
+    std::vector<double> initial_fcount;  // per owned lane, from the initial arena
+    int base_factor_count = 0;           // global lane 0's initial fcount (ExecStats, exec.cpp:376)
+
+    ~emt_engine() {
+        if (device >= 0) cudaSetDevice(device);
+        for (void* p : allocations) cudaFree(p);
+        if (d_waves) cudaFree(d_waves);
+        if (d_refactored) cudaFree(d_refactored);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    template <typename T>
+    emt_status upload(const std::vector<T>& host, const T*& dev) {
+        T* p = nullptr;
+        const size_t bytes = std::max<size_t>(sizeof(T), host.size() * sizeof(T));
+        CUDA_TRY(cudaMalloc(&p, bytes));
+        allocations.push_back(p);
+        if (!host.empty()) CUDA_TRY(cudaMemcpy(p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice));
+        dev = p;
+        return EMT_OK;
+    }
+};
+
+namespace {
+
+#define EMT_TRY(expr)                          \
+    do {                                       \
+        emt_status _s = (expr);                \
+        if (_s != EMT_OK) return _s;           \
+    } while (0)
+
+/// Checks done by interpret before stepping (exec.cpp:340-357).
+emt_status validate(const Schedule& s, int64_t initial_len, int width) {
+    if (initial_len != static_cast<int64_t>(s.extent) * width)
+        return set_error(EMT_DIMENSION_MISMATCH, "initial state size " + std::to_string(initial_len) +
+                                                     " does not match extent " + std::to_string(s.extent) +
+                                                     " x width " + std::to_string(width));
+    for (const Proc& p : s.procs) {
+        if (p.code < 0 || p.code >= kKernelCount)
+            return set_error(EMT_UNKNOWN_KIND, "process " + std::to_string(p.id) + ": kernel code " +
+                                                   std::to_string(p.code) + " is not registered");
+    }
+    if (static_cast<int>(s.l_col.size()) != s.l_nnz || static_cast<int>(s.u_col.size()) != s.u_nnz)
+        return set_error(EMT_MALFORMED_DOCUMENT, "schedule LU fill sizes are inconsistent");
+    return EMT_OK;
+}
+
+emt_status build_plan(emt_engine* e, const double* const_table, int width, const double* initial) {
+    Schedule& s = e->sched;
+    DevPlan& P = e->plan;
+    const int W = e->W;
+    P.W = W;
+    P.extent = s.extent;
+    P.consts = s.consts;
+    P.nch = static_cast<int>(s.channel_slot.size());
+    P.nlatch = static_cast<int>(s.latch_live.size());
+    P.layers = s.layers;
+    P.nodes = s.nodes;
+    P.comps = s.comps;
+    P.dim = s.dim;
+    P.nnz = static_cast<int>(s.col_idx.size());
+    P.nwatch = static_cast<int>(s.watch.size());
+    P.v_base = s.v_base;
+    P.mat = s.matrix;
+    P.l = s.l;
+    P.u = s.u;
+    P.scratch = s.scratch;
+    P.fcount = s.fcount;
+    P.dt = s.dt;
+    P.div_limit = e->divergence_limit;
+
+    // regular processes per layer + singleton flags
+    std::vector<int4> pa, pb;
+    std::vector<int> pid, layer_begin{0}, layer_flags;
+    for (int L = 0; L < s.layers; ++L) {
+        int flags = 0;
+        for (int k = s.layer_begin[static_cast<size_t>(L)]; k < s.layer_begin[static_cast<size_t>(L) + 1]; ++k) {
+            const Proc& p = s.procs[static_cast<size_t>(k)];
+            if (p.code == kFactorizeSystem) { flags |= 1; continue; }
+            if (p.code == kSolveSystem) { flags |= 2; continue; }
+            pa.push_back(make_int4(p.code, p.out, p.out2, p.state));
+            pb.push_back(make_int4(p.par, p.par_len, p.in_base, p.in_count));
+            pid.push_back(p.id);
+        }
+        layer_begin.push_back(static_cast<int>(pa.size()));
+        layer_flags.push_back(flags);
+    }
+    std::vector<int> fwd_ptr, fwd_rows, bwd_ptr, bwd_rows;
+    triangular_levels(s, fwd_ptr, fwd_rows, bwd_ptr, bwd_rows);
+    P.n_fwd = static_cast<int>(fwd_ptr.size()) - 1;
+    P.n_bwd = static_cast<int>(bwd_ptr.size()) - 1;
+    std::vector<int> fin = s.finalize;
+
+    EMT_TRY(e->upload(layer_begin, P.layer_begin));
+    EMT_TRY(e->upload(layer_flags, P.layer_flags));
+    EMT_TRY(e->upload(pa, P.procA));
+    EMT_TRY(e->upload(pb, P.procB));
+    EMT_TRY(e->upload(pid, P.proc_id));
+    EMT_TRY(e->upload(s.port_slot, P.port_slot));
+    EMT_TRY(e->upload(s.port_sign, P.port_sign));
+    EMT_TRY(e->upload(s.channel_slot, P.ch_slot));
+    EMT_TRY(e->upload(s.latch_live, P.latch_live));
+    EMT_TRY(e->upload(s.latch_shadow, P.latch_shadow));
+    EMT_TRY(e->upload(s.row_ptr, P.row_ptr));
+    EMT_TRY(e->upload(s.col_idx, P.col_idx));
+    EMT_TRY(e->upload(s.mentry_ptr, P.ment_ptr));
+    EMT_TRY(e->upload(s.mentry_slot, P.ment_slot));
+    EMT_TRY(e->upload(s.mentry_sign, P.ment_sign));
+    EMT_TRY(e->upload(s.gather_ptr, P.gat_ptr));
+    EMT_TRY(e->upload(s.gather_slot, P.gat_slot));
+    EMT_TRY(e->upload(fin, P.fin));
+    EMT_TRY(e->upload(s.watch, P.watch));
+    EMT_TRY(e->upload(s.l_row_ptr, P.l_row_ptr));
+    EMT_TRY(e->upload(s.l_col, P.l_col));
+    EMT_TRY(e->upload(s.u_row_ptr, P.u_row_ptr));
+    EMT_TRY(e->upload(s.u_col, P.u_col));
+    EMT_TRY(e->upload(fwd_ptr, P.fwd_ptr));
+    EMT_TRY(e->upload(fwd_rows, P.fwd_rows));
+    EMT_TRY(e->upload(bwd_ptr, P.bwd_ptr));
+    EMT_TRY(e->upload(bwd_rows, P.bwd_rows));
+
+    // lane slice of the const table and the initial arena (slot-major, lanes innermost)
+    std::vector<double> ctab(static_cast<size_t>(s.consts) * W), arena(static_cast<size_t>(s.extent) * W);
+    const double* src_c = const_table != nullptr ? const_table : s.const_table.data();
+    for (int k = 0; k < s.consts; ++k)
+        for (int l = 0; l < W; ++l)
+            ctab[static_cast<size_t>(k) * W + l] =
+                src_c[static_cast<size_t>(k) * width + static_cast<size_t>(e->lane_begin + l)];
+    for (int k = 0; k < s.extent; ++k)
+        for (int l = 0; l < W; ++l)
+            arena[static_cast<size_t>(k) * W + l] =
+                initial[static_cast<size_t>(k) * width + static_cast<size_t>(e->lane_begin + l)];
+    e->initial_fcount.resize(static_cast<size_t>(W));
+    for (int l = 0; l < W; ++l) e->initial_fcount[static_cast<size_t>(l)] = arena[static_cast<size_t>(s.fcount) * W + l];
+    e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
+    const double* dc = nullptr;
+    const double* da = nullptr;
+    EMT_TRY(e->upload(ctab, dc));
+    EMT_TRY(e->upload(arena, da));
+    P.ctab = dc;
+    P.arena = const_cast<double*>(da);
+
+    std::vector<LaneError> errs(static_cast<size_t>(W), LaneError{0, 0, 0, 0});
+    const LaneError* de = nullptr;
+    EMT_TRY(e->upload(errs, de));
+    P.lane_err = const_cast<LaneError*>(de);
+    std::vector<int> ev(static_cast<size_t>(3 * e->max_events + 3), 0), nev(1, 0);
+    const int* dev_ev = nullptr;
+    const int* dev_nev = nullptr;
+    EMT_TRY(e->upload(ev, dev_ev));
+    EMT_TRY(e->upload(nev, dev_nev));
+    P.events = const_cast<int*>(dev_ev);
+    P.n_events = const_cast<int*>(dev_nev);
+    P.max_events = e->max_events;
+
+    // work-area geometry: arena then constants per lane
+    P.ext_pad = (s.extent + 1) & ~1;
+    P.lane_stride = P.ext_pad + ((s.consts + 1) & ~1);
+    const size_t lane_bytes = static_cast<size_t>(P.lane_stride) * sizeof(double);
+    int dev_smem = 0, sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+    const int max_lpb_smem = static_cast<int>(static_cast<size_t>(dev_smem) / lane_bytes);
+    P.use_smem = max_lpb_smem >= 1 ? 1 : 0;
+    int lpb = (W + sms - 1) / sms;  // one CTA per SM when the batch is large enough
+    lpb = std::max(1, std::min(lpb, 32));
+    if (P.use_smem) lpb = std::min(lpb, max_lpb_smem);
+    P.lpb = lpb;
+    P.work = nullptr;
+    if (!P.use_smem) {
+        double* w = nullptr;
+        CUDA_TRY(cudaMalloc(&w, lane_bytes * static_cast<size_t>(W)));
+        e->allocations.push_back(w);
+        P.work = w;
+    }
+    e->block = 32 * lpb;
+    e->grid = (W + lpb - 1) / lpb;
+    e->smem_bytes = P.use_smem ? lane_bytes * static_cast<size_t>(lpb) : 0;
+    CUDA_TRY(cudaFuncSetAttribute(emt_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max<size_t>(e->smem_bytes, 0))));
+    return EMT_OK;
+}
+
+emt_status check_lane_errors(emt_engine* e) {
+    std::vector<LaneError> errs(static_cast<size_t>(e->W));
+    CUDA_TRY(cudaMemcpy(errs.data(), e->plan.lane_err, errs.size() * sizeof(LaneError), cudaMemcpyDeviceToHost));
+    // The reference throws at the first failing (step, layer); within it, the
+    // lowest row/node index, then the lowest lane (sparse.cpp:135-143, exec.cpp:229-237).
+    const LaneError* best = nullptr;
+    int best_lane = -1;
+    for (int l = 0; l < e->W; ++l) {
+        const LaneError& x = errs[static_cast<size_t>(l)];
+        if (x.code == 0) continue;
+        if (best == nullptr || x.step < best->step || (x.step == best->step && x.layer < best->layer) ||
+            (x.step == best->step && x.layer == best->layer && x.index < best->index)) {
+            best = &x;
+            best_lane = l;
+        }
+    }
+    if (best == nullptr) return EMT_OK;
+    e->failed = 1;
+    const int glane = e->lane_begin + best_lane;
+    if (best->code == EMT_SINGULAR_MATRIX)
+        return set_error(best->code, "row " + std::to_string(best->index) + ": zero pivot below tolerance" +
+                                         (e->sched.width > 1 ? " in lane " + std::to_string(glane) : std::string()) +
+                                         " (step " + std::to_string(best->step) + ")");
+    return set_error(best->code, "node index " + std::to_string(best->index) + ": node voltage diverged (step " +
+                                     std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* emt_last_error(void) { return g_last_error.c_str(); }
+
+const char* emt_version(void) {
+    return "emtb200 persistent-warp engine; sm_100a; -fmad=false";
+}
+
+emt_status emt_engine_create(const char* schedule_text, const double* const_table, int32_t width,
+                             const double* initial, int64_t initial_len, const emt_config* cfg,
+                             emt_engine** out) {
+    if (out == nullptr || schedule_text == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    *out = nullptr;
+    auto e = std::make_unique<emt_engine>();
+    Failure f;
+    if (!parse_schedule(schedule_text, e->sched, f))
+        return set_error(f.code, (f.where.empty() ? "" : f.where + ": ") + f.message);
+    if (width <= 0) width = e->sched.width;
+    if (const_table == nullptr && width != e->sched.width)
+        return set_error(EMT_DIMENSION_MISMATCH, "width differs from the schedule and no const table was given");
+    lu_symbolic(e->sched);
+    EMT_TRY(validate(e->sched, initial_len, width));
+    emt_config c{};
+    if (cfg != nullptr) c = *cfg;
+    e->device = c.device;
+    e->lane_begin = c.lane_begin;
+    e->W = c.lane_count > 0 ? c.lane_count : width - c.lane_begin;
+    if (e->lane_begin < 0 || e->W < 1 || e->lane_begin + e->W > width)
+        return set_error(EMT_NON_POSITIVE_INPUT, "lane range outside the batch");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    EMT_TRY(build_plan(e.get(), const_table, width, initial));
+    if (c.lanes_per_block > 0) {
+        e->plan.lpb = std::min(c.lanes_per_block, 32);
+        const size_t lane_bytes = static_cast<size_t>(e->plan.lane_stride) * sizeof(double);
+        e->block = 32 * e->plan.lpb;
+        e->grid = (e->W + e->plan.lpb - 1) / e->plan.lpb;
+        e->smem_bytes = e->plan.use_smem ? lane_bytes * static_cast<size_t>(e->plan.lpb) : 0;
+        CUDA_TRY(cudaFuncSetAttribute(emt_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(e->smem_bytes)));
+    }
+    *out = e.release();
+    return EMT_OK;
+}
+
+void emt_engine_destroy(emt_engine* engine) { delete engine; }
+
+emt_status emt_engine_shape(const emt_engine* e, int32_t* lanes, int32_t* channels, int32_t* extent,
+                            int32_t* consts, int32_t* steps, int32_t* nodes, int32_t* l_nnz, int32_t* u_nnz,
+                            int32_t* layers) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (lanes) *lanes = e->W;
+    if (channels) *channels = static_cast<int32_t>(e->sched.channel_slot.size());
+    if (extent) *extent = e->sched.extent;
+    if (consts) *consts = e->sched.consts;
+    if (steps) *steps = e->sched.steps;
+    if (nodes) *nodes = e->sched.nodes;
+    if (l_nnz) *l_nnz = static_cast<int32_t>(e->sched.l_col.size());
+    if (u_nnz) *u_nnz = static_cast<int32_t>(e->sched.u_col.size());
+    if (layers) *layers = e->sched.layers;
+    return EMT_OK;
+}
+
+emt_status emt_engine_reserve(emt_engine* e, int32_t capacity_steps) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (capacity_steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative capacity");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (capacity_steps > e->capacity) {
+        if (e->d_waves) cudaFree(e->d_waves);
+        if (e->d_refactored) cudaFree(e->d_refactored);
+        e->d_waves = nullptr;
+        e->d_refactored = nullptr;
+        const size_t row = static_cast<size_t>(e->plan.nch) * e->W;
+        CUDA_TRY(cudaMalloc(&e->d_waves, std::max<size_t>(8, row * capacity_steps * sizeof(double))));
+        CUDA_TRY(cudaMalloc(&e->d_refactored, std::max<size_t>(1, static_cast<size_t>(capacity_steps))));
+        e->capacity = capacity_steps;
+    }
+    if (e->d_refactored) CUDA_TRY(cudaMemset(e->d_refactored, 0, static_cast<size_t>(std::max(1, e->capacity))));
+    e->rows = 0;
+    return EMT_OK;
+}
+
+emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
+    if (e->failed) return set_error(EMT_INVALID_HANDLE, "engine stopped after an error: " + g_last_error);
+    if (steps == 0) return EMT_OK;
+    if (e->rows + steps > e->capacity)
+        return set_error(EMT_CAPACITY_EXCEEDED, "waveform store holds " + std::to_string(e->capacity) + " rows");
+    CUDA_TRY(cudaSetDevice(e->device));
+    DevPlan P = e->plan;
+    P.waves = e->d_waves;
+    P.refactored = e->d_refactored;
+    emt_step_kernel<<<e->grid, e->block, e->smem_bytes, e->stream>>>(P, e->step, steps, e->rows);
+    CUDA_TRY(cudaGetLastError());
+    e->launches += 1;
+    e->step += steps;
+    e->rows += steps;
+    if (sync) return emt_engine_sync(e);
+    return EMT_OK;
+}
+
+emt_status emt_engine_sync(emt_engine* e) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return check_lane_errors(e);
+}
+
+emt_status emt_engine_read_waves(emt_engine* e, int32_t row0, int32_t rows, double* waves, double* time) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (row0 < 0 || rows < 0 || row0 + rows > e->rows) return set_error(EMT_NON_POSITIVE_INPUT, "row range");
+    EMT_TRY(emt_engine_sync(e));
+    const size_t row = static_cast<size_t>(e->plan.nch) * e->W;
+    if (waves != nullptr && rows > 0)
+        CUDA_TRY(cudaMemcpy(waves, e->d_waves + row * row0, row * rows * sizeof(double), cudaMemcpyDeviceToHost));
+    if (time != nullptr) {
+        const int first_step = e->step - e->rows;
+        for (int r = 0; r < rows; ++r) time[r] = static_cast<double>(first_step + row0 + r + 1) * e->sched.dt;
+    }
+    return EMT_OK;
+}
+
+emt_status emt_engine_read_state(emt_engine* e, double* arena) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    CUDA_TRY(cudaMemcpy(arena, e->plan.arena, static_cast<size_t>(e->sched.extent) * e->W * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    // The reference bumps every lane's fcount on each batch refactorization
+    // (exec.cpp:201-202); lanes refactorize individually here, so rebuild it.
+    emt_exec_stats st{};
+    EMT_TRY(emt_engine_stats(e, &st));
+    const int passes = st.factor_count - e->base_factor_count;
+    for (int l = 0; l < e->W; ++l)
+        arena[static_cast<size_t>(e->sched.fcount) * e->W + l] = e->initial_fcount[static_cast<size_t>(l)] + passes;
+    return EMT_OK;
+}
+
+emt_status emt_engine_read_events(emt_engine* e, emt_switch_event* events, int32_t max, int32_t* count) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    int n = 0;
+    CUDA_TRY(cudaMemcpy(&n, e->plan.n_events, sizeof(int), cudaMemcpyDeviceToHost));
+    if (count) *count = n;
+    const int take = std::min(std::min(n, e->max_events), std::max(0, max));
+    if (events != nullptr && take > 0) {
+        std::vector<int> raw(static_cast<size_t>(3 * take));
+        CUDA_TRY(cudaMemcpy(raw.data(), e->plan.events, raw.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        std::vector<emt_switch_event> ev(static_cast<size_t>(take));
+        for (int k = 0; k < take; ++k)
+            ev[static_cast<size_t>(k)] = {raw[3 * k], raw[3 * k + 1] + e->lane_begin, raw[3 * k + 2]};
+        std::sort(ev.begin(), ev.end(), [](const emt_switch_event& a, const emt_switch_event& b) {
+            if (a.step != b.step) return a.step < b.step;
+            if (a.lane != b.lane) return a.lane < b.lane;
+            return a.process < b.process;
+        });
+        std::memcpy(events, ev.data(), ev.size() * sizeof(emt_switch_event));
+    }
+    return EMT_OK;
+}
+
+emt_status emt_engine_stats(emt_engine* e, emt_exec_stats* stats) {
+    if (e == nullptr || stats == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    std::vector<unsigned char> flags(static_cast<size_t>(std::max(1, e->rows)));
+    if (e->rows > 0)
+        CUDA_TRY(cudaMemcpy(flags.data(), e->d_refactored, static_cast<size_t>(e->rows), cudaMemcpyDeviceToHost));
+    int fc = 0;
+    for (int r = 0; r < e->rows; ++r) fc += flags[static_cast<size_t>(r)] ? 1 : 0;
+    // fcount slot of the arena carries refactorizations before this recording window
+    stats->factor_count = fc + e->base_factor_count;
+    int n = 0;
+    CUDA_TRY(cudaMemcpy(&n, e->plan.n_events, sizeof(int), cudaMemcpyDeviceToHost));
+    stats->switch_events = n;
+    stats->kernel_launches = e->launches;
+    return EMT_OK;
+}
+
+void* emt_engine_device_waves(emt_engine* e) { return e ? e->d_waves : nullptr; }
+void* emt_engine_stream(emt_engine* e) { return e ? e->stream : nullptr; }
+
+emt_status emt_interpret(const char* schedule_text, const double* initial, int64_t initial_len, int32_t steps,
+                         const emt_exec_options* options, const emt_config* cfg, double* waves, double* time,
+                         emt_exec_stats* stats) {
+    if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
+    emt_engine* raw = nullptr;
+    emt_config c{};
+    if (cfg) c = *cfg;
+    c.lane_begin = 0;
+    c.lane_count = 0;
+    EMT_TRY(emt_engine_create(schedule_text, nullptr, 0, initial, initial_len, &c, &raw));
+    std::unique_ptr<emt_engine> e(raw);
+    if (options && options->divergence_limit > 0) e->plan.div_limit = options->divergence_limit;
+    const int warm = options ? std::max(0, std::min<int>(options->warmup_steps, steps)) : 0;
+    EMT_TRY(emt_engine_reserve(e.get(), steps));
+    cudaEvent_t t0, t1;
+    CUDA_TRY(cudaEventCreate(&t0));
+    CUDA_TRY(cudaEventCreate(&t1));
+    EMT_TRY(emt_engine_advance(e.get(), warm, 0));
+    CUDA_TRY(cudaEventRecord(t0, e->stream));
+    EMT_TRY(emt_engine_advance(e.get(), steps - warm, 0));
+    CUDA_TRY(cudaEventRecord(t1, e->stream));
+    emt_status st = emt_engine_sync(e.get());
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (st != EMT_OK) return st;
+    EMT_TRY(emt_engine_read_waves(e.get(), 0, steps, waves, time));
+    if (stats) {
+        EMT_TRY(emt_engine_stats(e.get(), stats));
+        stats->measured_steps = steps - warm;
+        stats->measured_seconds = static_cast<double>(ms) * 1e-3;
+    }
+    return EMT_OK;
+}
+
+}  // extern "C"

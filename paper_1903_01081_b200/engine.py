@@ -1,0 +1,292 @@
+"""Python host API over libemtb200.so, mirroring the reference executor interface.
+
+    interpret(schedule, initial, steps, options)          ~ emtgrid::interpret
+        /root/reference/proj/include/emtgrid/exec.hpp:29-30, proj/src/exec.cpp:350-383
+    execute_parallel(schedule, initial, workers, steps)   ~ emtgrid::execute_parallel
+        proj/include/emtgrid/exec.hpp:36-37 (the device is the parallel executor)
+    WaveformSet                                           ~ proj/include/emtgrid/waveform.hpp:12-37
+    EmtError(code, where, message)                        ~ emtgrid::Error, proj/include/emtgrid/common.hpp:39-58
+
+`schedule` is the reference's canonical `.cgmsched` text (ScheduleProgram::serialize)
+and `initial` the flat extent*width arena (build_initial_arena / parse_state).
+There is no CPU path: a missing or unloadable libemtb200.so raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import build as _build
+
+ERROR_CODES = [
+    "MalformedDocument", "UnknownComponentKind", "DanglingReference", "DuplicateIdentifier",
+    "InvalidParameter", "ArityMismatch", "NonFiniteState", "SingularMatrix", "SingularSystem",
+    "DimensionMismatch", "CycleDetected", "TopologyMismatch", "CapacityExceeded", "UnknownKind",
+    "UnknownDialect", "ToolchainUnavailable", "CompilationFailed", "UnknownTask", "NotFinished",
+    "NonPositiveInput", "IoError",
+]
+
+
+class EmtError(RuntimeError):
+    """emtgrid::Error equivalent: ``code`` is the ErrorCode name, ``status`` the C status."""
+
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        if 1 <= status <= len(ERROR_CODES):
+            self.code = ERROR_CODES[status - 1]
+        elif status == 64:
+            self.code = "CudaError"
+        else:
+            self.code = f"Status{status}"
+        self.detail = detail
+        super().__init__(f"{self.code}: {detail}")
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("lane_begin", ctypes.c_int32), ("lane_count", ctypes.c_int32),
+                ("lanes_per_block", ctypes.c_int32), ("threads_per_lane", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("divergence_limit", ctypes.c_double), ("warmup_steps", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("factor_count", ctypes.c_int32), ("measured_steps", ctypes.c_int32),
+                ("measured_seconds", ctypes.c_double), ("kernel_launches", ctypes.c_int32),
+                ("switch_events", ctypes.c_int32)]
+
+
+class _Event(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int32), ("lane", ctypes.c_int32), ("process", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Loads the in-tree CUDA library; raises if it is absent (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError(f"{_build.LIB} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(_build.LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        ip = ctypes.POINTER(ctypes.c_int32)
+        vp = ctypes.c_void_p
+        L.emt_last_error.restype = ctypes.c_char_p
+        L.emt_version.restype = ctypes.c_char_p
+        L.emt_interpret.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32,
+                                    ctypes.POINTER(_Options), ctypes.POINTER(_Config), dp, dp,
+                                    ctypes.POINTER(_Stats)]
+        L.emt_engine_create.argtypes = [ctypes.c_char_p, dp, ctypes.c_int32, dp, ctypes.c_int64,
+                                        ctypes.POINTER(_Config), ctypes.POINTER(vp)]
+        L.emt_engine_destroy.argtypes = [vp]
+        L.emt_engine_destroy.restype = None
+        L.emt_engine_shape.argtypes = [vp] + [ip] * 9
+        L.emt_engine_reserve.argtypes = [vp, ctypes.c_int32]
+        L.emt_engine_advance.argtypes = [vp, ctypes.c_int32, ctypes.c_int32]
+        L.emt_engine_sync.argtypes = [vp]
+        L.emt_engine_read_waves.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp, dp]
+        L.emt_engine_read_state.argtypes = [vp, dp]
+        L.emt_engine_read_events.argtypes = [vp, ctypes.POINTER(_Event), ctypes.c_int32, ip]
+        L.emt_engine_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
+        L.emt_engine_device_waves.argtypes = [vp]
+        L.emt_engine_device_waves.restype = vp
+        L.emt_engine_stream.argtypes = [vp]
+        L.emt_engine_stream.restype = vp
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = [
+    "emt_interpret", "emt_last_error", "emt_engine_create", "emt_engine_destroy", "emt_engine_shape",
+    "emt_engine_reserve", "emt_engine_advance", "emt_engine_sync", "emt_engine_read_waves",
+    "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
+    "emt_engine_stream", "emt_version",
+]
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise EmtError(status, lib().emt_last_error().decode(errors="replace"))
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def channel_names(schedule: str) -> List[str]:
+    return [ln.split()[1] for ln in schedule.splitlines() if ln.startswith("CHANNEL ")]
+
+
+def schedule_width(schedule: str) -> int:
+    head = schedule.split("\n", 1)[0].split()
+    return int(next(t for t in head if t.startswith("width=")).split("=")[1])
+
+
+@dataclass
+class ExecStats:
+    factor_count: int = 0
+    measured_seconds: float = 0.0
+    measured_steps: int = 0
+    kernel_launches: int = 0
+    switch_events: int = 0
+
+
+@dataclass
+class ExecOptions:
+    divergence_limit: float = 1e12
+    warmup_steps: int = 0
+    stats: Optional[ExecStats] = None
+
+
+@dataclass
+class WaveformSet:
+    """Recorded channels; values rows = steps, column = channel*width + lane."""
+    channels: List[str]
+    width: int
+    time: np.ndarray
+    values: np.ndarray
+
+    def steps(self) -> int:
+        return len(self.time)
+
+    def at(self, step: int, channel: int, lane: int = 0) -> float:
+        return float(self.values[step, channel * self.width + lane])
+
+    def lane(self, lane: int) -> "WaveformSet":
+        cols = [c * self.width + lane for c in range(len(self.channels))]
+        return WaveformSet(list(self.channels), 1, self.time.copy(), self.values[:, cols].copy())
+
+    def to_text(self) -> str:
+        """WaveformSet::to_text (proj/src/waveform.cpp:22-42): %.17g rows."""
+        head = ["time"]
+        for name in self.channels:
+            head += [name] if self.width == 1 else [f"{name}#{l}" for l in range(self.width)]
+        lines = [" ".join(head)]
+        for r in range(len(self.time)):
+            lines.append(" ".join(["%.17g" % self.time[r]] + ["%.17g" % x for x in self.values[r]]))
+        return "\n".join(lines) + "\n"
+
+
+def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per_block: int = 0) -> _Config:
+    c = _Config()
+    c.device, c.lane_begin, c.lane_count, c.lanes_per_block = device, lane_begin, lane_count, lanes_per_block
+    return c
+
+
+def interpret(schedule: str, initial: np.ndarray, steps: int, options: Optional[ExecOptions] = None,
+              device: int = 0) -> WaveformSet:
+    """Drop-in for emtgrid::interpret on the B200 (one-shot: upload, run, download)."""
+    L = lib()
+    init = np.ascontiguousarray(initial, dtype=np.float64)
+    width = schedule_width(schedule)
+    names = channel_names(schedule)
+    waves = np.zeros((max(steps, 0), len(names) * width))
+    time = np.zeros(max(steps, 0))
+    opt = _Options()
+    opt.divergence_limit = options.divergence_limit if options else 1e12
+    opt.warmup_steps = options.warmup_steps if options else 0
+    st = _Stats()
+    cfg = _config(device)
+    _check(L.emt_interpret(schedule.encode(), _dp(init), init.size, steps, ctypes.byref(opt), ctypes.byref(cfg),
+                           _dp(waves), _dp(time), ctypes.byref(st)))
+    if options is not None and options.stats is not None:
+        s = options.stats
+        s.factor_count, s.measured_seconds, s.measured_steps = st.factor_count, st.measured_seconds, st.measured_steps
+        s.kernel_launches, s.switch_events = st.kernel_launches, st.switch_events
+    return WaveformSet(names, width, time, waves)
+
+
+def execute_parallel(schedule: str, initial: np.ndarray, workers: int, steps: int,
+                     options: Optional[ExecOptions] = None, device: int = 0) -> WaveformSet:
+    """emtgrid::execute_parallel signature; the GPU is the parallel executor, so
+    `workers` only keeps the reference's NonPositiveInput contract (exec.cpp:387-389)."""
+    if workers < 1:
+        raise EmtError(20, "worker count must be at least 1")
+    return interpret(schedule, initial, steps, options, device)
+
+
+class Engine:
+    """Device-resident batch: create once, advance in chunks, read waveforms/state."""
+
+    def __init__(self, schedule: str, initial: np.ndarray, const_table: Optional[np.ndarray] = None,
+                 width: int = 0, device: int = 0, lane_begin: int = 0, lane_count: int = 0,
+                 lanes_per_block: int = 0):
+        L = lib()
+        self._h = ctypes.c_void_p()
+        init = np.ascontiguousarray(initial, dtype=np.float64)
+        ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
+        cfg = _config(device, lane_begin, lane_count, lanes_per_block)
+        _check(L.emt_engine_create(schedule.encode(), _dp(ct) if ct is not None else None, int(width), _dp(init),
+                                   init.size, ctypes.byref(cfg), ctypes.byref(self._h)))
+        vals = [ctypes.c_int32() for _ in range(9)]
+        _check(L.emt_engine_shape(self._h, *[ctypes.byref(v) for v in vals]))
+        (self.lanes, self.channels, self.extent, self.consts, self.default_steps, self.nodes, self.l_nnz,
+         self.u_nnz, self.layers) = (v.value for v in vals)
+        self.channel_names = channel_names(schedule)
+        self.rows = 0
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            lib().emt_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def reserve(self, capacity_steps: int) -> None:
+        _check(lib().emt_engine_reserve(self._h, int(capacity_steps)))
+        self.rows = 0
+
+    def advance(self, steps: int, sync: bool = False) -> None:
+        _check(lib().emt_engine_advance(self._h, int(steps), 1 if sync else 0))
+        self.rows += steps
+
+    def sync(self) -> None:
+        _check(lib().emt_engine_sync(self._h))
+
+    def waves(self, row0: int = 0, rows: Optional[int] = None) -> WaveformSet:
+        rows = self.rows - row0 if rows is None else rows
+        v = np.zeros((rows, self.channels * self.lanes))
+        t = np.zeros(rows)
+        _check(lib().emt_engine_read_waves(self._h, row0, rows, _dp(v), _dp(t)))
+        return WaveformSet(list(self.channel_names), self.lanes, t, v)
+
+    def state(self) -> np.ndarray:
+        a = np.zeros(self.extent * self.lanes)
+        _check(lib().emt_engine_read_state(self._h, _dp(a)))
+        return a
+
+    def events(self, max_events: int = 1 << 16) -> np.ndarray:
+        buf = (_Event * max_events)()
+        n = ctypes.c_int32()
+        _check(lib().emt_engine_read_events(self._h, buf, max_events, ctypes.byref(n)))
+        k = min(n.value, max_events)
+        return np.array([(buf[i].step, buf[i].lane, buf[i].process) for i in range(k)], dtype=np.int32).reshape(-1, 3)
+
+    def stats(self) -> ExecStats:
+        st = _Stats()
+        _check(lib().emt_engine_stats(self._h, ctypes.byref(st)))
+        return ExecStats(st.factor_count, st.measured_seconds, st.measured_steps, st.kernel_launches,
+                         st.switch_events)
+
+    def device_waves_ptr(self) -> int:
+        return int(lib().emt_engine_device_waves(self._h) or 0)
+
+    def stream_ptr(self) -> int:
+        return int(lib().emt_engine_stream(self._h) or 0)

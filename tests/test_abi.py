@@ -1,0 +1,37 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol the header declares.
+
+No compute calls here (no GPU in the dev container)."""
+import ctypes
+import os
+import re
+import subprocess
+
+from conftest import ROOT
+from paper_1903_01081_b200 import build, engine
+
+HEADER = os.path.join(ROOT, "include", "emt_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(emt_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_builds_and_exports_header_symbols():
+    path = build.build()
+    assert os.path.exists(path)
+    lib = ctypes.CDLL(path)
+    syms = declared_symbols()
+    assert "emt_interpret" in syms and "emt_engine_advance" in syms
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert set(engine.EXPORTED_SYMBOLS) <= set(syms)
+
+
+def test_library_is_sm100a_native():
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_version_string():
+    assert b"sm_100a" in engine.lib().emt_version()

@@ -1,0 +1,92 @@
+"""CUDA engine vs the oracle / reference goldens (runs on the B200 box: -m gpu).
+
+Bar (north_star): waveforms within 1e-9 relative + 1e-12 absolute on every
+sample; switch events, topology and factor counts bit-exact. Cases without
+cos() sources must be bit-identical (same operation order, -fmad=false).
+"""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_CASES, bitwise_equal, load_golden, within_tolerance
+from oracle import oracle
+from paper_1903_01081_b200 import engine
+
+pytestmark = pytest.mark.gpu
+
+# cases whose sources are all DC (omega == 0): no libm/CUDA cos difference possible
+BITWISE = {"rc_discharge", "switched_dc_w3", "control_only", "diverging", "singular_islands"}
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_engine_matches_golden(name):
+    g = load_golden(name)
+    if g.error_code:
+        with pytest.raises(engine.EmtError) as ei:
+            engine.interpret(g.schedule, g.initial, g.steps)
+        assert ei.value.status == g.error_code
+        # same location as the reference: "row k" / "node index k"
+        where = g.error_msg.split("|where=")[-1]
+        assert where in ei.value.detail
+        return
+    stats = engine.ExecStats()
+    w = engine.interpret(g.schedule, g.initial, g.steps, engine.ExecOptions(stats=stats))
+    assert within_tolerance(w.values, g.waves), (name, np.max(np.abs(w.values - g.waves)))
+    if name in BITWISE:
+        assert bitwise_equal(w.values, g.waves), name
+    assert bitwise_equal(w.time, g.time)
+    assert stats.factor_count == g.factor_count
+
+
+@pytest.mark.parametrize("name", ["switched_rc", "ieee39_n1_w8", "switched_dc_w3"])
+def test_switch_events_bit_exact(name):
+    g = load_golden(name)
+    ref_run = oracle.Schedule(g.schedule).interpret(g.initial, g.steps)
+    eng = engine.Engine(g.schedule, g.initial)
+    eng.reserve(g.steps)
+    eng.advance(g.steps, sync=True)
+    ev = eng.events()
+    assert np.array_equal(ev, ref_run.events)
+    assert eng.stats().factor_count == ref_run.factor_count
+
+
+def test_chunked_advance_equals_one_shot():
+    g = load_golden("feeder")
+    one = engine.interpret(g.schedule, g.initial, 600)
+    eng = engine.Engine(g.schedule, g.initial)
+    eng.reserve(600)
+    for n in (1, 99, 200, 300):
+        eng.advance(n)
+    w = eng.waves()
+    assert bitwise_equal(w.values, one.values)
+    assert bitwise_equal(w.time, one.time)
+
+
+def test_final_state_matches_oracle_arena():
+    g = load_golden("switched_dc_w3")
+    ref_run = oracle.Schedule(g.schedule).interpret(g.initial, g.steps)
+    eng = engine.Engine(g.schedule, g.initial)
+    eng.reserve(g.steps)
+    eng.advance(g.steps, sync=True)
+    assert bitwise_equal(eng.state(), ref_run.final_arena)
+
+
+def test_lane_sharding_equals_full_batch():
+    g = load_golden("feeder_w4")
+    full = engine.interpret(g.schedule, g.initial, 200)
+    for begin, count in ((0, 2), (2, 2), (1, 3)):
+        eng = engine.Engine(g.schedule, g.initial, lane_begin=begin, lane_count=count)
+        eng.reserve(200)
+        eng.advance(200)
+        part = eng.waves()
+        for j in range(count):
+            assert bitwise_equal(part.lane(j).values, full.lane(begin + j).values)
+
+
+def test_lanes_per_block_variants_agree():
+    g = load_golden("ieee39_n1_w8")
+    base = engine.interpret(g.schedule, g.initial, 400)
+    for lpb in (1, 3, 8):
+        eng = engine.Engine(g.schedule, g.initial, lanes_per_block=lpb)
+        eng.reserve(400)
+        eng.advance(400)
+        assert bitwise_equal(eng.waves().values, base.values)
