@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: IEEE-39 N-1 contingency sweep (BASELINE.json metric, config C3).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: 1000 scenarios (46 breakers x 22 fault times 0.10-0.31 s, first 1000,
+outage-major; cases.n1_scenarios) of the synthetic IEEE 39-bus EMT case
+(n = 85 nodes, m = 149 components, dt = 50 us), sharded contiguously over the
+N GPUs (one process per GPU under torchrun). One bench "step" = one launch of
+the persistent step-loop kernel advancing every scenario by `--emt-steps`
+(default 1000) EMT passes, i.e. 50 ms of simulated time; the default K + W
+covers 1.15 s of simulated time.
+
+value = total scenario-steps / max-over-ranks device time of the K timed
+launches (CUDA events on the engine's stream, L2 flushed between launches).
+e2e   = the same metric through the C ABI with HOST buffers: engine create
+(H2D of arena + constants + tables), advance, waveform D2H, per step.
+The reference arm (--impl reference) runs the reference library
+(oracle/_ref/libemtref.so, emtgrid::interpret) over lane shards on all host
+cores, as BASELINE.md §2 prescribes.
+"""
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DATA = os.path.join(ROOT, "paper_1903_01081_b200", "data")
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def load_case(name="ieee39"):
+    from paper_1903_01081_b200 import schedule as sch
+    s = gzip.open(os.path.join(DATA, f"{name}.cgmsched.gz"), "rt").read()
+    st, _ = sch.parse_state(gzip.open(os.path.join(DATA, f"{name}.state.gz"), "rt").read())
+    ids = json.load(open(os.path.join(DATA, f"{name}.json")))["component_ids"]
+    return s, st, ids
+
+
+def build_batch(scenarios: int):
+    from paper_1903_01081_b200 import cases
+    from paper_1903_01081_b200 import schedule as sch
+    s, st, ids = load_case("ieee39")
+    scen = [(f"sw{b:02d}", tf) for b, tf in cases.n1_scenarios(scenarios)]
+    return sch.n1_batch(s, st, ids, scen), sch.parse_info(s)
+
+
+def algorithmic_bytes_per_scenario_step(info, batch) -> int:
+    """B = 8 [2 (n + m + S_blk + 2 N_sw + N_latch) + F_lane + C_var + K]."""
+    text = batch.schedule
+    lines = text.splitlines()
+    mat = next(l for l in lines if l.startswith("MATRIX")).split()
+    lnnz = int(mat[3].split("=")[1])
+    unnz = int(mat[4].split("=")[1])
+    n_sw = sum(1 for p in info.procs if p.code == 7)
+    s_blk = sum(p.state_len for p in info.procs if p.kind >= 4)
+    n_latch = sum(1 for l in lines if l.startswith("LATCH"))
+    ct = batch.const_table
+    c_var = int(np.sum(np.any(ct != ct[:, :1], axis=1)))
+    k = len(info.channels)
+    return 8 * (2 * (info.nodes + info.comps + s_blk + 2 * n_sw + n_latch) + (lnnz + unnz) + c_var + k)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for ln in open(self.path):
+                f = [x.strip() for x in ln.split(",")]
+                if len(f) >= 9:
+                    rows.append(f)
+        except OSError:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        load = [x for x in sm if x > 0.5 * (max(smax) if smax else 1)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)  # 256 MiB write > 126 MB L2
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1903_01081_b200 import engine
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = local
+
+    batch, info = build_batch(args.scenarios)
+    W = batch.width
+    lo = rank * W // world
+    hi = (rank + 1) * W // world
+    S = args.emt_steps
+    total_steps = (args.warmup + args.steps) * S
+
+    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=W, device=dev,
+                        lane_begin=lo, lane_count=hi - lo)
+    eng.reserve(total_steps)
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        eng.advance(S)
+    eng.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(dev) as clocks:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush_l2(torch, flush)
+                starts[k].record(stream)
+            eng.advance(S)
+            ends[k].record(stream)
+        eng.sync()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per_launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    local_ms = sum(per_launch_ms)
+    st = eng.stats()
+
+    # ---- e2e through the C ABI with host buffers (create/H2D, advance, D2H), rank-local shard
+    e2e_steps = max(1, min(3, args.steps))
+    host_waves = np.zeros((S, len(info.channels) * (hi - lo)))
+    ct_host = np.ascontiguousarray(batch.const_table)
+    init_host = np.ascontiguousarray(batch.initial)
+    e2e_s = []
+    for k in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=W, device=dev, lane_begin=lo,
+                           lane_count=hi - lo)
+        e2.reserve(S)
+        e2.advance(S)
+        w = e2.waves(0, S)
+        host_waves[:] = w.values
+        e2.close()
+        t1 = time.perf_counter()
+        if k > 0:  # first call warms the module / allocator
+            e2e_s.append(t1 - t0)
+    e2e_local = statistics.median(e2e_s)
+
+    if world > 1:
+        t = torch.tensor([local_ms, e2e_local, float(st.factor_count)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms, e2e_max, fc = t.tolist()
+        # final result gather: per-rank waveform checksums (the only inter-GPU traffic)
+        chk = torch.tensor([float(np.sum(host_waves))], dtype=torch.float64, device=dev)
+        gathered = [torch.zeros_like(chk) for _ in range(world)]
+        dist.all_gather(gathered, chk)
+    else:
+        max_ms, e2e_max, fc = local_ms, e2e_local, float(st.factor_count)
+
+    scen_steps = W * S * args.steps
+    value = scen_steps / (max_ms * 1e-3)
+    clk = clocks.summary()
+    if rank == 0:
+        peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+        peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
+        bytes_per = algorithmic_bytes_per_scenario_step(info, batch)
+        avg_launch_s = (local_ms / args.steps) * 1e-3
+        lanes_local = hi - lo
+        achieved = bytes_per * lanes_local * S / avg_launch_s / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
+        h2d = (batch.const_table[:, lo:hi].nbytes + info.extent * (hi - lo) * 8) / S
+        d2h = len(info.channels) * (hi - lo) * 8
+        out = {
+            "metric": "scenario-steps/sec for N-1 EMT batch",
+            "value": value,
+            "unit": "scenario-steps/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W,
+                       "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
+                       "components": info.comps, "case": "ieee39-synthetic (cases.py)",
+                       "parallelism": f"scenario lanes sharded over {world} GPU(s), no per-step traffic",
+                       "l2": "flushed (256 MiB write) between timed launches"},
+            "e2e": {"value": W * S / e2e_max, "unit": "scenario-steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "note": "engine create + H2D, advance, waveform D2H per call"},
+            "gpu_launches": args.steps,
+            "kernel": "emt_step_kernel (persistent, warp per scenario lane)",
+            "factor_count": int(fc),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_scenario_step": bytes_per,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "clocks": clk,
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- reference (CPU) arm
+
+def _ref_worker(args_tuple):
+    text, init, steps, warmup = args_tuple
+    from oracle import ref
+    r = ref.execute(text, init, warmup + steps, warmup=warmup)
+    return r.measured_seconds  # step loop after warm-up (ExecStats, proj/src/exec.cpp:375-381)
+
+
+def _shard(batch, lo, hi):
+    from paper_1903_01081_b200 import schedule as sch
+    ct = batch.const_table[:, lo:hi]
+    ext = batch.initial.size // batch.width
+    init = batch.initial.reshape(ext, batch.width)[:, lo:hi].reshape(-1)
+    return sch.widen_text(batch.schedule, ct), np.ascontiguousarray(init)
+
+
+def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: int):
+    """emtgrid::interpret (the reference, unmodified) on contiguous lane shards, one
+    process per host core; returns (lanes, max step-loop seconds)."""
+    import multiprocessing as mp
+    batch, info = build_batch(scenarios)
+    W = batch.width
+    procs = max(1, min(procs, W))
+    bounds = [(p * W // procs, (p + 1) * W // procs) for p in range(procs)]
+    jobs = []
+    for lo, hi in bounds:
+        text, init = _shard(batch, lo, hi)
+        jobs.append((text, init, emt_steps, warmup_emt))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_ref_worker, jobs)
+    return W, max(res), procs
+
+
+def cpu_baseline(args):
+    steps = args.cpu_emt_steps
+    W, secs, procs = reference_measure(args.scenarios, steps, 20, os.cpu_count() or 1)
+    return {"value": W * steps / secs, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
+            "sample": f"{W} scenarios x {steps} EMT steps (after 20 warm-up), emtgrid::interpret on "
+                      f"{procs} contiguous lane shards, one process per core (oracle/_ref/libemtref.so)"}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    S = args.cpu_emt_steps_per_step
+    W, secs, procs = reference_measure(args.scenarios, S * args.steps, S * args.warmup, os.cpu_count() or 1)
+    value = W * S * args.steps / secs
+    out = {
+        "impl": "reference",
+        "metric": "scenario-steps/sec for N-1 EMT batch",
+        "value": value, "unit": "scenario-steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "emt_steps_per_bench_step": S,
+                   "parallelism": f"{procs} host processes over contiguous lane shards"},
+        "cpu_baseline": {"value": value, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
+                         "sample": f"{W} scenarios x {S} EMT steps per bench step "
+                                   f"({args.warmup} warm-up + {args.steps} timed), emtgrid::interpret"},
+        "e2e": {"value": value, "unit": "scenario-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scenarios", type=int, default=1000)
+    ap.add_argument("--emt-steps", type=int, default=1000, help="EMT passes per bench step (one launch)")
+    ap.add_argument("--cpu-emt-steps", type=int, default=8000, help="EMT passes in the cpu_baseline sample")
+    ap.add_argument("--cpu-emt-steps-per-step", type=int, default=200,
+                    help="EMT passes per bench step in the reference arm")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
