@@ -53,10 +53,18 @@ typedef struct emt_config {
     int32_t device;          /* CUDA device ordinal */
     int32_t lane_begin;      /* first scenario lane this engine owns (multi-GPU shard) */
     int32_t lane_count;      /* lanes owned; 0 = all lanes from lane_begin */
-    int32_t lanes_per_block; /* 0 = auto (one CTA per SM when the batch allows) */
-    int32_t threads_per_lane;/* 0 = auto (32: one warp per scenario lane) */
-    int32_t reserved[3];
+    int32_t lanes_per_block; /* generic kernel: warps (= lanes) per CTA, 0 = auto */
+    int32_t warps_per_group; /* specialised kernel: warps sharing one 32-lane group, 0 = auto (4) */
+    int32_t kernel;          /* EMT_KERNEL_AUTO / _SPECIALISED / _GENERIC */
+    int32_t reserved[2];
 } emt_config;
+
+/* Step-loop kernel selection. AUTO generates and JIT-compiles (NVRTC) a kernel
+ * specialised to the schedule — the code generator of the reference's
+ * emit_source (proj/src/codegen.cpp:84-230) retargeted to sm_100a — and uses
+ * the table-driven generic kernel only when the specialised one cannot be
+ * built (e.g. the hot arena exceeds shared memory). Both run on the GPU. */
+enum { EMT_KERNEL_AUTO = 0, EMT_KERNEL_SPECIALISED = 1, EMT_KERNEL_GENERIC = 2 };
 
 /* ExecOptions (proj/include/emtgrid/exec.hpp:17-25). */
 typedef struct emt_exec_options {
@@ -140,6 +148,20 @@ emt_status emt_engine_stats(emt_engine* engine, emt_exec_stats* stats);
  * and the CUDA stream the engine launches on (cudaStream_t as void*). */
 void* emt_engine_device_waves(emt_engine* engine);
 void* emt_engine_stream(emt_engine* engine);
+
+/* Which kernel the engine runs (EMT_KERNEL_SPECIALISED or _GENERIC), the
+ * generated CUDA source (empty for the generic kernel) and a one-line plan
+ * summary (tasks, phases, shared-memory bytes, JIT time). */
+int32_t emt_engine_kernel(const emt_engine* engine);
+const char* emt_engine_source(const emt_engine* engine);
+const char* emt_engine_summary(const emt_engine* engine);
+
+/* Generates the specialised kernel source for a schedule without touching a
+ * device and, when `compile` != 0, compiles it with NVRTC for `arch`
+ * (e.g. "sm_100a"). Returned strings stay valid until the next call on this
+ * thread. Used by the build check and the CPU test-suite. */
+emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,
+                       int32_t compile, const char* arch, const char** source, const char** summary);
 
 /* Library build string (arch, flags). */
 const char* emt_version(void);

@@ -12,8 +12,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libemtb200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_schedule.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", "host_schedule.hpp"), os.path.join(ROOT, "include", "emt_b200.h")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_schedule.cpp", "codegen.cpp", "jit.cpp")]
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("host_schedule.hpp", "codegen.hpp", "jit.hpp")] + [
+    os.path.join(ROOT, "include", "emt_b200.h")]
+CUDA = "/usr/local/cuda"
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -22,6 +24,8 @@ NVCC_FLAGS = [
     "-std=c++17",
     "-ccbin", "/usr/bin/g++",  # system libstdc++ (dynamic), same as the Python process
     "-Xcompiler", "-fPIC", "-shared",
+    # NVRTC (runtime code generation); driver entry points come via cudaGetDriverEntryPoint
+    f"-L{CUDA}/lib64", "-lnvrtc", f"-Xlinker=-rpath,{CUDA}/lib64",
 ]
 
 

@@ -1,0 +1,42 @@
+// Schedule -> specialised sm_100a kernel source (the code generator of
+// SURVEY.md §8(f).1; the reference's C++ emitter is proj/src/codegen.cpp:84-230).
+//
+// The generated kernel runs 32 scenario lanes per CTA, one lane per thread
+// (SIMT over scenarios: every thread executes the same straight-line code on
+// its own lane's state), and splits the per-step work of those lanes across
+// `warps` warps (warp-specialised partitions separated by CTA barriers).
+// Every arena slot index, every lane-invariant constant and every sparse-LU
+// index is baked into the instruction stream as an immediate.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "host_schedule.hpp"
+
+namespace emtb200 {
+
+struct CodegenOptions {
+    int warps = 4;                  // warps per CTA (work partitions of one 32-lane group)
+    size_t smem_budget = 227 * 1024;  // bytes of dynamic shared memory per CTA
+    bool lu_in_smem = true;         // keep L/U factors on chip when they fit
+};
+
+struct GeneratedKernel {
+    std::string source;
+    std::string name = "emt_cg_kernel";
+    int warps = 4;
+    size_t smem_bytes = 0;
+    int hot_slots = 0;      // arena slots resident in shared memory
+    int lu_smem = 0;        // 1 when L/U live in shared memory
+    int phases_a = 0, phases_b = 0;
+    int tasks = 0;
+    std::string summary;
+};
+
+/// `ctab` = consts x lanes constant table of the engine's lanes (slot-major);
+/// a constant slot equal across all lanes becomes an immediate.
+bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
+                     GeneratedKernel& out, Failure& fail);
+
+}  // namespace emtb200

@@ -26,7 +26,9 @@
 #include <vector>
 
 #include "../../include/emt_b200.h"
+#include "codegen.hpp"
 #include "host_schedule.hpp"
+#include "jit.hpp"
 
 namespace emtb200 {
 
@@ -36,6 +38,20 @@ constexpr double kDefaultDivergence = 1e12;  // kDivergenceLimit, kernels.hpp:24
 // Per-lane error record in global memory: code (1+ErrorCode), step, index.
 struct LaneError {
     int code, step, index, layer;
+};
+
+// Argument block of the generated kernel (layout mirrored in codegen.cpp).
+struct CgArgs {
+    double* arena;
+    const double* ctab;
+    double* waves;
+    unsigned char* refac;
+    int* lane_err;
+    int* events;
+    int* n_events;
+    int max_events;
+    int step0, nsteps, row0;
+    double div_limit;
 };
 
 struct DevPlan {
@@ -427,11 +443,17 @@ struct emt_engine {
     int failed = 0;
     int max_events = 1 << 16;
     double divergence_limit = kDefaultDivergence;
+    std::vector<double> host_ctab;       // consts x W (this engine's lanes)
+    int kernel_mode = EMT_KERNEL_GENERIC;
+    GeneratedKernel gen;
+    JitModule jit;
+    std::string summary;
     std::vector<double> initial_fcount;  // per owned lane, from the initial arena
     int base_factor_count = 0;           // global lane 0's initial fcount (ExecStats, exec.cpp:376)
 
     ~emt_engine() {
         if (device >= 0) cudaSetDevice(device);
+        if (jit.module && driver()) driver()->ModuleUnload(jit.module);
         for (void* p : allocations) cudaFree(p);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
@@ -559,6 +581,7 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
         for (int l = 0; l < W; ++l)
             arena[static_cast<size_t>(k) * W + l] =
                 initial[static_cast<size_t>(k) * width + static_cast<size_t>(e->lane_begin + l)];
+    e->host_ctab = ctab;
     e->initial_fcount.resize(static_cast<size_t>(W));
     for (int l = 0; l < W; ++l) e->initial_fcount[static_cast<size_t>(l)] = arena[static_cast<size_t>(s.fcount) * W + l];
     e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
@@ -680,6 +703,40 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         CUDA_TRY(cudaFuncSetAttribute(emt_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(e->smem_bytes)));
     }
+    e->kernel_mode = EMT_KERNEL_GENERIC;
+    e->summary = "generic table-driven kernel, grid=" + std::to_string(e->grid) + " block=" + std::to_string(e->block);
+    if (c.kernel != EMT_KERNEL_GENERIC) {
+        CodegenOptions opt;
+        opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 4;
+        int dev_smem = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+        opt.smem_budget = static_cast<size_t>(dev_smem);
+        Failure gf;
+        std::string log;
+        const auto t0 = std::chrono::steady_clock::now();
+        bool ok = generate_kernel(e->sched, e->host_ctab, e->W, opt, e->gen, gf);
+        const double gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (ok) ok = jit_load(e->gen.source, e->gen.name, e->device, e->jit, log);
+        if (ok) {
+            if (driver()->FuncSetAttribute(e->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                           static_cast<int>(e->gen.smem_bytes)) != CUDA_SUCCESS) {
+                ok = false;
+                log = "cuFuncSetAttribute(max dynamic smem) failed";
+            }
+        }
+        if (ok) {
+            e->kernel_mode = EMT_KERNEL_SPECIALISED;
+            char b[160];
+            std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s", gen_s, e->jit.compile_seconds,
+                          e->jit.cached ? " (cached)" : "");
+            e->summary = "specialised kernel: " + e->gen.summary + b;
+        } else if (c.kernel == EMT_KERNEL_SPECIALISED) {
+            return set_error(gf.code ? gf.code : EMT_CUDA_ERROR,
+                             "specialised kernel unavailable: " + (gf.message.empty() ? log : gf.message));
+        } else {
+            e->summary += " (specialised kernel unavailable: " + (gf.message.empty() ? log.substr(0, 300) : gf.message) + ")";
+        }
+    }
     *out = e.release();
     return EMT_OK;
 }
@@ -730,11 +787,26 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
     if (e->rows + steps > e->capacity)
         return set_error(EMT_CAPACITY_EXCEEDED, "waveform store holds " + std::to_string(e->capacity) + " rows");
     CUDA_TRY(cudaSetDevice(e->device));
-    DevPlan P = e->plan;
-    P.waves = e->d_waves;
-    P.refactored = e->d_refactored;
-    emt_step_kernel<<<e->grid, e->block, e->smem_bytes, e->stream>>>(P, e->step, steps, e->rows);
-    CUDA_TRY(cudaGetLastError());
+    if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
+        CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
+                 e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit};
+        void* params[] = {&a};
+        const unsigned grid = static_cast<unsigned>((e->W + 31) / 32);
+        const CUresult r = driver()->LaunchKernel(e->jit.function, grid, 1, 1, static_cast<unsigned>(32 * e->gen.warps), 1, 1,
+                                          static_cast<unsigned>(e->gen.smem_bytes), reinterpret_cast<CUstream>(e->stream),
+                                          params, nullptr);
+        if (r != CUDA_SUCCESS) {
+            const char* msg = nullptr;
+            driver()->GetErrorString(r, &msg);
+            return set_error(EMT_CUDA_ERROR, std::string("cuLaunchKernel: ") + (msg ? msg : "?"));
+        }
+    } else {
+        DevPlan P = e->plan;
+        P.waves = e->d_waves;
+        P.refactored = e->d_refactored;
+        emt_step_kernel<<<e->grid, e->block, e->smem_bytes, e->stream>>>(P, e->step, steps, e->rows);
+        CUDA_TRY(cudaGetLastError());
+    }
     e->launches += 1;
     e->step += steps;
     e->rows += steps;
@@ -820,6 +892,44 @@ emt_status emt_engine_stats(emt_engine* e, emt_exec_stats* stats) {
     stats->kernel_launches = e->launches;
     return EMT_OK;
 }
+
+emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,
+                       int32_t compile, const char* arch, const char** source, const char** summary) {
+    thread_local std::string src_out, sum_out;
+    Schedule s;
+    Failure f;
+    if (schedule_text == nullptr || !parse_schedule(schedule_text, s, f))
+        return set_error(f.code ? f.code : EMT_INVALID_HANDLE, f.where + ": " + f.message);
+    lu_symbolic(s);
+    if (width <= 0) width = s.width;
+    if (const_table == nullptr && width != s.width) return set_error(EMT_DIMENSION_MISMATCH, "width without const table");
+    std::vector<double> ct(const_table ? const_table : s.const_table.data(),
+                           (const_table ? const_table : s.const_table.data()) + static_cast<size_t>(s.consts) * width);
+    CodegenOptions opt;
+    opt.warps = warps > 0 ? warps : 4;
+    GeneratedKernel g;
+    if (!generate_kernel(s, ct, width, opt, g, f)) return set_error(f.code, f.message);
+    src_out = g.source;
+    sum_out = g.summary;
+    if (compile) {
+        std::vector<char> cubin;
+        std::string log;
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!jit_compile(g.source, arch ? arch : "sm_100a", cubin, log))
+            return set_error(EMT_CUDA_ERROR, "NVRTC: " + log.substr(0, 4000));
+        char b[96];
+        std::snprintf(b, sizeof b, " nvrtc=%.3fs cubin=%zuB", std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(),
+                      cubin.size());
+        sum_out += b;
+    }
+    if (source) *source = src_out.c_str();
+    if (summary) *summary = sum_out.c_str();
+    return EMT_OK;
+}
+
+int32_t emt_engine_kernel(const emt_engine* e) { return e ? e->kernel_mode : 0; }
+const char* emt_engine_source(const emt_engine* e) { return e ? e->gen.source.c_str() : ""; }
+const char* emt_engine_summary(const emt_engine* e) { return e ? e->summary.c_str() : ""; }
 
 void* emt_engine_device_waves(emt_engine* e) { return e ? e->d_waves : nullptr; }
 void* emt_engine_stream(emt_engine* e) { return e ? e->stream : nullptr; }

@@ -48,8 +48,11 @@ class EmtError(RuntimeError):
 
 class _Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("lane_begin", ctypes.c_int32), ("lane_count", ctypes.c_int32),
-                ("lanes_per_block", ctypes.c_int32), ("threads_per_lane", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("lanes_per_block", ctypes.c_int32), ("warps_per_group", ctypes.c_int32),
+                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+
+
+KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC = 0, 1, 2
 
 
 class _Options(ctypes.Structure):
@@ -105,6 +108,14 @@ def lib():
         L.emt_engine_device_waves.restype = vp
         L.emt_engine_stream.argtypes = [vp]
         L.emt_engine_stream.restype = vp
+        L.emt_engine_kernel.argtypes = [vp]
+        L.emt_engine_kernel.restype = ctypes.c_int32
+        L.emt_engine_source.argtypes = [vp]
+        L.emt_engine_source.restype = ctypes.c_char_p
+        L.emt_engine_summary.argtypes = [vp]
+        L.emt_engine_summary.restype = ctypes.c_char_p
+        L.emt_codegen.argtypes = [ctypes.c_char_p, dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                  ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_char_p)]
         _lib = L
     return _lib
 
@@ -113,7 +124,8 @@ EXPORTED_SYMBOLS = [
     "emt_interpret", "emt_last_error", "emt_engine_create", "emt_engine_destroy", "emt_engine_shape",
     "emt_engine_reserve", "emt_engine_advance", "emt_engine_sync", "emt_engine_read_waves",
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
-    "emt_engine_stream", "emt_version",
+    "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
+    "emt_codegen",
 ]
 
 
@@ -180,14 +192,27 @@ class WaveformSet:
         return "\n".join(lines) + "\n"
 
 
-def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per_block: int = 0) -> _Config:
+def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per_block: int = 0,
+            warps: int = 0, kernel: int = KERNEL_AUTO) -> _Config:
     c = _Config()
     c.device, c.lane_begin, c.lane_count, c.lanes_per_block = device, lane_begin, lane_count, lanes_per_block
+    c.warps_per_group, c.kernel = warps, kernel
     return c
 
 
+def codegen(schedule: str, const_table: Optional[np.ndarray] = None, width: int = 0, warps: int = 4,
+            compile: bool = False, arch: str = "sm_100a"):
+    """Generated kernel source + plan summary for a schedule (no GPU needed)."""
+    L = lib()
+    ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
+    src, summ = ctypes.c_char_p(), ctypes.c_char_p()
+    _check(L.emt_codegen(schedule.encode(), _dp(ct) if ct is not None else None, int(width), int(warps),
+                         1 if compile else 0, arch.encode(), ctypes.byref(src), ctypes.byref(summ)))
+    return src.value.decode(), summ.value.decode()
+
+
 def interpret(schedule: str, initial: np.ndarray, steps: int, options: Optional[ExecOptions] = None,
-              device: int = 0) -> WaveformSet:
+              device: int = 0, kernel: int = KERNEL_AUTO, warps: int = 0) -> WaveformSet:
     """Drop-in for emtgrid::interpret on the B200 (one-shot: upload, run, download)."""
     L = lib()
     init = np.ascontiguousarray(initial, dtype=np.float64)
@@ -199,7 +224,7 @@ def interpret(schedule: str, initial: np.ndarray, steps: int, options: Optional[
     opt.divergence_limit = options.divergence_limit if options else 1e12
     opt.warmup_steps = options.warmup_steps if options else 0
     st = _Stats()
-    cfg = _config(device)
+    cfg = _config(device, warps=warps, kernel=kernel)
     _check(L.emt_interpret(schedule.encode(), _dp(init), init.size, steps, ctypes.byref(opt), ctypes.byref(cfg),
                            _dp(waves), _dp(time), ctypes.byref(st)))
     if options is not None and options.stats is not None:
@@ -223,12 +248,12 @@ class Engine:
 
     def __init__(self, schedule: str, initial: np.ndarray, const_table: Optional[np.ndarray] = None,
                  width: int = 0, device: int = 0, lane_begin: int = 0, lane_count: int = 0,
-                 lanes_per_block: int = 0):
+                 lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO):
         L = lib()
         self._h = ctypes.c_void_p()
         init = np.ascontiguousarray(initial, dtype=np.float64)
         ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
-        cfg = _config(device, lane_begin, lane_count, lanes_per_block)
+        cfg = _config(device, lane_begin, lane_count, lanes_per_block, warps, kernel)
         _check(L.emt_engine_create(schedule.encode(), _dp(ct) if ct is not None else None, int(width), _dp(init),
                                    init.size, ctypes.byref(cfg), ctypes.byref(self._h)))
         vals = [ctypes.c_int32() for _ in range(9)]
@@ -284,6 +309,18 @@ class Engine:
         _check(lib().emt_engine_stats(self._h, ctypes.byref(st)))
         return ExecStats(st.factor_count, st.measured_seconds, st.measured_steps, st.kernel_launches,
                          st.switch_events)
+
+    @property
+    def kernel(self) -> int:
+        return int(lib().emt_engine_kernel(self._h))
+
+    @property
+    def summary(self) -> str:
+        return lib().emt_engine_summary(self._h).decode()
+
+    @property
+    def source(self) -> str:
+        return lib().emt_engine_source(self._h).decode()
 
     def device_waves_ptr(self) -> int:
         return int(lib().emt_engine_device_waves(self._h) or 0)

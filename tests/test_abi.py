@@ -35,3 +35,20 @@ def test_library_is_sm100a_native():
 
 def test_version_string():
     assert b"sm_100a" in engine.lib().emt_version()
+
+
+def test_codegen_generates_for_every_golden_schedule():
+    from conftest import GOLDEN_CASES, load_golden
+    for name in GOLDEN_CASES:
+        g = load_golden(name)
+        src, summary = engine.codegen(g.schedule, warps=4)
+        assert "emt_cg_kernel" in src and "tasks=" in summary, name
+
+
+def test_codegen_nvrtc_compiles_sm100a():
+    """NVRTC compiles the generated kernels for sm_100a (no device needed)."""
+    from conftest import load_golden
+    for name in ("cyclic_controls", "switched_dc_w3"):
+        g = load_golden(name)
+        src, summary = engine.codegen(g.schedule, warps=4, compile=True)
+        assert "nvrtc=" in summary and "cubin=" in summary

@@ -17,19 +17,24 @@ pytestmark = pytest.mark.gpu
 BITWISE = {"rc_discharge", "switched_dc_w3", "control_only", "diverging", "singular_islands"}
 
 
+KERNELS = {"specialised": engine.KERNEL_SPECIALISED, "generic": engine.KERNEL_GENERIC}
+
+
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
 @pytest.mark.parametrize("name", GOLDEN_CASES)
-def test_engine_matches_golden(name):
+def test_engine_matches_golden(name, kernel):
     g = load_golden(name)
+    k = KERNELS[kernel]
     if g.error_code:
         with pytest.raises(engine.EmtError) as ei:
-            engine.interpret(g.schedule, g.initial, g.steps)
+            engine.interpret(g.schedule, g.initial, g.steps, kernel=k)
         assert ei.value.status == g.error_code
         # same location as the reference: "row k" / "node index k"
         where = g.error_msg.split("|where=")[-1]
         assert where in ei.value.detail
         return
     stats = engine.ExecStats()
-    w = engine.interpret(g.schedule, g.initial, g.steps, engine.ExecOptions(stats=stats))
+    w = engine.interpret(g.schedule, g.initial, g.steps, engine.ExecOptions(stats=stats), kernel=k)
     assert within_tolerance(w.values, g.waves), (name, np.max(np.abs(w.values - g.waves)))
     if name in BITWISE:
         assert bitwise_equal(w.values, g.waves), name
@@ -37,11 +42,12 @@ def test_engine_matches_golden(name):
     assert stats.factor_count == g.factor_count
 
 
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
 @pytest.mark.parametrize("name", ["switched_rc", "ieee39_n1_w8", "switched_dc_w3"])
-def test_switch_events_bit_exact(name):
+def test_switch_events_bit_exact(name, kernel):
     g = load_golden(name)
     ref_run = oracle.Schedule(g.schedule).interpret(g.initial, g.steps)
-    eng = engine.Engine(g.schedule, g.initial)
+    eng = engine.Engine(g.schedule, g.initial, kernel=KERNELS[kernel])
     eng.reserve(g.steps)
     eng.advance(g.steps, sync=True)
     ev = eng.events()
@@ -49,10 +55,11 @@ def test_switch_events_bit_exact(name):
     assert eng.stats().factor_count == ref_run.factor_count
 
 
-def test_chunked_advance_equals_one_shot():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_chunked_advance_equals_one_shot(kernel):
     g = load_golden("feeder")
-    one = engine.interpret(g.schedule, g.initial, 600)
-    eng = engine.Engine(g.schedule, g.initial)
+    one = engine.interpret(g.schedule, g.initial, 600, kernel=KERNELS[kernel])
+    eng = engine.Engine(g.schedule, g.initial, kernel=KERNELS[kernel])
     eng.reserve(600)
     for n in (1, 99, 200, 300):
         eng.advance(n)
@@ -61,20 +68,23 @@ def test_chunked_advance_equals_one_shot():
     assert bitwise_equal(w.time, one.time)
 
 
-def test_final_state_matches_oracle_arena():
-    g = load_golden("switched_dc_w3")
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+@pytest.mark.parametrize("name", ["switched_dc_w3", "control_only", "rc_discharge"])
+def test_final_state_matches_oracle_arena(name, kernel):
+    g = load_golden(name)
     ref_run = oracle.Schedule(g.schedule).interpret(g.initial, g.steps)
-    eng = engine.Engine(g.schedule, g.initial)
+    eng = engine.Engine(g.schedule, g.initial, kernel=KERNELS[kernel])
     eng.reserve(g.steps)
     eng.advance(g.steps, sync=True)
     assert bitwise_equal(eng.state(), ref_run.final_arena)
 
 
-def test_lane_sharding_equals_full_batch():
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_lane_sharding_equals_full_batch(kernel):
     g = load_golden("feeder_w4")
-    full = engine.interpret(g.schedule, g.initial, 200)
+    full = engine.interpret(g.schedule, g.initial, 200, kernel=KERNELS[kernel])
     for begin, count in ((0, 2), (2, 2), (1, 3)):
-        eng = engine.Engine(g.schedule, g.initial, lane_begin=begin, lane_count=count)
+        eng = engine.Engine(g.schedule, g.initial, lane_begin=begin, lane_count=count, kernel=KERNELS[kernel])
         eng.reserve(200)
         eng.advance(200)
         part = eng.waves()
@@ -86,7 +96,37 @@ def test_lanes_per_block_variants_agree():
     g = load_golden("ieee39_n1_w8")
     base = engine.interpret(g.schedule, g.initial, 400)
     for lpb in (1, 3, 8):
-        eng = engine.Engine(g.schedule, g.initial, lanes_per_block=lpb)
+        eng = engine.Engine(g.schedule, g.initial, lanes_per_block=lpb, kernel=engine.KERNEL_GENERIC)
         eng.reserve(400)
         eng.advance(400)
         assert bitwise_equal(eng.waves().values, base.values)
+    for warps in (1, 2, 3, 8):
+        eng = engine.Engine(g.schedule, g.initial, warps=warps, kernel=engine.KERNEL_SPECIALISED)
+        assert eng.kernel == engine.KERNEL_SPECIALISED
+        eng.reserve(400)
+        eng.advance(400)
+        assert bitwise_equal(eng.waves().values, base.values), warps
+
+
+@pytest.mark.parametrize("name", ["ieee39", "feeder", "ieee39_n1_w8", "cyclic_controls"])
+def test_auto_selects_specialised_kernel(name):
+    g = load_golden(name)
+    eng = engine.Engine(g.schedule, g.initial)
+    assert eng.kernel == engine.KERNEL_SPECIALISED, eng.summary
+    assert "emt_cg_kernel" in eng.source
+
+
+def test_specialised_equals_generic_bitwise_full_n1_sample():
+    """Both device kernels run the same operation order: identical bits on a 64-lane N-1 batch."""
+    import bench
+    batch, info = bench.build_batch(64)
+    out = []
+    for k in (engine.KERNEL_SPECIALISED, engine.KERNEL_GENERIC):
+        eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, kernel=k)
+        eng.reserve(3000)
+        eng.advance(3000)
+        out.append((eng.waves().values, eng.stats().factor_count, eng.events(), eng.state()))
+    assert bitwise_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])
+    assert bitwise_equal(out[0][3], out[1][3])

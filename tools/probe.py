@@ -22,8 +22,11 @@ def load(name):
     return s, st, ids
 
 
-def run(label, schedule, initial, const_table=None, width=0, steps=2000, lpb=0):
-    eng = engine.Engine(schedule, initial, const_table=const_table, width=width, lanes_per_block=lpb)
+def run(label, schedule, initial, const_table=None, width=0, steps=2000, lpb=0, kernel=0, warps=0):
+    t0 = time.perf_counter()
+    eng = engine.Engine(schedule, initial, const_table=const_table, width=width, lanes_per_block=lpb, kernel=kernel,
+                        warps=warps)
+    tc = time.perf_counter() - t0
     eng.reserve(steps + 200)
     eng.advance(200, sync=True)
     t = time.perf_counter()
@@ -31,24 +34,29 @@ def run(label, schedule, initial, const_table=None, width=0, steps=2000, lpb=0):
     dt = time.perf_counter() - t
     W = eng.lanes
     print(f"{label:40s} W={W:5d} {dt / steps * 1e6:8.3f} us/step  {W * steps / dt:.3e} scen-steps/s  "
-          f"fc={eng.stats().factor_count}", flush=True)
+          f"fc={eng.stats().factor_count} create={tc:.2f}s | {eng.summary[:150]}", flush=True)
     return eng
 
 
 def main():
     s, st, ids = load("ieee39")
-    run("ieee39 W=1", s, st)
+    run("ieee39 W=1 generic", s, st, kernel=2)
+    for w in (2, 4, 8):
+        run(f"ieee39 W=1 spec warps={w}", s, st, warps=w)
     scen = cases.n1_scenarios(1000)
     b = sch.n1_batch(s, st, ids, [(f"sw{br:02d}", tf) for br, tf in scen])
-    for lpb in (0, 1, 2, 4, 8):
-        run(f"ieee39 N-1 W=1000 lpb={lpb}", s, b.initial, b.const_table, b.width, lpb=lpb)
+    run("ieee39 N-1 W=1000 generic", s, b.initial, b.const_table, b.width, kernel=2, lpb=8)
+    for w in (2, 4, 8, 16):
+        run(f"ieee39 N-1 W=1000 spec warps={w}", s, b.initial, b.const_table, b.width, warps=w)
     f, fst, _ = load("feeder33_pv3")
-    run("feeder W=1", f, fst)
+    run("feeder W=1 generic", f, fst, kernel=2)
+    run("feeder W=1 spec", f, fst)
     info = sch.parse_info(f)
     for W in (1000, 4096):
         ct = np.repeat(info.const_table, W, axis=1)
         init = np.repeat(fst.reshape(-1, 1), W, axis=1).reshape(-1)
-        run(f"feeder W={W}", f, init, ct, W)
+        for w in (4, 8):
+            run(f"feeder W={W} spec warps={w}", f, init, ct, W, warps=w)
 
 
 if __name__ == "__main__":
