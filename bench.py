@@ -232,8 +232,9 @@ def run_ours(args):
         achieved = bytes_per * lanes_local * S / avg_launch_s / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        if os.path.exists(tp):  # ncu --set full capture of the same kernel (tools/ncu_summary.py), per EMT step
+            per_step = json.load(open(tp)).get("dram_bytes_per_emt_step")
+            traffic = per_step * S * lanes_local / json.load(open(tp)).get("lanes", lanes_local) if per_step else None
         cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
         h2d = (batch.const_table[:, lo:hi].nbytes + info.extent * (hi - lo) * 8) / S
         d2h = len(info.channels) * (hi - lo) * 8
@@ -258,7 +259,7 @@ def run_ours(args):
             "e2e": {"value": W * S / e2e_max, "unit": "scenario-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "note": "engine create + H2D, advance, waveform D2H per call"},
             "gpu_launches": args.steps,
-            "kernel": "emt_step_kernel (persistent, warp per scenario lane)",
+            "kernel": eng.summary[:200],
             "factor_count": int(fc),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -54,7 +54,7 @@ typedef struct emt_config {
     int32_t lane_begin;      /* first scenario lane this engine owns (multi-GPU shard) */
     int32_t lane_count;      /* lanes owned; 0 = all lanes from lane_begin */
     int32_t lanes_per_block; /* generic kernel: warps (= lanes) per CTA, 0 = auto */
-    int32_t warps_per_group; /* specialised kernel: warps sharing one 32-lane group, 0 = auto (4) */
+    int32_t warps_per_group; /* specialised kernel: warps sharing one 32-lane group, 0 = auto (8) */
     int32_t kernel;          /* EMT_KERNEL_AUTO / _SPECIALISED / _GENERIC */
     int32_t reserved[2];
 } emt_config;

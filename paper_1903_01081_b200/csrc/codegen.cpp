@@ -2,19 +2,26 @@
 //
 // Semantics are those of the reference's per-process kernels
 // (Engine::run_proc, /root/reference/proj/src/exec.cpp:77-311, and the
-// code-database templates proj/data/codedb/cpp/*.tpl); the generator turns the
-// schedule's sequential process order into a dependency DAG of fine-grained
-// tasks (one per Norton update, gather node, triangular-solve row, finalize
-// component, control block, channel record, latch), then list-schedules the
-// DAG onto the CTA's warps in barrier-separated phases. Within a task every
-// floating-point operation keeps the reference's order (no FMA contraction:
-// compiled with --fmad=false), so results stay bit-compatible.
+// code-database templates proj/data/codedb/cpp/*.tpl). The generator
+//  1. turns the schedule's sequential process order into a dependency DAG of
+//     fine-grained tasks (one per Norton update, gather node, triangular-solve
+//     row, finalize component, control block, channel record, latch);
+//  2. list-schedules the DAG onto the CTA's warps in barrier-separated phases;
+//  3. emits, per component / block type, one compact loop over a constant-
+//     memory task table (warp-uniform records, one scenario lane per thread),
+//     and a per-warp phase program of (type, table range) segments.
+// Compact loops keep the whole step in the instruction cache (a fully
+// unrolled straight-line variant measured instruction-fetch bound, see
+// profiles/ncu_r1b_cg8.json). Within a task every floating-point operation
+// keeps the reference's order; NVRTC compiles with --fmad=false.
 #include "codegen.hpp"
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <set>
 #include <sstream>
@@ -22,6 +29,11 @@
 namespace emtb200 {
 
 namespace {
+
+int knob(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
 
 std::string lit(double v) {
     if (std::isnan(v) || std::isinf(v)) {
@@ -36,14 +48,29 @@ std::string lit(double v) {
     return b;
 }
 
+// Task kinds of the compact kernel; record strides in ints.
+enum Kind {
+    K_IND, K_CAP, K_SRL, K_VSRC, K_ISRC, K_CSRC, K_SW, K_GATHER, K_FWD, K_BWD, K_FINC, K_FINS,
+    K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_NKINDS
+};
+const char* const kKindName[K_NKINDS] = {"IND", "CAP", "SRL", "VSRC", "ISRC", "CSRC", "SW", "GATHER",
+                                         "FWD", "BWD", "FINC", "FINS", "GAIN", "SUM", "INTEG", "LAG",
+                                         "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH"};
+// kinds whose tasks never depend on another task of the same kind: eligible
+// for the unrolled (loads-first) loop when a segment has no internal edges
+bool unrollable(int k) { return k != K_SW; }
+
 struct Task {
-    std::string code;
-    std::vector<int> reads, writes;  // arena slots (after contrib aliasing)
+    int kind = 0;
+    std::vector<int> f;                      // integer record fields (shared-memory offsets, flags)
+    std::vector<int> ck;                     // constant-table slots of the constant fields
+    std::vector<std::pair<int, int>> terms;  // variable-length operand list
+    std::vector<int> reads, writes;          // arena slots, for dependencies
     int cost = 1;
     int region = 0;  // 0: before FactorizeSystem, 1: after
 };
 
-enum Cls { kNone = 0, kHot, kDerived, kContrib, kSolver, kGlobal };
+enum Cls { kNone = 0, kHot, kDerived, kContrib, kSolver, kChg };
 
 struct Gen {
     const Schedule& s;
@@ -51,14 +78,17 @@ struct Gen {
     int W;
     CodegenOptions opt;
 
-    std::vector<int> cls;           // per arena slot
-    std::vector<std::string> dexpr; // derived constant expression
-    std::vector<int> derived_const; // const slot for derived g (-1: literal 0.0)
+    std::vector<int> cls;            // per arena slot
+    std::vector<int> derived_const;  // derived slot: const slot (or -1: literal 0.0)
     std::vector<int> contrib_h, contrib_sign;
-    std::vector<int> hot_index;
-    std::vector<int> hot_slots;
-    int l_base_smem = -1;  // hot index of L[0] when L/U are in smem
-    int u_base_smem = -1;
+    std::vector<int> hot_index;      // shared-memory slot (index 0 is the constant-0.0 slot)
+    std::vector<int> hot_slots;      // arena slot per shared slot (-1 for the zero slot)
+    int l_base_smem = -1, u_base_smem = -1;
+    std::vector<int> vc_index;       // per const slot: shared slot caching a lane-varying constant, or -1
+    std::vector<int> vc_slots;       // const slot per cached shared slot (in order)
+    int vc_base = 0;                 // first shared slot of the constant cache
+    bool chg_flag = false;           // switch "changed" slots replaced by one per-lane flag
+    std::vector<int> chg_slots;
     std::vector<Task> tasks;
     int fact_layer = 0, solve_layer = 0;
 
@@ -70,64 +100,47 @@ struct Gen {
             if (std::memcmp(&row[l], &row[0], sizeof(double)) != 0) return false;
         return true;
     }
-    std::string C(int k) const {
-        if (invariant(k)) return lit(ct[static_cast<size_t>(k) * W]);
-        return "__ldg(C + " + std::to_string(static_cast<long long>(k) * W) + ")";
-    }
-    std::string R(int slot) const {
-        if (slot < 0) return "(0.0)";
-        switch (cls[static_cast<size_t>(slot)]) {
-            case kDerived: return dexpr[static_cast<size_t>(slot)];
-            case kContrib: {
-                const std::string h = R(contrib_h[static_cast<size_t>(slot)]);
-                return contrib_sign[static_cast<size_t>(slot)] > 0 ? h : "(-" + h + ")";
-            }
-            case kHot: return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]";
-            case kGlobal: return "A[" + std::to_string(static_cast<long long>(slot) * W) + "]";
-            default: return "/*bad slot " + std::to_string(slot) + "*/(0.0)";
-        }
-    }
-    // Writes to global-resident slots from clamped tail threads duplicate lane W-1
-    // bit for bit (same inputs, same instruction), so they need no guard.
-    std::string Wr(int slot) const {
-        if (slot >= 0 && cls[static_cast<size_t>(slot)] == kGlobal)
-            return "A[" + std::to_string(static_cast<long long>(slot) * W) + "]";
-        return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]";
+    double c0(int k) const { return ct[static_cast<size_t>(k) * W]; }
+    /// shared-memory byte offset of an arena slot relative to the lane base
+    int off(int slot) const {
+        if (slot < 0) return 0;  // ground sentinel reads the zero slot
+        if (cls[static_cast<size_t>(slot)] == kDerived && derived_const[static_cast<size_t>(slot)] < 0) return 0;
+        if (hot_index[static_cast<size_t>(slot)] < 0) return 0;  // pass 1 (offsets not assigned yet)
+        return hot_index[static_cast<size_t>(slot)] * 32 * 8;
     }
     int dep_slot(int slot) const {
         if (slot >= 0 && cls[static_cast<size_t>(slot)] == kContrib) return contrib_h[static_cast<size_t>(slot)];
         return slot;
     }
-    std::string Lr(int k) const {
-        if (l_base_smem >= 0) return "S[" + std::to_string((l_base_smem + k) * 32) + "]";
-        return "A[" + std::to_string(static_cast<long long>(s.l + k) * W) + "]";
+    int lu_l(int k) const { return l_base_smem >= 0 ? (l_base_smem + k) * 256 : s.l + k; }
+    int lu_u(int k) const { return u_base_smem >= 0 ? (u_base_smem + k) * 256 : s.u + k; }
+
+    // ---- expressions for the straight-line refactorization
+    std::string C(int k) const {
+        if (invariant(k)) return lit(c0(k));
+        return "__ldg(C + " + std::to_string(static_cast<long long>(k) * W) + ")";
     }
-    std::string Ur(int k) const {
-        if (u_base_smem >= 0) return "S[" + std::to_string((u_base_smem + k) * 32) + "]";
-        return "A[" + std::to_string(static_cast<long long>(s.u + k) * W) + "]";
+    std::string R(int slot) const {
+        if (slot < 0) return "(0.0)";
+        if (cls[static_cast<size_t>(slot)] == kDerived) {
+            const int k = derived_const[static_cast<size_t>(slot)];
+            return k < 0 ? std::string("(0.0)") : C(k);
+        }
+        return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]";
     }
+    std::string Wr(int slot) const { return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]"; }
     std::string Lw(int k, const std::string& v) const {
-        if (l_base_smem >= 0) return Lr(k) + " = " + v + ";";
-        return "if (live) " + Lr(k) + " = " + v + ";";
+        if (l_base_smem >= 0) return "S[" + std::to_string((l_base_smem + k) * 32) + "] = " + v + ";";
+        return "if (live) A[" + std::to_string(static_cast<long long>(s.l + k) * W) + "] = " + v + ";";
     }
     std::string Uw(int k, const std::string& v) const {
-        if (u_base_smem >= 0) return Ur(k) + " = " + v + ";";
-        return "if (live) " + Ur(k) + " = " + v + ";";
-    }
-
-    // kern::source_value (proj/include/emtgrid/kernels.hpp:68-70)
-    std::string source(int kmag, int kom, int kph) const {
-        if (invariant(kom)) {
-            if (ct[static_cast<size_t>(kom) * W] == 0.0) return C(kmag);
-            return "(" + C(kmag) + " * cos(" + C(kom) + " * t + " + C(kph) + "))";
-        }
-        return "((" + C(kom) + ") == 0.0 ? " + C(kmag) + " : " + C(kmag) + " * cos(" + C(kom) + " * t + " + C(kph) + "))";
+        if (u_base_smem >= 0) return "S[" + std::to_string((u_base_smem + k) * 32) + "] = " + v + ";";
+        return "if (live) A[" + std::to_string(static_cast<long long>(s.u + k) * W) + "] = " + v + ";";
     }
 
     void classify() {
         const size_t n = static_cast<size_t>(s.extent);
         cls.assign(n, kNone);
-        dexpr.assign(n, "");
         derived_const.assign(n, -2);
         contrib_h.assign(n, -1);
         contrib_sign.assign(n, 0);
@@ -142,29 +155,23 @@ struct Gen {
         mark_range(s.scratch, s.dim);
         if (s.fcount >= 0) cls[static_cast<size_t>(s.fcount)] = kSolver;
         for (const Proc& p : s.procs) {
-            if (p.code <= kNortonSwitch && p.code != kNortonSwitch && p.out >= 0) {
+            // Norton outputs that are constants every pass (exec.cpp:85-150)
+            if (p.code < kNortonSwitch && p.out >= 0) {
                 cls[static_cast<size_t>(p.out)] = kDerived;
-                if (p.code == kNortonCurrentSource || p.code == kNortonControlledSource) {
-                    dexpr[static_cast<size_t>(p.out)] = "(0.0)";
-                    derived_const[static_cast<size_t>(p.out)] = -1;
-                } else {
-                    dexpr[static_cast<size_t>(p.out)] = C(p.par);
-                    derived_const[static_cast<size_t>(p.out)] = p.par;
-                }
+                derived_const[static_cast<size_t>(p.out)] =
+                    (p.code == kNortonCurrentSource || p.code == kNortonControlledSource) ? -1 : p.par;
             }
             if ((p.code == kNortonResistor || p.code == kNortonSwitch) && p.out2 >= 0) {
                 cls[static_cast<size_t>(p.out2)] = kDerived;
-                dexpr[static_cast<size_t>(p.out2)] = "(0.0)";
                 derived_const[static_cast<size_t>(p.out2)] = -1;
             }
-            if (p.code == kInjectionPair && p.out >= 0 && p.in_count >= 1) {
+            if (p.code == kInjectionPair && p.out >= 0 && p.in_count >= 1) {  // contrib = +-h (exact)
                 const int h = s.port_slot[static_cast<size_t>(p.in_base)];
-                cls[static_cast<size_t>(p.out)] = kContrib;
-                cls[static_cast<size_t>(p.out + 1)] = kContrib;
-                contrib_h[static_cast<size_t>(p.out)] = h;
-                contrib_sign[static_cast<size_t>(p.out)] = 1;
-                contrib_h[static_cast<size_t>(p.out + 1)] = h;
-                contrib_sign[static_cast<size_t>(p.out + 1)] = -1;
+                for (int d = 0; d < 2; ++d) {
+                    cls[static_cast<size_t>(p.out + d)] = kContrib;
+                    contrib_h[static_cast<size_t>(p.out + d)] = h;
+                    contrib_sign[static_cast<size_t>(p.out + d)] = d == 0 ? 1 : -1;
+                }
             }
         }
     }
@@ -174,144 +181,124 @@ struct Gen {
         tasks.push_back(std::move(t));
     }
 
-    std::string sgn(double v) const { return lit(v); }
+    void reads(Task& t, std::initializer_list<int> sl) const {
+        for (int x : sl)
+            if (x >= 0) t.reads.push_back(dep_slot(x));
+    }
 
-    // One non-singleton process: Engine::run_proc cases (exec.cpp:85-309).
+    // One non-singleton process (exec.cpp:85-309) -> task record.
     void emit_proc(const Proc& p, int region) {
         const int* in = s.port_slot.data() + p.in_base;
         const double* sg = s.port_sign.data() + p.in_base;
         auto IN = [&](int j) { return j < p.in_count ? in[j] : -1; };
+        auto NEG = [&](int j) { return sg[j] < 0 ? 1 : 0; };
         Task t;
-        std::ostringstream o;
-        auto reads = [&](std::initializer_list<int> sl) {
-            for (int x : sl)
-                if (x >= 0) t.reads.push_back(dep_slot(x));
-        };
         switch (p.code) {
             case kNortonResistor:
-                return;  // g, h are constants
+            case kInjectionPair:
+                return;  // constants / exact aliases of h
             case kNortonInductor:
             case kNortonCapacitor:
-            case kNortonSeriesRL: {
-                reads({IN(0), IN(1), IN(2)});
-                t.writes.push_back(p.out2);
-                o << "{ const double vs = " << R(IN(1)) << " - " << R(IN(0)) << "; const double g = " << C(p.par) << "; ";
-                if (p.code == kNortonInductor)
-                    o << Wr(p.out2) << " = " << R(IN(2)) << " + g * vs; }";
-                else if (p.code == kNortonCapacitor)
-                    o << Wr(p.out2) << " = -" << R(IN(2)) << " - g * vs; }";
-                else
-                    o << Wr(p.out2) << " = " << C(p.par + 1) << " * " << R(IN(2)) << " + g * vs; }";
-                t.cost = 8;
+            case kNortonSeriesRL:
+                t.kind = p.code == kNortonInductor ? K_IND : p.code == kNortonCapacitor ? K_CAP : K_SRL;
+                reads(t, {IN(0), IN(1), IN(2)});
+                t.writes = {p.out2};
+                t.f = {off(IN(0)), off(IN(1)), off(IN(2)), off(p.out2)};
+                t.ck = {p.par};
+                if (p.code == kNortonSeriesRL) t.ck.push_back(p.par + 1);
+                t.cost = 10;
                 break;
-            }
-            case kNortonVoltageSource: {
-                t.writes.push_back(p.out2);
-                o << "{ const double g = " << C(p.par) << "; " << Wr(p.out2) << " = g * "
-                  << source(p.par + 1, p.par + 2, p.par + 3) << "; }";
-                t.cost = invariant(p.par + 2) && ct[static_cast<size_t>(p.par + 2) * W] == 0.0 ? 3 : 90;
+            case kNortonVoltageSource:
+                t.kind = K_VSRC;
+                t.writes = {p.out2};
+                t.f = {off(p.out2)};
+                t.ck = {p.par, p.par + 1, p.par + 2, p.par + 3};
+                t.cost = invariant(p.par + 2) && c0(p.par + 2) == 0.0 ? 6 : 90;
                 break;
-            }
-            case kNortonCurrentSource: {
-                t.writes.push_back(p.out2);
-                o << Wr(p.out2) << " = " << source(p.par, p.par + 1, p.par + 2) << ";";
-                t.cost = invariant(p.par + 1) && ct[static_cast<size_t>(p.par + 1) * W] == 0.0 ? 2 : 90;
+            case kNortonCurrentSource:
+                t.kind = K_ISRC;
+                t.writes = {p.out2};
+                t.f = {off(p.out2)};
+                t.ck = {p.par, p.par + 1, p.par + 2};
+                t.cost = invariant(p.par + 1) && c0(p.par + 1) == 0.0 ? 5 : 90;
                 break;
-            }
-            case kNortonControlledSource: {
-                if (p.in_count > 3) reads({IN(3)});
-                t.writes.push_back(p.out2);
-                o << Wr(p.out2) << " = " << C(p.par) << " * " << (p.in_count > 3 ? R(IN(3)) : std::string("(0.0)")) << ";";
-                t.cost = 3;
+            case kNortonControlledSource:
+                t.kind = K_CSRC;
+                if (p.in_count > 3) reads(t, {IN(3)});
+                t.writes = {p.out2};
+                t.f = {off(p.out2), p.in_count > 3 ? off(IN(3)) : 0};
+                t.ck = {p.par};
+                t.cost = 6;
                 break;
-            }
-            case kNortonSwitch: {  // exec.cpp:151-165
-                t.reads.push_back(p.state);
-                t.writes.push_back(p.state);
-                t.writes.push_back(p.state + 1);
-                t.writes.push_back(p.out);
-                o << "{ int now = " << C(p.par + 2) << " != 0.0 ? 1 : 0; ";
-                for (int j = 3; j < p.par_len; ++j) o << "if (t >= " << C(p.par + j) << ") now ^= 1; ";
-                o << "const double chg = (double)now != " << R(p.state) << " ? 1.0 : 0.0; "
-                  << Wr(p.state + 1) << " = chg; " << Wr(p.state) << " = (double)now; " << Wr(p.out)
-                  << " = now != 0 ? " << C(p.par) << " : " << C(p.par + 1) << "; "
-                  << "if (chg != 0.0) { wflag = 1; if (live && a.events) { const int q = atomicAdd(a.n_events, 1); "
-                  << "if (q < a.max_events) { a.events[3*q] = step; a.events[3*q+1] = gl; a.events[3*q+2] = " << p.id
-                  << "; } } } }";
-                t.cost = 8 + 2 * (p.par_len - 3);
+            case kNortonSwitch:  // exec.cpp:151-165
+                t.kind = K_SW;
+                t.reads = {p.state};
+                t.writes = {p.state, p.state + 1, p.out};
+                t.f = {off(p.state), off(p.state + 1), off(p.out), p.id};
+                for (int j = 0; j < p.par_len; ++j) t.ck.push_back(p.par + j);
+                t.cost = 14 + 3 * (p.par_len - 3);
                 break;
-            }
-            case kInjectionPair:
-                return;  // contrib slots alias +-h (exact negation)
             case kCtlGain:
-                reads({IN(0)});
-                t.writes.push_back(p.out);
-                o << Wr(p.out) << " = " << C(p.par) << " * (" << sgn(sg[0]) << " * " << R(IN(0)) << ");";
-                t.cost = 3;
+                t.kind = K_GAIN;
+                reads(t, {IN(0)});
+                t.writes = {p.out};
+                t.f = {off(p.out), off(IN(0)), NEG(0)};
+                t.ck = {p.par};
+                t.cost = 6;
                 break;
-            case kCtlSum: {
-                o << "{ double acc = 0.0; ";
+            case kCtlSum:
+                t.kind = K_SUM;
                 for (int j = 0; j < p.in_count; ++j) {
-                    reads({IN(j)});
-                    o << "acc = acc + " << sgn(sg[j]) << " * " << R(IN(j)) << "; ";
+                    reads(t, {IN(j)});
+                    t.terms.push_back({off(IN(j)), NEG(j)});
                 }
-                t.writes.push_back(p.out);
-                o << Wr(p.out) << " = acc; }";
-                t.cost = 2 + 3 * p.in_count;
+                t.writes = {p.out};
+                t.f = {off(p.out)};
+                t.cost = 6 + 4 * p.in_count;
                 break;
-            }
             case kCtlIntegrator:
             case kCtlFirstOrderLag:
-            case kCtlPiController: {
-                reads({IN(0), p.state, p.state + 1});
-                t.writes.push_back(p.state);
-                t.writes.push_back(p.state + 1);
-                t.writes.push_back(p.out);
-                const std::string s0 = R(p.state), s1 = R(p.state + 1);
-                o << "{ const double u = " << sgn(sg[0]) << " * " << R(IN(0)) << "; ";
-                if (p.code == kCtlIntegrator) {
-                    o << "const double y = " << s0 << " + " << C(p.par) << " * (u + " << s1 << "); " << Wr(p.state)
-                      << " = y; " << Wr(p.state + 1) << " = u; " << Wr(p.out) << " = y; }";
-                } else if (p.code == kCtlFirstOrderLag) {
-                    o << "const double y = " << C(p.par) << " * " << s0 << " + " << C(p.par + 1) << " * (u + " << s1
-                      << "); " << Wr(p.state) << " = y; " << Wr(p.state + 1) << " = u; " << Wr(p.out) << " = y; }";
-                } else {
-                    o << "const double y = " << s0 << " + " << C(p.par + 1) << " * (u + " << s1 << "); "
-                      << Wr(p.state) << " = y; " << Wr(p.state + 1) << " = u; " << Wr(p.out) << " = " << C(p.par)
-                      << " * u + y; }";
-                }
-                t.cost = 8;
+            case kCtlPiController:
+                t.kind = p.code == kCtlIntegrator ? K_INTEG : p.code == kCtlFirstOrderLag ? K_LAG : K_PI;
+                reads(t, {IN(0), p.state, p.state + 1});
+                t.writes = {p.state, p.state + 1, p.out};
+                t.f = {off(p.out), off(IN(0)), off(p.state), off(p.state + 1), NEG(0)};
+                t.ck = {p.par};
+                if (p.code != kCtlIntegrator) t.ck.push_back(p.par + 1);
+                t.cost = 10;
                 break;
-            }
             case kCtlLimiter:
-                reads({IN(0)});
-                t.writes.push_back(p.out);
-                o << "{ const double u = " << sgn(sg[0]) << " * " << R(IN(0)) << "; const double lo = " << C(p.par)
-                  << ", hi = " << C(p.par + 1) << "; " << Wr(p.out) << " = u < lo ? lo : (u > hi ? hi : u); }";
-                t.cost = 4;
+                t.kind = K_LIM;
+                reads(t, {IN(0)});
+                t.writes = {p.out};
+                t.f = {off(p.out), off(IN(0)), NEG(0)};
+                t.ck = {p.par, p.par + 1};
+                t.cost = 7;
                 break;
             case kCtlComparator:
-                reads({IN(0), IN(1)});
-                t.writes.push_back(p.out);
-                o << Wr(p.out) << " = " << sgn(sg[0]) << " * " << R(IN(0)) << " >= " << sgn(sg[1]) << " * " << R(IN(1))
-                  << " ? 1.0 : 0.0;";
-                t.cost = 4;
+                t.kind = K_CMP;
+                reads(t, {IN(0), IN(1)});
+                t.writes = {p.out};
+                t.f = {off(p.out), off(IN(0)), off(IN(1)), NEG(0), NEG(1)};
+                t.cost = 7;
                 break;
             case kCtlConstant:
-                t.writes.push_back(p.out);
-                o << Wr(p.out) << " = " << C(p.par) << ";";
-                t.cost = 1;
+                t.kind = K_CONST;
+                t.writes = {p.out};
+                t.f = {off(p.out)};
+                t.ck = {p.par};
+                t.cost = 3;
                 break;
             case kCtlDelay:
-                reads({IN(0)});
-                t.writes.push_back(p.out);
-                o << Wr(p.out) << " = " << sgn(sg[0]) << " * " << R(IN(0)) << ";";
-                t.cost = 2;
+                t.kind = K_DELAY;
+                reads(t, {IN(0)});
+                t.writes = {p.out};
+                t.f = {off(p.out), off(IN(0)), NEG(0)};
+                t.cost = 4;
                 break;
             default:
                 return;
         }
-        t.code = o.str();
         add(std::move(t), region);
     }
 
@@ -320,17 +307,19 @@ struct Gen {
         const int v = s.v_base;
         for (int node = 0; node < s.nodes; ++node) {
             Task t;
-            std::ostringstream o;
-            o << "{ double acc = 0.0; ";
+            t.kind = K_GATHER;
             for (int q = s.gather_ptr[static_cast<size_t>(node)]; q < s.gather_ptr[static_cast<size_t>(node) + 1]; ++q) {
                 const int slot = s.gather_slot[static_cast<size_t>(q)];
                 t.reads.push_back(dep_slot(slot));
-                o << "acc = acc + " << R(slot) << "; ";
+                if (slot >= 0 && cls[static_cast<size_t>(slot)] == kContrib)
+                    t.terms.push_back({off(contrib_h[static_cast<size_t>(slot)]),
+                                       contrib_sign[static_cast<size_t>(slot)] < 0 ? 1 : 0});
+                else
+                    t.terms.push_back({off(slot), 0});
             }
-            o << Wr(v + node) << " = acc; }";
-            t.writes.push_back(v + node);
-            t.cost = 2 + 2 * static_cast<int>(t.reads.size());
-            t.code = o.str();
+            t.writes = {v + node};
+            t.f = {off(v + node)};
+            t.cost = 8 + 4 * static_cast<int>(t.terms.size());
             add(std::move(t), region);
         }
         if (s.nodes > 0) {
@@ -338,36 +327,31 @@ struct Gen {
                 const int lb = s.l_row_ptr[static_cast<size_t>(i)], le = s.l_row_ptr[static_cast<size_t>(i) + 1];
                 if (lb == le) continue;
                 Task t;
-                std::ostringstream o;
-                o << "{ double x = " << R(v + i) << "; ";
+                t.kind = K_FWD;
                 t.reads.push_back(v + i);
                 for (int k = lb; k < le; ++k) {
                     const int c = s.l_col[static_cast<size_t>(k)];
                     t.reads.push_back(v + c);
-                    o << "x = x - " << Lr(k) << " * " << R(v + c) << "; ";
+                    t.terms.push_back({lu_l(k), off(v + c)});
                 }
-                o << Wr(v + i) << " = x; }";
-                t.writes.push_back(v + i);
-                t.cost = 2 + 3 * (le - lb);
-                t.code = o.str();
+                t.writes = {v + i};
+                t.f = {off(v + i)};
+                t.cost = 8 + 5 * (le - lb);
                 add(std::move(t), region);
             }
-            for (int i = s.dim - 1; i >= 0; --i) {  // backward (sparse.cpp:161-171) + divergence (exec.cpp:229-237)
+            for (int i = s.dim - 1; i >= 0; --i) {  // backward (sparse.cpp:161-171) + divergence check
                 const int ub = s.u_row_ptr[static_cast<size_t>(i)], ue = s.u_row_ptr[static_cast<size_t>(i) + 1];
                 Task t;
-                std::ostringstream o;
-                o << "{ double x = " << R(v + i) << "; ";
+                t.kind = K_BWD;
                 t.reads.push_back(v + i);
                 for (int k = ub + 1; k < ue; ++k) {
                     const int c = s.u_col[static_cast<size_t>(k)];
                     t.reads.push_back(v + c);
-                    o << "x = x - " << Ur(k) << " * " << R(v + c) << "; ";
+                    t.terms.push_back({lu_u(k), off(v + c)});
                 }
-                o << "x = x / " << Ur(ub) << "; " << Wr(v + i) << " = x; "
-                  << "if (!(fabs(x) <= a.div_limit) && " << i << " < bad) bad = " << i << "; }";
-                t.writes.push_back(v + i);
-                t.cost = 24 + 3 * (ue - ub - 1);
-                t.code = o.str();
+                t.writes = {v + i};
+                t.f = {off(v + i), lu_u(ub), i};
+                t.cost = 40 + 5 * (ue - ub - 1);
                 add(std::move(t), region);
             }
         }
@@ -377,61 +361,125 @@ struct Gen {
             t.reads = {dep_slot(f[1]), dep_slot(f[2])};
             if (f[3] >= 0) t.reads.push_back(f[3]);
             if (f[4] >= 0) t.reads.push_back(f[4]);
-            t.writes.push_back(f[0]);
-            std::ostringstream o;
-            o << Wr(f[0]) << " = " << R(f[1]) << " * (" << R(f[4]) << " - " << R(f[3]) << ") + " << R(f[2]) << ";";
-            t.cost = 6;
-            t.code = o.str();
+            t.writes = {f[0]};
+            const bool gconst = f[1] >= 0 && cls[static_cast<size_t>(f[1])] == kDerived && derived_const[static_cast<size_t>(f[1])] >= 0;
+            t.kind = gconst ? K_FINC : K_FINS;
+            t.f = {off(f[0]), off(f[2]), off(f[3]), off(f[4])};
+            if (gconst) t.ck = {derived_const[static_cast<size_t>(f[1])]};
+            else t.f.push_back(off(f[1]));
+            t.cost = 9;
             add(std::move(t), region);
         }
     }
 
-    // Classifies the arena slots the step loop touches: the most accessed go to
-    // shared memory ([slot][32 lanes]) until the budget is spent, the rest stay
-    // in the global arena ([slot][W], L2-resident, coalesced across lanes).
-    void assign_hot(bool& lu_smem, size_t& smem_bytes) {
-        std::map<int, long> uses;
-        for (const Task& t : tasks) {
-            for (int x : t.reads)
-                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) uses[x] += 1;
-            for (int x : t.writes)
-                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) uses[x] += 1;
-        }
-        for (int x : s.watch)
-            if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) uses[x] += 0;
-        for (int x : s.channel_slot)
-            if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) uses[x] += 1;
-        for (size_t q = 0; q < s.latch_live.size(); ++q) {
-            uses[s.latch_live[q]] += 1;
-            uses[s.latch_shadow[q]] += 1;
-        }
-        for (int x : s.mentry_slot)
-            if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) uses[x] += 0;
-        std::vector<std::pair<long, int>> order;
-        for (const auto& kv : uses)
-            if (cls[static_cast<size_t>(kv.first)] == kNone) order.push_back({-kv.second, kv.first});
-        std::sort(order.begin(), order.end());
-        const size_t per_slot = 32 * sizeof(double);
-        const size_t fixed = 32 * sizeof(int);
-        const size_t cap = opt.smem_budget > fixed ? (opt.smem_budget - fixed) / per_slot : 0;
-        for (const auto& pr : order) {
-            const int x = pr.second;
-            if (hot_slots.size() < cap) {
-                cls[static_cast<size_t>(x)] = kHot;
-                hot_index[static_cast<size_t>(x)] = static_cast<int>(hot_slots.size());
-                hot_slots.push_back(x);
-            } else {
-                cls[static_cast<size_t>(x)] = kGlobal;
+    void emit_all(int& fact_count) {
+        tasks.clear();
+        int region = 0;
+        fact_count = 0;
+        for (int L = 0; L < s.layers; ++L) {
+            for (int k = s.layer_begin[static_cast<size_t>(L)]; k < s.layer_begin[static_cast<size_t>(L) + 1]; ++k) {
+                const Proc& p = s.procs[static_cast<size_t>(k)];
+                if (p.code == kFactorizeSystem) {
+                    ++fact_count;
+                    region = 1;
+                    fact_layer = L;
+                    continue;
+                }
+                if (p.code == kSolveSystem) {
+                    solve_layer = L;
+                    emit_solve(region);
+                    continue;
+                }
+                emit_proc(p, region);
             }
         }
-        const size_t base = hot_slots.size() * per_slot + fixed;
-        const size_t lu = (s.l_col.size() + s.u_col.size()) * per_slot;
-        lu_smem = opt.lu_in_smem && base + lu <= opt.smem_budget;
-        smem_bytes = base + (lu_smem ? lu : 0);
-        if (lu_smem) {
-            l_base_smem = static_cast<int>(hot_slots.size());
-            u_base_smem = l_base_smem + static_cast<int>(s.l_col.size());
+        for (size_t ch = 0; ch < s.channel_slot.size(); ++ch) {  // record (exec.cpp:313-321)
+            Task t;
+            t.kind = K_REC;
+            const int slot = s.channel_slot[ch];
+            if (slot >= 0) t.reads.push_back(dep_slot(slot));
+            t.f = {static_cast<int>(ch), off(slot)};
+            t.cost = 4;
+            add(std::move(t), 1);
         }
+        for (size_t q = 0; q < s.latch_live.size(); ++q) {  // latch (exec.cpp:323-329)
+            Task t;
+            t.kind = K_LATCH;
+            t.reads = {s.latch_live[q]};
+            t.writes = {s.latch_shadow[q]};
+            t.f = {off(s.latch_live[q]), off(s.latch_shadow[q])};
+            t.cost = 3;
+            add(std::move(t), 1);
+        }
+    }
+
+    // Shared-memory layout per 32-lane group ([slot][lane] doubles): slot 0 holds
+    // 0.0 (ground / derived zeros); then every arena slot the step loop reads or
+    // writes, the watch slots and the switch conductances the refactorization
+    // reads; then lane-varying constants the step reads (cached once per
+    // launch); then L and U when they fit. Switch "changed" slots are always 0
+    // at the end of a pass (FactorizeSystem clears them), so when every switch
+    // updates before the factorization point they collapse into one per-lane
+    // refactor flag instead of a slot each.
+    bool assign_hot(bool& lu_smem, size_t& smem_bytes) {
+        chg_flag = true;
+        chg_slots.clear();
+        for (const Proc& p : s.procs)
+            if (p.code == kNortonSwitch) chg_slots.push_back(p.state + 1);
+        for (const Task& t : tasks)
+            if (t.kind == K_SW && t.region != 0) chg_flag = false;
+        if (chg_flag)
+            for (int x : chg_slots) cls[static_cast<size_t>(x)] = kChg;
+        std::set<int> need;
+        for (const Task& t : tasks) {
+            for (int x : t.reads)
+                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+            for (int x : t.writes)
+                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+        }
+        for (int x : s.watch)
+            if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+        for (int x : s.mentry_slot)
+            if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+        hot_slots.assign(1, -1);
+        for (int x : need) {
+            cls[static_cast<size_t>(x)] = kHot;
+            hot_index[static_cast<size_t>(x)] = static_cast<int>(hot_slots.size());
+            hot_slots.push_back(x);
+        }
+        const size_t per_slot = 32 * sizeof(double);
+        const size_t fixed = 2 * 32 * sizeof(int);  // serr + refactor flags
+        size_t used = hot_slots.size() * per_slot + fixed;
+        if (used > opt.smem_budget) return false;
+        std::set<int> vc;
+        for (const Task& t : tasks)
+            for (int k : t.ck)
+                if (!invariant(k)) vc.insert(k);
+        vc_index.assign(static_cast<size_t>(s.consts), -1);
+        vc_slots.clear();
+        vc_base = static_cast<int>(hot_slots.size());
+        if (used + vc.size() * per_slot <= opt.smem_budget) {
+            for (int k : vc) {
+                vc_index[static_cast<size_t>(k)] = vc_base + static_cast<int>(vc_slots.size());
+                vc_slots.push_back(k);
+            }
+            used += vc.size() * per_slot;
+        }
+        const int next = vc_base + static_cast<int>(vc_slots.size());
+        const size_t lu = (s.l_col.size() + s.u_col.size()) * per_slot;
+        lu_smem = opt.lu_in_smem && used + lu <= opt.smem_budget;
+        if (lu_smem) {
+            l_base_smem = next;
+            u_base_smem = l_base_smem + static_cast<int>(s.l_col.size());
+            used += lu;
+        }
+        smem_bytes = used;
+        return true;
+    }
+
+    int smem_slots() const {
+        return vc_base + static_cast<int>(vc_slots.size()) +
+               (l_base_smem >= 0 ? static_cast<int>(s.l_col.size() + s.u_col.size()) : 0);
     }
 
     // Refactorization (FactorizeSystem, exec.cpp:175-204; lu_factor, sparse.cpp:79-145)
@@ -440,7 +488,9 @@ struct Gen {
     std::string emit_refactor() const {
         std::ostringstream o;
         o << "      bool need = false;\n";
-        for (int x : s.watch) o << "      need = need || (" << R(x) << " != 0.0);\n";
+        for (int x : s.watch)
+            if (x >= 0 && cls[static_cast<size_t>(x)] != kChg) o << "      need = need || (" << R(x) << " != 0.0);\n";
+        if (chg_flag) o << "      need = need || (needS[lane] != 0);\n";
         o << "      if (need) {\n";
         const int nnz = static_cast<int>(s.col_idx.size());
         for (int k = 0; k < nnz; ++k) {
@@ -452,7 +502,7 @@ struct Gen {
         }
         o << "        double mx = 0.0;\n";
         for (int k = 0; k < nnz; ++k) o << "        { const double x = fabs(G" << k << "); mx = mx < x ? x : mx; }\n";
-        // last row touching each scratch column (final scratch contents, sparse.cpp:92-131)
+        // last row touching each scratch column: final scratch contents (sparse.cpp:92-131)
         std::vector<int> last_row(static_cast<size_t>(s.dim), -1);
         for (int i = 0; i < s.dim; ++i) {
             for (int k = s.l_row_ptr[static_cast<size_t>(i)]; k < s.l_row_ptr[static_cast<size_t>(i) + 1]; ++k)
@@ -491,7 +541,9 @@ struct Gen {
             o << "          if (!(fabs(u" << ub << ") > " << lit(1e-12) << " * mx)) { srow = " << i << "; goto fact_done; }\n";
             o << "        }\n";
         }
-        for (int x : s.watch) o << "        " << Wr(x) << " = 0.0;\n";
+        for (int x : s.watch)
+            if (x >= 0 && cls[static_cast<size_t>(x)] != kChg) o << "        " << Wr(x) << " = 0.0;\n";
+        if (chg_flag) o << "        needS[lane] = 0;\n";
         o << "      fact_done:;\n";
         o << "      }\n";
         return o.str();
@@ -517,7 +569,7 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
         if (makespan) *makespan = 0;
         return out;
     }
-    std::map<int, int> local;  // task id -> position
+    std::map<int, int> local;
     for (size_t i = 0; i < n; ++i) local[ids[i]] = static_cast<int>(i);
     std::vector<std::vector<int>> pred(n), succ(n);
     for (size_t i = 0; i < n; ++i)
@@ -535,13 +587,12 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
         bottom[k] = cost[k] + b;
     }
     std::vector<int> missing(n), warp_of(n, -1), epoch(n, -1);
-    std::vector<long> finish(n, 0);
     for (size_t i = 0; i < n; ++i) missing[i] = static_cast<int>(pred[i].size());
     std::set<std::pair<long, int>> ready;  // (-bottom, i)
     for (size_t i = 0; i < n; ++i)
         if (missing[i] == 0) ready.insert({-bottom[i], static_cast<int>(i)});
     std::vector<long> T(static_cast<size_t>(G), 0);
-    std::vector<std::vector<std::pair<int, int>>> plan(static_cast<size_t>(G));  // (task, phase)
+    std::vector<std::vector<std::pair<int, int>>> plan(static_cast<size_t>(G));
     int nb = 0;
     size_t done = 0;
     auto visible = [&](int i, int w) {
@@ -576,7 +627,7 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
             continue;
         }
         if (first_starves) {
-            long waiting = 0;  // ready work only a barrier can expose to the idle warp
+            long waiting = 0;
             for (const auto& r : ready)
                 if (!visible(r.second, order[0])) waiting += cost[static_cast<size_t>(r.second)];
             const long spread = T[static_cast<size_t>(order.back())] - T[static_cast<size_t>(order[0])];
@@ -587,9 +638,7 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
         }
         const size_t i = static_cast<size_t>(pick_i);
         ready.erase({-bottom[i], pick_i});
-        long start = T[static_cast<size_t>(pick_w)];
-        T[static_cast<size_t>(pick_w)] = start + cost[i];
-        finish[i] = T[static_cast<size_t>(pick_w)];
+        T[static_cast<size_t>(pick_w)] += cost[i];
         warp_of[i] = pick_w;
         epoch[i] = nb;
         plan[static_cast<size_t>(pick_w)].push_back({ids[i], nb});
@@ -601,7 +650,6 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
     for (int w = 0; w < G; ++w)
         for (const auto& pr : plan[static_cast<size_t>(w)])
             out.phases[static_cast<size_t>(pr.second)][static_cast<size_t>(w)].push_back(pr.first);
-    // drop empty trailing phases
     while (out.phases.size() > 1) {
         bool empty = true;
         for (const auto& v : out.phases.back()) empty = empty && v.empty();
@@ -612,19 +660,310 @@ Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& id
     return out;
 }
 
-void emit_phases(std::ostringstream& o, const Sched& sc, const std::vector<Task>& tasks, const char* indent,
-                 bool barrier_after_last) {
-    for (size_t p = 0; p < sc.phases.size(); ++p) {
-        bool first = true;
-        for (size_t w = 0; w < sc.phases[p].size(); ++w) {
-            if (sc.phases[p][w].empty()) continue;
-            o << indent << (first ? "if" : "else if") << " (warp == " << w << ") {\n";
-            for (int id : sc.phases[p][w]) o << indent << "  " << tasks[static_cast<size_t>(id)].code << "\n";
-            o << indent << "}\n";
-            first = false;
-        }
-        if (p + 1 < sc.phases.size() || barrier_after_last) o << indent << "__syncthreads();\n";
+// Kind-major topological re-order of one (phase, warp) list, then split into
+// same-kind segments; a segment is "independent" when none of its tasks
+// depends on another task of the segment.
+struct Segment {
+    int kind, first, count, indep;
+};
+
+std::vector<Segment> segments_of(const std::vector<int>& list, const std::vector<std::vector<int>>& deps,
+                                 std::vector<Task>& tasks, std::vector<int>& ordered) {
+    std::set<int> in(list.begin(), list.end());
+    std::map<int, int> missing;
+    std::map<int, std::vector<int>> succ;
+    for (int id : list) {
+        int m = 0;
+        for (int d : deps[static_cast<size_t>(id)])
+            if (in.count(d)) {
+                ++m;
+                succ[d].push_back(id);
+            }
+        missing[id] = m;
     }
+    std::map<int, int> pos;
+    for (size_t i = 0; i < list.size(); ++i) pos[list[i]] = static_cast<int>(i);
+    auto key = [&](int id) {
+        const Task& t = tasks[static_cast<size_t>(id)];
+        return t.kind * 1000000 + static_cast<int>(t.terms.size()) * 1000 + static_cast<int>(t.ck.size());
+    };
+    std::set<std::pair<std::pair<int, int>, int>> ready;  // ((segment key, pos), id)
+    for (int id : list)
+        if (missing[id] == 0) ready.insert({{key(id), pos[id]}, id});
+    ordered.clear();
+    int cur_kind = -1;
+    while (!ready.empty()) {
+        auto it = ready.begin();
+        for (auto jt = ready.begin(); jt != ready.end(); ++jt)
+            if (jt->first.first == cur_kind) {  // keep same-kind runs together
+                it = jt;
+                break;
+            }
+        const int id = it->second;
+        cur_kind = it->first.first;
+        ready.erase(it);
+        ordered.push_back(id);
+        for (int sx : succ[id])
+            if (--missing[sx] == 0) ready.insert({{key(sx), pos[sx]}, sx});
+    }
+    std::vector<Segment> segs;
+    for (size_t i = 0; i < ordered.size();) {
+        size_t j = i;
+        const int kind = tasks[static_cast<size_t>(ordered[i])].kind;
+        std::set<int> members;
+        bool indep = unrollable(kind);
+        const size_t nterm = tasks[static_cast<size_t>(ordered[i])].terms.size();
+        const size_t ncst = tasks[static_cast<size_t>(ordered[i])].ck.size();
+        while (j < ordered.size() && tasks[static_cast<size_t>(ordered[j])].kind == kind &&
+               tasks[static_cast<size_t>(ordered[j])].terms.size() == nterm &&
+               tasks[static_cast<size_t>(ordered[j])].ck.size() == ncst) {
+            for (int d : deps[static_cast<size_t>(ordered[j])])
+                if (members.count(d)) indep = false;
+            members.insert(ordered[j]);
+            ++j;
+        }
+        segs.push_back({kind, static_cast<int>(i), static_cast<int>(j - i), indep ? 1 : 0});
+        i = j;
+    }
+    return segs;
+}
+
+// ---- device-side code templates --------------------------------------------
+// Per kind: operand loads / compute / store, with {I<n>} = integer record field
+// n and {C<n>} = constant field n of the task at unroll index @. A segment's
+// loop bounds and table bases are compile-time constants inside a warp-uniform
+// branch, so records come through the uniform datapath (LDCU) and shared-memory
+// accesses become LDS [lane_base + uniform offset].
+struct KindCode {
+    const char* loads;
+    const char* compute;
+    const char* store;
+};
+
+const KindCode kCode[K_NKINDS] = {
+    /*IND*/ {"const double vs@ = LD({I1}) - LD({I0}); const double ip@ = LD({I2}); const double g@ = {C0};",
+             "const double h@ = ip@ + g@ * vs@;", "ST({I3}, h@);"},
+    /*CAP*/ {"const double vs@ = LD({I1}) - LD({I0}); const double ip@ = LD({I2}); const double g@ = {C0};",
+             "const double h@ = -ip@ - g@ * vs@;", "ST({I3}, h@);"},
+    /*SRL*/ {"const double vs@ = LD({I1}) - LD({I0}); const double ip@ = LD({I2}); const double g@ = {C0}; const double d@ = {C1};",
+             "const double h@ = d@ * ip@ + g@ * vs@;", "ST({I3}, h@);"},
+    /*VSRC*/ {"const double g@ = {C0}; const double m@ = {C1}; const double w@ = {C2}; const double p@ = {C3};",
+              "const double h@ = g@ * (w@ == 0.0 ? m@ : m@ * cos(w@ * t + p@));", "ST({I0}, h@);"},
+    /*ISRC*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
+              "const double h@ = w@ == 0.0 ? m@ : m@ * cos(w@ * t + p@);", "ST({I0}, h@);"},
+    /*CSRC*/ {"const double k@ = {C0}; const double x@ = LD({I1});", "const double h@ = k@ * x@;", "ST({I0}, h@);"},
+    /*SW*/ {nullptr, nullptr, nullptr},
+    /*GATHER*/ {nullptr, nullptr, nullptr},
+    /*FWD*/ {nullptr, nullptr, nullptr},
+    /*BWD*/ {nullptr, nullptr, nullptr},
+    /*FINC*/ {"const double vs@ = LD({I3}) - LD({I2}); const double h@ = LD({I1}); const double g@ = {C0};",
+              "const double i@ = g@ * vs@ + h@;", "ST({I0}, i@);"},
+    /*FINS*/ {"const double vs@ = LD({I3}) - LD({I2}); const double h@ = LD({I1}); const double g@ = LD({I4});",
+              "const double i@ = g@ * vs@ + h@;", "ST({I0}, i@);"},
+    /*GAIN*/ {"const double x@ = SGN(LD({I1}), {I2}); const double k@ = {C0};", "const double y@ = k@ * x@;",
+              "ST({I0}, y@);"},
+    /*SUM*/ {nullptr, nullptr, nullptr},
+    /*INTEG*/ {"const double u@ = SGN(LD({I1}), {I4}); const double s0@ = LD({I2}); const double s1@ = LD({I3}); const double c0@ = {C0};",
+               "const double y@ = s0@ + c0@ * (u@ + s1@);", "ST({I2}, y@); ST({I3}, u@); ST({I0}, y@);"},
+    /*LAG*/ {"const double u@ = SGN(LD({I1}), {I4}); const double s0@ = LD({I2}); const double s1@ = LD({I3}); const double c0@ = {C0}; const double c1@ = {C1};",
+             "const double y@ = c0@ * s0@ + c1@ * (u@ + s1@);", "ST({I2}, y@); ST({I3}, u@); ST({I0}, y@);"},
+    /*PI*/ {"const double u@ = SGN(LD({I1}), {I4}); const double s0@ = LD({I2}); const double s1@ = LD({I3}); const double kp@ = {C0}; const double ki@ = {C1};",
+            "const double y@ = s0@ + ki@ * (u@ + s1@); const double o@ = kp@ * u@ + y@;",
+            "ST({I2}, y@); ST({I3}, u@); ST({I0}, o@);"},
+    /*LIM*/ {"const double u@ = SGN(LD({I1}), {I2}); const double lo@ = {C0}; const double hi@ = {C1};",
+             "const double y@ = u@ < lo@ ? lo@ : (u@ > hi@ ? hi@ : u@);", "ST({I0}, y@);"},
+    /*CMP*/ {"const double a@ = SGN(LD({I1}), {I3}); const double b@ = SGN(LD({I2}), {I4});",
+             "const double y@ = a@ >= b@ ? 1.0 : 0.0;", "ST({I0}, y@);"},
+    /*CONST*/ {"const double y@ = {C0};", "", "ST({I0}, y@);"},
+    /*DELAY*/ {"const double y@ = SGN(LD({I1}), {I2});", "", "ST({I0}, y@);"},
+    /*REC*/ {"const double y@ = LD({I1});", "",
+             "if (live) a.waves[((size_t)(a.row0 + it) * NCH + {I0}) * W_ + gl] = y@;"},
+    /*LATCH*/ {"const double y@ = LD({I0});", "", "ST({I1}, y@);"},
+};
+
+// Per-segment record layout. Constant field modes: 0 = lane-invariant value in
+// the double table, 1 = lane-varying, slot index (value from the per-lane
+// const table in HBM), 2 = lane-varying, cached in shared memory (byte offset).
+// Term operands (gather / sum / solve rows) are stored inline: a segment only
+// holds tasks with the same term count, so term loops fully unroll.
+struct SegLayout {
+    int nI = 0, nC = 0, TC = 0;
+    std::vector<int> cmode;
+    int SI = 0, SD = 0;
+    std::vector<int> cpos;  // per const field: position in the int (modes 1, 2) or double (mode 0) record
+};
+
+std::string cfield(const SegLayout& L, int n, const std::string& bi, const std::string& bd) {
+    const int m = L.cmode[static_cast<size_t>(n)];
+    const std::string pos = std::to_string(L.cpos[static_cast<size_t>(n)]);
+    if (m == 0) return "kRd[" + bd + " + " + pos + "]";
+    if (m == 2) return "LD(kRi[" + bi + " + " + pos + "])";
+    return "__ldg(C + (size_t)kRi[" + bi + " + " + pos + "] * W_)";
+}
+
+std::string expand(const char* tpl, int j, const SegLayout& L, const std::string& bi, const std::string& bd) {
+    std::string out;
+    for (const char* c = tpl; c && *c; ++c) {
+        if (*c == '@') {
+            out += std::to_string(j);
+        } else if (*c == '{' && (c[1] == 'I' || c[1] == 'C')) {
+            const char kind = c[1];
+            const char* e = std::strchr(c, '}');
+            const int n = std::atoi(std::string(c + 2, e).c_str());
+            if (kind == 'I') out += "kRi[" + bi + " + " + std::to_string(n) + "]";
+            else out += cfield(L, n, bi, bd);
+            c = e;
+        } else {
+            out += *c;
+        }
+    }
+    return out;
+}
+
+// Loads / compute / store text of one task at unroll index j (record base `bi`,
+// `bd`) for every kind except the switch.
+void task_parts(int kind, int j, const SegLayout& L, const std::string& bi, const std::string& bd, std::string& ld,
+                std::string& cp, std::string& st) {
+    const std::string J = std::to_string(j);
+    auto Tx = [&](int t) { return "kRi[" + bi + " + " + std::to_string(L.nI + 2 * t) + "]"; };
+    auto Ty = [&](int t) { return "kRi[" + bi + " + " + std::to_string(L.nI + 2 * t + 1) + "]"; };
+    auto I = [&](int n) { return "kRi[" + bi + " + " + std::to_string(n) + "]"; };
+    if (kCode[kind].loads != nullptr) {
+        ld = expand(kCode[kind].loads, j, L, bi, bd);
+        cp = expand(kCode[kind].compute, j, L, bi, bd);
+        st = expand(kCode[kind].store, j, L, bi, bd);
+        return;
+    }
+    std::ostringstream l, c;
+    if (kind == K_GATHER || kind == K_SUM) {  // sequential accumulation from 0.0 (exec.cpp:207-214, 245-253)
+        for (int t = 0; t < L.TC; ++t) l << "const double a" << J << "_" << t << " = SGN(LD(" << Tx(t) << "), " << Ty(t) << "); ";
+        c << "double acc" << J << " = 0.0; ";
+        for (int t = 0; t < L.TC; ++t) c << "acc" << J << " = acc" << J << " + a" << J << "_" << t << "; ";
+        st = "ST(" + I(0) + ", acc" + J + ");";
+    } else {  // FWD / BWD rows (sparse.cpp:152-171) + divergence (exec.cpp:229-237)
+        l << "double x" << J << " = LD(" << I(0) << "); ";
+        for (int t = 0; t < L.TC; ++t)
+            l << "const double p" << J << "_" << t << " = LU(" << Tx(t) << ") * LD(" << Ty(t) << "); ";
+        for (int t = 0; t < L.TC; ++t) c << "x" << J << " = x" << J << " - p" << J << "_" << t << "; ";
+        if (kind == K_BWD)
+            c << "x" << J << " = x" << J << " / LU(" << I(1) << "); if (!(fabs(x" << J << ") <= a.div_limit) && " << I(2)
+              << " < bad) bad = " << I(2) << "; ";
+        st = "ST(" + I(0) + ", x" + J + ");";
+    }
+    ld = l.str();
+    cp = c.str();
+}
+
+// Straight-line form of one task: every shared-memory offset and constant
+// index is a literal, so the compiler may interleave independent tasks freely
+// (no aliasing unknowns) — the latency-optimal form when the step fits the
+// instruction cache.
+struct LitCtx {
+    std::function<std::string(int)> cst;  // const slot -> expression
+};
+
+std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
+    std::string out;
+    for (const char* p = tpl; p && *p; ++p) {
+        if (*p == '@') {
+            out += "_";
+        } else if (*p == '{' && (p[1] == 'I' || p[1] == 'C')) {
+            const char kind = p[1];
+            const char* e = std::strchr(p, '}');
+            const int n = std::atoi(std::string(p + 2, e).c_str());
+            out += kind == 'I' ? std::to_string(t.f[static_cast<size_t>(n)]) : c.cst(t.ck[static_cast<size_t>(n)]);
+            p = e;
+        } else {
+            out += *p;
+        }
+    }
+    return out;
+}
+
+std::string task_literal(const Task& t, const LitCtx& c) {
+    std::ostringstream o;
+    o << "{ ";
+    if (kCode[t.kind].loads != nullptr) {
+        o << expand_lit(kCode[t.kind].loads, t, c) << " " << expand_lit(kCode[t.kind].compute, t, c) << " "
+          << expand_lit(kCode[t.kind].store, t, c);
+    } else if (t.kind == K_GATHER || t.kind == K_SUM) {
+        o << "double acc = 0.0; ";
+        for (const auto& tm : t.terms) o << "acc = acc + " << (tm.second ? "-" : "") << "LD(" << tm.first << "); ";
+        o << "ST(" << t.f[0] << ", acc);";
+    } else if (t.kind == K_FWD || t.kind == K_BWD) {
+        o << "double x = LD(" << t.f[0] << "); ";
+        for (const auto& tm : t.terms) o << "x = x - LU(" << tm.first << ") * LD(" << tm.second << "); ";
+        if (t.kind == K_BWD)
+            o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
+        o << "ST(" << t.f[0] << ", x);";
+    } else if (t.kind == K_SW) {
+        o << "int now = " << c.cst(t.ck[2]) << " != 0.0 ? 1 : 0; ";
+        for (size_t j = 3; j < t.ck.size(); ++j) o << "if (t >= " << c.cst(t.ck[j]) << ") now ^= 1; ";
+        o << "const double chg = (double)now != LD(" << t.f[0] << ") ? 1.0 : 0.0; SETCHG(" << t.f[1] << ", chg); ST("
+          << t.f[0] << ", (double)now); ST(" << t.f[2] << ", now != 0 ? " << c.cst(t.ck[0]) << " : " << c.cst(t.ck[1])
+          << "); if (chg != 0.0) { wflag = 1; if (live && a.events) { const int e = atomicAdd(a.n_events, 1); "
+          << "if (e < a.max_events) { a.events[3*e] = step; a.events[3*e+1] = gl; a.events[3*e+2] = " << t.f[3] << "; } } }";
+    }
+    o << " }";
+    return o.str();
+}
+
+// One segment: N tasks of `kind` at table bases (bi0, bd0). Independent
+// segments issue the operand loads of up to four tasks before any compute or
+// store (the compiler cannot hoist shared-memory loads above stores itself).
+std::string segment_code(int kind, int N, bool indep, int bi0, int bd0, const SegLayout& L, const char* ind) {
+    std::ostringstream o;
+    const std::string SI = std::to_string(L.SI), SD = std::to_string(L.SD);
+    o << ind << "{  // " << kKindName[kind] << " x" << N << (L.TC ? " terms " + std::to_string(L.TC) : std::string()) << "\n";
+    if (kind != K_SW) {
+        const int U = indep ? knob("EMTB200_CG_UNROLL", 1) : 1;
+        const int q0 = N - N % U;
+        auto block = [&](const std::string& qexpr, int count, const char* in2) {
+            std::string ld[4], cp[4], st[4];
+            for (int j = 0; j < count; ++j) {
+                const std::string bi = "bi" + std::to_string(j), bd = "bd" + std::to_string(j);
+                o << in2 << "const int " << bi << " = " << bi0 << " + (" << qexpr << " + " << j << ") * " << SI << "; const int "
+                  << bd << " = " << bd0 << " + (" << qexpr << " + " << j << ") * " << SD << "; (void)" << bd << ";\n";
+                task_parts(kind, j, L, bi, bd, ld[j], cp[j], st[j]);
+            }
+            for (int j = 0; j < count; ++j) o << in2 << ld[j] << "\n";
+            for (int j = 0; j < count; ++j) o << in2 << cp[j] << "\n";
+            for (int j = 0; j < count; ++j) o << in2 << st[j] << "\n";
+        };
+        const std::string in2 = std::string(ind) + "    ";
+        if (q0 > 0) {
+            if (q0 == U) {
+                o << ind << "  {\n";
+                block("0", U, in2.c_str());
+                o << ind << "  }\n";
+            } else {
+                o << ind << "  #pragma unroll 1\n" << ind << "  for (int q = 0; q < " << q0 << "; q += " << U << ") {\n";
+                block("q", U, in2.c_str());
+                o << ind << "  }\n";
+            }
+        }
+        if (q0 < N) {
+            o << ind << "  {\n";
+            block(std::to_string(q0), N - q0, in2.c_str());
+            o << ind << "  }\n";
+        }
+    } else {  // exec.cpp:151-165; consts [g_on, g_off, initial, t0, ...]
+        o << ind << "  #pragma unroll 1\n"
+          << ind << "  for (int q = 0; q < " << N << "; ++q) {\n"
+          << ind << "    const int bi = " << bi0 << " + q * " << SI << "; const int bd = " << bd0 << " + q * " << SD
+          << "; (void)bd;\n";
+        auto I = [&](int n) { return "kRi[bi + " + std::to_string(n) + "]"; };
+        o << ind << "    int now = " << cfield(L, 2, "bi", "bd") << " != 0.0 ? 1 : 0;\n";
+        for (int c = 3; c < L.nC; ++c) o << ind << "    if (t >= " << cfield(L, c, "bi", "bd") << ") now ^= 1;\n";
+        o << ind << "    const double chg = (double)now != LD(" << I(0) << ") ? 1.0 : 0.0;\n"
+          << ind << "    SETCHG(" << I(1) << ", chg); ST(" << I(0) << ", (double)now); ST(" << I(2) << ", now != 0 ? "
+          << cfield(L, 0, "bi", "bd") << " : " << cfield(L, 1, "bi", "bd") << ");\n"
+          << ind << "    if (chg != 0.0) { wflag = 1; if (live && a.events) { const int e = atomicAdd(a.n_events, 1);"
+          << " if (e < a.max_events) { a.events[3*e] = step; a.events[3*e+1] = gl; a.events[3*e+2] = " << I(3) << "; } } }\n"
+          << ind << "  }\n";
+    }
+    o << ind << "}\n";
+    return o.str();
 }
 
 }  // namespace
@@ -633,94 +972,19 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
     g.classify();
-
-    // Sequential process order -> tasks; the FactorizeSystem process splits regions.
-    int region = 0;
-    for (int L = 0; L < s.layers; ++L) {
-        for (int k = s.layer_begin[static_cast<size_t>(L)]; k < s.layer_begin[static_cast<size_t>(L) + 1]; ++k) {
-            const Proc& p = s.procs[static_cast<size_t>(k)];
-            if (p.code == kFactorizeSystem) {
-                if (region != 0) {
-                    fail = {13, "", "schedule has more than one FactorizeSystem process"};
-                    return false;
-                }
-                region = 1;
-                g.fact_layer = L;
-                continue;
-            }
-            if (p.code == kSolveSystem) {
-                g.solve_layer = L;
-                g.emit_solve(region);
-                continue;
-            }
-            g.emit_proc(p, region);
-        }
-    }
-    if (region == 0) {
-        fail = {13, "", "schedule has no FactorizeSystem process"};
+    int facts = 0;
+    g.emit_all(facts);  // pass 1: slot sets
+    if (facts != 1) {
+        fail = {13, "", "schedule must hold exactly one FactorizeSystem process"};
         return false;
     }
-    // record (exec.cpp:313-321) then latch (exec.cpp:323-329)
-    for (size_t ch = 0; ch < s.channel_slot.size(); ++ch) {
-        Task t;
-        const int slot = s.channel_slot[ch];
-        if (slot >= 0) t.reads.push_back(g.dep_slot(slot));
-        t.cost = 3;
-        t.code = "if (live) a.waves[((size_t)(a.row0 + it) * " + std::to_string(s.channel_slot.size()) + " + " +
-                 std::to_string(ch) + ") * " + std::to_string(lanes) + " + gl] = " + g.R(slot) + ";";
-        // R() needs hot classification: patch after assign_hot (placeholder marker)
-        t.code = "@REC" + std::to_string(ch) + "@";
-        g.add(std::move(t), 1);
-    }
-    for (size_t q = 0; q < s.latch_live.size(); ++q) {
-        Task t;
-        t.reads.push_back(s.latch_live[q]);
-        t.writes.push_back(s.latch_shadow[q]);
-        t.cost = 2;
-        t.code = "@LAT" + std::to_string(q) + "@";
-        g.add(std::move(t), 1);
-    }
-
     bool lu_smem = false;
     size_t smem = 0;
-    // Hot classification needs every task's slot sets; codes emitted before it
-    // referenced R()/Wr() of slots not yet indexed, so regenerate them now.
-    g.assign_hot(lu_smem, smem);
-    if (smem > opt.smem_budget) {
-        fail = {13, "", "arena hot set (" + std::to_string(smem) + " B) exceeds shared memory budget"};
+    if (!g.assign_hot(lu_smem, smem)) {
+        fail = {13, "", "arena hot set exceeds the shared-memory budget"};
         return false;
     }
-    {
-        std::vector<Task> saved = std::move(g.tasks);
-        g.tasks.clear();
-        region = 0;
-        for (int L = 0; L < s.layers; ++L) {
-            for (int k = s.layer_begin[static_cast<size_t>(L)]; k < s.layer_begin[static_cast<size_t>(L) + 1]; ++k) {
-                const Proc& p = s.procs[static_cast<size_t>(k)];
-                if (p.code == kFactorizeSystem) { region = 1; continue; }
-                if (p.code == kSolveSystem) { g.emit_solve(region); continue; }
-                g.emit_proc(p, region);
-            }
-        }
-        for (size_t ch = 0; ch < s.channel_slot.size(); ++ch) {
-            Task t;
-            const int slot = s.channel_slot[ch];
-            if (slot >= 0) t.reads.push_back(g.dep_slot(slot));
-            t.cost = 3;
-            t.code = "if (live) a.waves[((size_t)(a.row0 + it) * " + std::to_string(s.channel_slot.size()) + " + " +
-                     std::to_string(ch) + ") * " + std::to_string(lanes) + " + gl] = " + g.R(slot) + ";";
-            g.add(std::move(t), 1);
-        }
-        for (size_t q = 0; q < s.latch_live.size(); ++q) {
-            Task t;
-            t.reads.push_back(s.latch_live[q]);
-            t.writes.push_back(s.latch_shadow[q]);
-            t.cost = 2;
-            t.code = g.Wr(s.latch_shadow[q]) + " = " + g.R(s.latch_live[q]) + ";";
-            g.add(std::move(t), 1);
-        }
-        (void)saved;
-    }
+    g.emit_all(facts);  // pass 2: records with shared-memory offsets
 
     // Dependencies from the sequential order (RAW, WAR, WAW), per region.
     const size_t nt = g.tasks.size();
@@ -762,19 +1026,112 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
     const Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
 
+    // ---- tables (records: ints + doubles, terms) and per-(phase, warp) segment code
+    std::vector<int> rki;
+    std::vector<double> rkd;
+    int segs_total = 0;
+    const bool straight = opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", opt.mode == 1 ? 1 : 1) != 0;
+    LitCtx lctx;
+    lctx.cst = [&](int k) -> std::string {
+        if (g.invariant(k)) return "kC[" + std::to_string(k) + "]";
+        if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * 256) + ")";
+        return "__ldg(C + " + std::to_string(static_cast<long long>(k) * lanes) + ")";
+    };
+    auto region_code = [&](const Sched& sc) {
+        std::ostringstream rc;
+        for (size_t p = 0; p < sc.phases.size(); ++p) {
+            if (p > 0) rc << "    __syncthreads();\n";
+            bool first = true;
+            for (int w = 0; w < G; ++w) {
+                std::vector<int> ordered;
+                const auto segs = segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
+                if (segs.empty()) continue;
+                rc << "    " << (first ? "if" : "else if") << " (warp == " << w << ") {\n";
+                first = false;
+                if (straight) {
+                    for (int id : ordered) rc << "      " << task_literal(g.tasks[static_cast<size_t>(id)], lctx) << "\n";
+                    rc << "    }\n";
+                    continue;
+                }
+                for (const Segment& sg : segs) {
+                    SegLayout L;
+                    const Task& t0 = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first)])];
+                    L.nI = static_cast<int>(t0.f.size());
+                    L.nC = static_cast<int>(t0.ck.size());
+                    L.TC = static_cast<int>(t0.terms.size());
+                    L.cmode.assign(static_cast<size_t>(L.nC), 0);
+                    for (int c = 0; c < L.nC; ++c) {
+                        bool all_inv = true, all_cached = true;
+                        for (int q = 0; q < sg.count; ++q) {
+                            const int k = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])].ck[static_cast<size_t>(c)];
+                            all_inv = all_inv && g.invariant(k);
+                            all_cached = all_cached && g.vc_index[static_cast<size_t>(k)] >= 0;
+                        }
+                        L.cmode[static_cast<size_t>(c)] = all_inv ? 0 : (all_cached ? 2 : 1);
+                    }
+                    L.SI = L.nI + 2 * L.TC;
+                    L.SD = 0;
+                    L.cpos.assign(static_cast<size_t>(L.nC), 0);
+                    for (int c = 0; c < L.nC; ++c) L.cpos[static_cast<size_t>(c)] = L.cmode[static_cast<size_t>(c)] ? L.SI++ : L.SD++;
+                    const int bi0 = static_cast<int>(rki.size()), bd0 = static_cast<int>(rkd.size());
+                    for (int q = 0; q < sg.count; ++q) {
+                        const Task& t = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])];
+                        std::vector<int> rec(static_cast<size_t>(L.SI), 0);
+                        std::copy(t.f.begin(), t.f.end(), rec.begin());
+                        for (int j = 0; j < L.TC; ++j) {
+                            rec[static_cast<size_t>(L.nI + 2 * j)] = t.terms[static_cast<size_t>(j)].first;
+                            rec[static_cast<size_t>(L.nI + 2 * j + 1)] = t.terms[static_cast<size_t>(j)].second;
+                        }
+                        for (int c = 0; c < L.nC; ++c) {
+                            const int k = t.ck[static_cast<size_t>(c)];
+                            const int m = L.cmode[static_cast<size_t>(c)];
+                            if (m == 0) rkd.push_back(g.c0(k));
+                            else rec[static_cast<size_t>(L.cpos[static_cast<size_t>(c)])] = m == 2 ? g.vc_index[static_cast<size_t>(k)] * 256 : k;
+                        }
+                        rki.insert(rki.end(), rec.begin(), rec.end());
+                    }
+                    rc << segment_code(sg.kind, sg.count, sg.indep != 0, bi0, bd0, L, "      ");
+                    ++segs_total;
+                }
+                rc << "    }\n";
+            }
+        }
+        return rc.str();
+    };
+    const std::string code_a = region_code(sa);
+    const std::string code_b = region_code(sb);
+    const size_t const_bytes = rki.size() * 4 + rkd.size() * 8 + static_cast<size_t>(s.consts) * 8;
+    if (const_bytes > 62 * 1024) {
+        fail = {13, "", "task tables (" + std::to_string(const_bytes) + " B) exceed constant memory"};
+        return false;
+    }
+
     // ---- source
     std::ostringstream o;
     const int nhot = static_cast<int>(g.hot_slots.size());
+    const long long Wl = lanes;
     o << "// generated by emtb200 codegen: " << s.nodes << " nodes, " << s.comps << " components, " << s.layers
-      << " layers, " << lanes << " lanes, " << G << " warps\n";
-
+      << " layers, " << lanes << " lanes, " << G << " warps, " << nt << " tasks, " << segs_total << " segments\n";
+    o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit; };\n";
-    o << "__device__ const int kHot[" << std::max(1, nhot) << "] = {";
-    for (int q = 0; q < nhot; ++q) o << (q ? "," : "") << g.hot_slots[static_cast<size_t>(q)];
-    if (nhot == 0) o << "0";
+    auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
+        o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
+        for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
+        if (v.empty()) o << "0";
+        o << "};\n";
+    };
+    o << "__constant__ double kC[" << std::max(1, s.consts) << "] = {";
+    for (int k = 0; k < s.consts; ++k) o << (k ? "," : "") << lit(g.c0(k));
+    if (s.consts == 0) o << "0.0";
     o << "};\n";
-    // derived + contrib slots materialised at save time
+    carr_i("__constant__", "kRi", rki);
+    o << "__constant__ double kRd[" << std::max<size_t>(1, rkd.size()) << "] = {";
+    for (size_t q = 0; q < rkd.size(); ++q) o << (q ? "," : "") << lit(rkd[q]);
+    if (rkd.empty()) o << "0.0";
+    o << "};\n";
+    std::vector<int> hot_arena(g.hot_slots.begin() + 1, g.hot_slots.end());
+    carr_i("__device__ const", "kHot", hot_arena);
     std::vector<int> dslot, dconst, cslot, chot, csign;
     for (int x = 0; x < s.extent; ++x) {
         if (g.cls[static_cast<size_t>(x)] == kDerived) {
@@ -787,60 +1144,74 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             csign.push_back(g.contrib_sign[static_cast<size_t>(x)]);
         }
     }
-    auto arr = [&](const char* name, const std::vector<int>& v) {
-        o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
-        for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
-        if (v.empty()) o << "0";
-        o << "};\n";
-    };
-    arr("kDerSlot", dslot);
-    arr("kDerConst", dconst);
-    arr("kConSlot", cslot);
-    arr("kConHot", chot);
-    arr("kConSign", csign);
-    const long long Wl = lanes;
+    carr_i("__device__ const", "kDerSlot", dslot);
+    carr_i("__device__ const", "kVC", g.vc_slots);
+    carr_i("__device__ const", "kChgSlot", g.chg_flag ? g.chg_slots : std::vector<int>());
+    carr_i("__device__ const", "kDerConst", dconst);
+    carr_i("__device__ const", "kConSlot", cslot);
+    carr_i("__device__ const", "kConHot", chot);
+    carr_i("__device__ const", "kConSign", csign);
+    o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
+      << "#define ST(o, v) (*(double*)(Sb + (o)) = (v))\n"
+      << "#define SGN(x, n) ((n) ? -(x) : (x))\n";
+    if (g.chg_flag)
+        o << "#define SETCHG(o, c) do { if ((c) != 0.0) needS[lane] = 1; } while (0)\n";
+    else
+        o << "#define SETCHG(o, c) ST(o, c)\n";
+    if (lu_smem)
+        o << "#define LU(x) LD(x)\n";
+    else
+        o << "#define LU(x) (A[(size_t)(x) * W_])\n";
+
+    // Refactorization in its own (non-inlined) function: its hundreds of
+    // temporaries must not raise the register pressure of the step loop.
+    if (knob("EMTB200_CG_NOINLINE", 0)) o << "__device__ __noinline__ int emt_refactor(double* __restrict__ S, double* __restrict__ A, const double* __restrict__ C,"
+      << " const bool live, const int lane, int* needS) {\n"
+      << "  int srow = -1; (void)C; (void)needS; (void)lane;\n"
+      << g.emit_refactor()
+      << "  return srow;\n}\n";
+    else o << "";
     o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * G << ", 1) emt_cg_kernel(const KArgs a) {\n"
       << "  extern __shared__ double sm[];\n"
       << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
-      << "  const int graw = blockIdx.x * 32 + lane; const bool live = graw < " << Wl << ";\n"
-      << "  const int gl = live ? graw : " << (Wl - 1) << ";\n"
+      << "  const int graw = blockIdx.x * 32 + lane; const bool live = graw < W_;\n"
+      << "  const int gl = live ? graw : (int)(W_ - 1);\n"
       << "  double* __restrict__ S = sm + lane;\n"
-      << "  int* serr = (int*)(sm + " << (static_cast<long long>(nhot) + (lu_smem ? static_cast<long long>(s.l_col.size() + s.u_col.size()) : 0)) * 32 << ");\n"
+      << "  char* __restrict__ Sb = (char*)S;\n"
+      << "  int* serr = (int*)(sm + " << static_cast<long long>(g.smem_slots()) * 32 << ");\n"
+      << "  int* needS = serr + 32; (void)needS;\n"
       << "  double* __restrict__ A = a.arena + gl;\n"
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
-      << "  for (int q = warp; q < " << nhot << "; q += " << G << ") S[q * 32] = A[(size_t)kHot[q] * " << Wl << "];\n";
+      << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+      << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * 32] = __ldg(C + (size_t)kVC[q] * W_);\n"
+      << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * 32] = A[(size_t)kHot[q] * W_];\n";
     if (lu_smem) {
         o << "  for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * 32] = A[(size_t)("
-          << s.l << " + q) * " << Wl << "];\n";
+          << s.l << " + q) * W_];\n";
         o << "  for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * 32] = A[(size_t)("
-          << s.u << " + q) * " << Wl << "];\n";
+          << s.u << " + q) * W_];\n";
     }
-    o << "  if (warp == 0) serr[lane] = 0x7fffffff;\n"
-      << "  __syncthreads();\n"
+    // watch slots not rewritten by region-A tasks (the dirty flag) are checked up front
+    std::set<int> written_a;
+    for (const Task& t : g.tasks)
+        if (t.region == 0)
+            for (int w : t.writes) written_a.insert(w);
+    o << "  __syncthreads();\n"
       << "  int it = 0;\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1;\n"
-      << "    (void)t; (void)bad; (void)srow;\n";
-    // Watch slots not rewritten by region-A tasks this step (the dirty flag, or
-    // slots set after the factorization point last step) are checked up front;
-    // switch updates raise wflag inside their own tasks.
-    {
-        std::set<int> written_a;
-        for (const Task& t : g.tasks)
-            if (t.region == 0)
-                for (int w : t.writes) written_a.insert(w);
-        o << "    if (warp == 0) { ";
-        for (int x : s.watch)
-            if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
-        o << "}\n";
-    }
-    emit_phases(o, sa, g.tasks, "    ", false);
+      << "    (void)t; (void)bad; (void)srow; (void)step;\n"
+      << "    if (warp == 0) { ";
+    for (int x : s.watch)
+        if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
+    o << "}\n";
+    o << code_a;
     o << "    if (__syncthreads_or(wflag)) {\n"
       << "      if (warp == 0) {\n"
-      << g.emit_refactor()
+      << (knob("EMTB200_CG_NOINLINE", 0) ? "        srow = emt_refactor(S, A, C, live, lane, needS);\n" : g.emit_refactor())
       << "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
       << "      }\n"
       << "      if (__syncthreads_or(srow >= 0 && live)) {\n"
@@ -849,7 +1220,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "        return;\n"
       << "      }\n"
       << "    }\n";
-    emit_phases(o, sb, g.tasks, "    ", false);
+    o << code_b;
     o << "    if (__syncthreads_or(bad != 0x7fffffff && live)) {\n"
       << "      if (bad != 0x7fffffff) atomicMin(&serr[lane], bad);\n"
       << "      __syncthreads();\n"
@@ -858,21 +1229,21 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      return;\n"
       << "    }\n"
       << "  }\n";
-    // save
+    // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
       << "  if (live) {\n"
-      << "    for (int q = warp; q < " << nhot << "; q += " << G << ") A[(size_t)kHot[q] * " << Wl << "] = S[q * 32];\n";
+      << "    for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * 32];\n";
     if (lu_smem) {
-        o << "    for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * " << Wl
-          << "] = S[(" << g.l_base_smem << " + q) * 32];\n";
-        o << "    for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * " << Wl
-          << "] = S[(" << g.u_base_smem << " + q) * 32];\n";
+        o << "    for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * W_] = S[("
+          << g.l_base_smem << " + q) * 32];\n";
+        o << "    for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * W_] = S[("
+          << g.u_base_smem << " + q) * 32];\n";
     }
     o << "    if (a.nsteps > 0) {\n"
-      << "      for (int q = warp; q < " << dslot.size() << "; q += " << G << ") A[(size_t)kDerSlot[q] * " << Wl
-      << "] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * " << Wl << "];\n"
+      << "      for (int q = warp; q < " << dslot.size() << "; q += " << G << ") A[(size_t)kDerSlot[q] * W_] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * W_];\n"
       << "      for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * 32]; "
-      << "A[(size_t)kConSlot[q] * " << Wl << "] = kConSign[q] > 0 ? h : -h; }\n"
+      << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
+      << "      for (int q = warp; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << G << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n"
       << "    }\n"
       << "  }\n"
       << "}\n";
@@ -885,12 +1256,12 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     out.phases_a = static_cast<int>(sa.phases.size());
     out.phases_b = static_cast<int>(sb.phases.size());
     out.tasks = static_cast<int>(nt);
-    std::ostringstream sum;
     long work = 0;
     for (const Task& t : g.tasks) work += t.cost;
-    sum << "tasks=" << nt << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem << " phasesA=" << sa.phases.size()
-        << " phasesB=" << sb.phases.size() << " warps=" << G << " est_span=" << static_cast<long>(span_a + span_b)
-        << " est_work=" << work;
+    std::ostringstream sum;
+    sum << (straight ? "straight " : "compact ") << "tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
+        << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
+        << " est_span=" << static_cast<long>(span_a + span_b) << " est_work=" << work;
     out.summary = sum.str();
     return true;
 }

@@ -20,6 +20,7 @@ struct CodegenOptions {
     int warps = 4;                  // warps per CTA (work partitions of one 32-lane group)
     size_t smem_budget = 227 * 1024;  // bytes of dynamic shared memory per CTA
     bool lu_in_smem = true;         // keep L/U factors on chip when they fit
+    int mode = 0;                   // 0 auto, 1 straight-line tasks, 2 compact per-type loops
 };
 
 struct GeneratedKernel {

@@ -707,7 +707,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     e->summary = "generic table-driven kernel, grid=" + std::to_string(e->grid) + " block=" + std::to_string(e->block);
     if (c.kernel != EMT_KERNEL_GENERIC) {
         CodegenOptions opt;
-        opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 4;
+        opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
         int dev_smem = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
         opt.smem_budget = static_cast<size_t>(dev_smem);

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 BITWISE = {"rc_discharge", "switched_dc_w3", "control_only", "diverging", "singular_islands"}
 
 
-KERNELS = {"specialised": engine.KERNEL_SPECIALISED, "generic": engine.KERNEL_GENERIC}
+KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}
 
 
 @pytest.mark.parametrize("kernel", sorted(KERNELS))

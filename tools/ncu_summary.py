@@ -78,13 +78,17 @@ def main():
     print(json.dumps(summ, indent=1))
     if a.traffic_json and summ["kernels"]:
         k = summ["kernels"][0]
-        rd = float(k["dram__bytes_read.sum"].split()[0])
-        wr = float(k["dram__bytes_write.sum"].split()[0])
-        unit = k["dram__bytes_read.sum"].split()[1] if len(k["dram__bytes_read.sum"].split()) > 1 else "byte"
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-        traffic = (rd + wr) * scale
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def nbytes(v):
+            num, unit = (v.split() + ["byte"])[:2]
+            return float(num) * scale.get(unit, 1)
+
+        traffic = nbytes(k["dram__bytes_read.sum"]) + nbytes(k["dram__bytes_write.sum"])
         info = {"dram_bytes_per_launch": traffic, "source": out, "kernel": k["name"],
                 "emt_steps_per_launch": a.emt_steps, "lanes": a.lanes}
+        if a.emt_steps:
+            info["dram_bytes_per_emt_step"] = traffic / a.emt_steps
         if a.bytes_per and a.emt_steps and a.lanes:
             info["algorithmic_bytes_per_launch"] = a.bytes_per * a.emt_steps * a.lanes
         json.dump(info, open(a.traffic_json, "w"), indent=1)
