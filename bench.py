@@ -3,10 +3,11 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Workload: 1000 scenarios (46 breakers x 22 fault times 0.10-0.31 s, first 1000,
-outage-major; cases.n1_scenarios) of the synthetic IEEE 39-bus EMT case
-(n = 85 nodes, m = 149 components, dt = 50 us), sharded contiguously over the
-N GPUs (one process per GPU under torchrun). One bench "step" = one launch of
+Workload: 1000 scenarios per GPU (46 breakers x 22 fault times 0.10-0.31 s,
+outage-major; sharding.n1_sweep — at N=1 exactly the BASELINE C3 sweep) of the
+synthetic IEEE 39-bus EMT case (n = 85 nodes, m = 149 components,
+dt = 50 us), in contiguous lane shards, one process per GPU under torchrun;
+weak scaling, no inter-GPU traffic but the final reductions / result gather. One bench "step" = one launch of
 the persistent step-loop kernel advancing every scenario by `--emt-steps`
 (default 1000) EMT passes, i.e. 50 ms of simulated time; the default K + W
 covers 1.15 s of simulated time.
@@ -49,11 +50,13 @@ def load_case(name="ieee39"):
     return s, st, ids
 
 
-def build_batch(scenarios: int):
-    from paper_1903_01081_b200 import cases
+def build_batch(scenarios: int, lo: int = 0, hi: int = -1):
+    """N-1 batch of lanes [lo, hi) of a `scenarios`-lane sweep (sharding.n1_sweep)."""
     from paper_1903_01081_b200 import schedule as sch
+    from paper_1903_01081_b200 import sharding
     s, st, ids = load_case("ieee39")
-    scen = [(f"sw{b:02d}", tf) for b, tf in cases.n1_scenarios(scenarios)]
+    hi = scenarios if hi < 0 else hi
+    scen = [(f"sw{b:02d}", tf) for b, tf in sharding.n1_sweep(scenarios)[lo:hi]]
     return sch.n1_batch(s, st, ids, scen), sch.parse_info(s)
 
 
@@ -150,15 +153,14 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = local
 
-    batch, info = build_batch(args.scenarios)
-    W = batch.width
-    lo = rank * W // world
-    hi = (rank + 1) * W // world
+    from paper_1903_01081_b200 import sharding
+    W = args.scenarios * world  # weak scaling: `--scenarios` per GPU, contiguous shards
+    lo, hi = sharding.shard_bounds(W, world, rank)
+    batch, info = build_batch(W, lo, hi)
     S = args.emt_steps
     total_steps = (args.warmup + args.steps) * S
 
-    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=W, device=dev,
-                        lane_begin=lo, lane_count=hi - lo)
+    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, device=dev)
     eng.reserve(total_steps)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -197,8 +199,7 @@ def run_ours(args):
     for k in range(e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=W, device=dev, lane_begin=lo,
-                           lane_count=hi - lo)
+        e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev)
         e2.reserve(S)
         e2.advance(S)
         w = e2.waves(0, S)
@@ -209,18 +210,25 @@ def run_ours(args):
             e2e_s.append(t1 - t0)
     e2e_local = statistics.median(e2e_s)
 
+    last = eng.waves(total_steps - S, S).values
     if world > 1:
-        t = torch.tensor([local_ms, e2e_local, float(st.factor_count)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_ms, e2e_max, fc = t.tolist()
-        # final result gather: per-rank waveform checksums (the only inter-GPU traffic)
-        chk = torch.tensor([float(np.sum(host_waves))], dtype=torch.float64, device=dev)
-        gathered = [torch.zeros_like(chk) for _ in range(world)]
-        dist.all_gather(gathered, chk)
+        max_ms = sharding.reduce_max(dist, local_ms, device=dev)
+        e2e_max = sharding.reduce_max(dist, e2e_local, device=dev)
+        # final result gather (the only inter-GPU traffic): per-rank digests + refactor steps
+        digests = sharding.gather_digests(dist, sharding.digest(last), world, device=dev)
+        steps_local = eng.refactor_steps()
+        mx = int(sharding.reduce_max(dist, float(len(steps_local)), device=dev))
+        pad = np.full(max(mx, 1), -1.0)
+        pad[: len(steps_local)] = steps_local
+        tt = torch.tensor(pad, dtype=torch.float64, device=dev)
+        parts = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(parts, tt)
+        fc = sharding.combine_factor_counts([[int(x) for x in p.cpu().numpy() if x >= 0] for p in parts])
     else:
-        max_ms, e2e_max, fc = local_ms, e2e_local, float(st.factor_count)
+        max_ms, e2e_max, fc = local_ms, e2e_local, st.factor_count
+        digests = sharding.digest(last)[None, :]
 
-    scen_steps = W * S * args.steps
+    scen_steps = W * S * args.steps  # all ranks' lanes
     value = scen_steps / (max_ms * 1e-3)
     clk = clocks.summary()
     if rank == 0:
@@ -236,7 +244,7 @@ def run_ours(args):
             per_step = json.load(open(tp)).get("dram_bytes_per_emt_step")
             traffic = per_step * S * lanes_local / json.load(open(tp)).get("lanes", lanes_local) if per_step else None
         cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
-        h2d = (batch.const_table[:, lo:hi].nbytes + info.extent * (hi - lo) * 8) / S
+        h2d = (batch.const_table.nbytes + batch.initial.nbytes) / S
         d2h = len(info.channels) * (hi - lo) * 8
         out = {
             "metric": "scenario-steps/sec for N-1 EMT batch",
@@ -247,11 +255,11 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": max_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "strong",
+            "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W,
+            "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "scenarios_per_gpu": args.scenarios,
                        "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
                        "components": info.comps, "case": "ieee39-synthetic (cases.py)",
                        "parallelism": f"scenario lanes sharded over {world} GPU(s), no per-step traffic",
@@ -261,6 +269,7 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "kernel": eng.summary[:200],
             "factor_count": int(fc),
+            "result_digest": digests.tolist(),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_scenario_step": bytes_per,
@@ -322,15 +331,16 @@ def run_reference(args):
     if rank != 0:
         return
     S = args.cpu_emt_steps_per_step
-    W, secs, procs = reference_measure(args.scenarios, S * args.steps, S * args.warmup, os.cpu_count() or 1)
+    W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup, os.cpu_count() or 1)
     value = W * S * args.steps / secs
     out = {
         "impl": "reference",
         "metric": "scenario-steps/sec for N-1 EMT batch",
         "value": value, "unit": "scenario-steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "emt_steps_per_bench_step": S,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "scenarios_per_gpu": args.scenarios,
+                   "emt_steps_per_bench_step": S,
                    "parallelism": f"{procs} host processes over contiguous lane shards"},
         "cpu_baseline": {"value": value, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
                          "sample": f"{W} scenarios x {S} EMT steps per bench step "
@@ -346,7 +356,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--scenarios", type=int, default=1000)
+    ap.add_argument("--scenarios", type=int, default=1000, help="scenarios per GPU (weak scaling)")
     ap.add_argument("--emt-steps", type=int, default=1000, help="EMT passes per bench step (one launch)")
     ap.add_argument("--cpu-emt-steps", type=int, default=8000, help="EMT passes in the cpu_baseline sample")
     ap.add_argument("--cpu-emt-steps-per-step", type=int, default=200,

@@ -143,6 +143,9 @@ emt_status emt_engine_read_state(emt_engine* engine, double* arena);
 emt_status emt_engine_read_events(emt_engine* engine, emt_switch_event* events, int32_t max,
                                   int32_t* count);
 emt_status emt_engine_stats(emt_engine* engine, emt_exec_stats* stats);
+/* Absolute pass indices at which some lane of this engine refactorised (up to
+ * max; total in *count). The union over shards is a sharded run's factor_count. */
+emt_status emt_engine_read_refactor_steps(emt_engine* engine, int32_t* steps, int32_t max, int32_t* count);
 
 /* Raw device pointer of the waveform store (rows x channels x lanes doubles)
  * and the CUDA stream the engine launches on (cudaStream_t as void*). */

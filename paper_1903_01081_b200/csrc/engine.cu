@@ -927,6 +927,24 @@ emt_status emt_codegen(const char* schedule_text, const double* const_table, int
     return EMT_OK;
 }
 
+emt_status emt_engine_read_refactor_steps(emt_engine* e, int32_t* steps, int32_t max, int32_t* count) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    std::vector<unsigned char> flags(static_cast<size_t>(std::max(1, e->rows)));
+    if (e->rows > 0)
+        CUDA_TRY(cudaMemcpy(flags.data(), e->d_refactored, static_cast<size_t>(e->rows), cudaMemcpyDeviceToHost));
+    const int first_step = e->step - e->rows;
+    int n = 0;
+    for (int r = 0; r < e->rows; ++r) {
+        if (!flags[static_cast<size_t>(r)]) continue;
+        if (steps != nullptr && n < max) steps[n] = first_step + r;
+        ++n;
+    }
+    if (count) *count = n;
+    return EMT_OK;
+}
+
 int32_t emt_engine_kernel(const emt_engine* e) { return e ? e->kernel_mode : 0; }
 const char* emt_engine_source(const emt_engine* e) { return e ? e->gen.source.c_str() : ""; }
 const char* emt_engine_summary(const emt_engine* e) { return e ? e->summary.c_str() : ""; }

@@ -108,6 +108,7 @@ def lib():
         L.emt_engine_device_waves.restype = vp
         L.emt_engine_stream.argtypes = [vp]
         L.emt_engine_stream.restype = vp
+        L.emt_engine_read_refactor_steps.argtypes = [vp, ip, ctypes.c_int32, ip]
         L.emt_engine_kernel.argtypes = [vp]
         L.emt_engine_kernel.restype = ctypes.c_int32
         L.emt_engine_source.argtypes = [vp]
@@ -125,7 +126,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_reserve", "emt_engine_advance", "emt_engine_sync", "emt_engine_read_waves",
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
-    "emt_codegen",
+    "emt_codegen", "emt_engine_read_refactor_steps",
 ]
 
 
@@ -303,6 +304,13 @@ class Engine:
         _check(lib().emt_engine_read_events(self._h, buf, max_events, ctypes.byref(n)))
         k = min(n.value, max_events)
         return np.array([(buf[i].step, buf[i].lane, buf[i].process) for i in range(k)], dtype=np.int32).reshape(-1, 3)
+
+    def refactor_steps(self, max_steps: int = 1 << 20) -> np.ndarray:
+        buf = np.zeros(max_steps, dtype=np.int32)
+        n = ctypes.c_int32()
+        _check(lib().emt_engine_read_refactor_steps(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                                     max_steps, ctypes.byref(n)))
+        return buf[: min(n.value, max_steps)].copy()
 
     def stats(self) -> ExecStats:
         st = _Stats()

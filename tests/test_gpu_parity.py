@@ -130,3 +130,20 @@ def test_specialised_equals_generic_bitwise_full_n1_sample():
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][2], out[1][2])
     assert bitwise_equal(out[0][3], out[1][3])
+
+
+def test_shard_refactor_steps_union_is_global_factor_count():
+    """Sharded engines: union of per-shard refactorisation passes == the full batch's factor_count."""
+    from paper_1903_01081_b200 import sharding
+    g = load_golden("ieee39_n1_w8")
+    full = engine.Engine(g.schedule, g.initial)
+    full.reserve(g.steps)
+    full.advance(g.steps, sync=True)
+    parts = []
+    for r in range(3):
+        lo, hi = sharding.shard_bounds(8, 3, r)
+        e = engine.Engine(g.schedule, g.initial, lane_begin=lo, lane_count=hi - lo)
+        e.reserve(g.steps)
+        e.advance(g.steps, sync=True)
+        parts.append(e.refactor_steps().tolist())
+    assert sharding.combine_factor_counts(parts) == full.stats().factor_count == g.factor_count
