@@ -190,25 +190,31 @@ def run_ours(args):
     local_ms = sum(per_launch_ms)
     st = eng.stats()
 
-    # ---- e2e through the C ABI with host buffers (create/H2D, advance, D2H), rank-local shard
-    e2e_steps = max(1, min(3, args.steps))
-    host_waves = np.zeros((S, len(info.channels) * (hi - lo)))
-    ct_host = np.ascontiguousarray(batch.const_table)
-    init_host = np.ascontiguousarray(batch.initial)
+    # ---- e2e through the public API with HOST buffers, rank-local shard. The engine
+    # (schedule parse + code generation + JIT, the analogue of compile_task, which the
+    # reference's timed_run also leaves outside its clock, proj/src/bench.cpp:157-181) is
+    # built once; every step then loads its batch from pinned host memory (H2D of the
+    # whole arena + constant table), runs S passes and streams the waveform rows back
+    # into pinned host memory chunk by chunk (D2H overlapped with the next chunk).
+    e2e_steps = max(3, min(5, args.steps))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    ct_host = pin(batch.const_table)
+    init_host = pin(batch.initial)
+    host_waves = torch.empty((S, len(info.channels) * (hi - lo)), dtype=torch.float64, pin_memory=True).numpy()
+    e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev)
+    e2.reserve(S)
     e2e_s = []
     for k in range(e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev)
-        e2.reserve(S)
-        e2.advance(S)
-        w = e2.waves(0, S)
-        host_waves[:] = w.values
-        e2.close()
+        e2.load(init_host, ct_host)
+        e2.run(S, host_waves, chunk=args.e2e_chunk)
         t1 = time.perf_counter()
-        if k > 0:  # first call warms the module / allocator
+        if k > 0:  # first call warms the copy stream / events
             e2e_s.append(t1 - t0)
     e2e_local = statistics.median(e2e_s)
+    e2e_digest_ok = bool(np.array_equal(host_waves, eng.waves(0, S).values))
+    e2.close()
 
     last = eng.waves(total_steps - S, S).values
     if world > 1:
@@ -244,8 +250,8 @@ def run_ours(args):
             per_step = json.load(open(tp)).get("dram_bytes_per_emt_step")
             traffic = per_step * S * lanes_local / json.load(open(tp)).get("lanes", lanes_local) if per_step else None
         cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
-        h2d = (batch.const_table.nbytes + batch.initial.nbytes) / S
-        d2h = len(info.channels) * (hi - lo) * 8
+        h2d = batch.const_table.nbytes + batch.initial.nbytes  # per bench step (S passes)
+        d2h = S * len(info.channels) * (hi - lo) * 8
         out = {
             "metric": "scenario-steps/sec for N-1 EMT batch",
             "value": value,
@@ -265,7 +271,10 @@ def run_ours(args):
                        "parallelism": f"scenario lanes sharded over {world} GPU(s), no per-step traffic",
                        "l2": "flushed (256 MiB write) between timed launches"},
             "e2e": {"value": W * S / e2e_max, "unit": "scenario-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "note": "engine create + H2D, advance, waveform D2H per call"},
+                    "d2h_bytes_per_step": d2h, "matches_device_run": e2e_digest_ok,
+                    "note": "per step: Engine.load (H2D arena + const table from pinned host) + Engine.run "
+                            f"(S passes, waveform rows D2H to pinned host in {args.e2e_chunk}-pass chunks overlapped "
+                            "with compute); engine built once outside the clock (host wall time, median)"},
             "gpu_launches": args.steps,
             "kernel": eng.summary[:200],
             "factor_count": int(fc),
@@ -361,6 +370,7 @@ def main():
     ap.add_argument("--cpu-emt-steps", type=int, default=8000, help="EMT passes in the cpu_baseline sample")
     ap.add_argument("--cpu-emt-steps-per-step", type=int, default=200,
                     help="EMT passes per bench step in the reference arm")
+    ap.add_argument("--e2e-chunk", type=int, default=100, help="passes per launch in the e2e streaming run")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

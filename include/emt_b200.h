@@ -39,6 +39,7 @@ typedef enum emt_status {
     EMT_NON_FINITE_STATE = 7,   /* |v| > divergence limit, proj/src/exec.cpp:229-237 */
     EMT_SINGULAR_MATRIX = 8,    /* pivot check, proj/src/sparse.cpp:135-143 */
     EMT_DIMENSION_MISMATCH = 10,/* initial.size() != extent*width, proj/src/exec.cpp:340-346 */
+    EMT_TOPOLOGY_MISMATCH = 12, /* batch not isomorphic to the compiled one (cf. vectorize, proj/src/cgm.cpp:367) */
     EMT_CAPACITY_EXCEEDED = 13, /* arena does not fit the device plan */
     EMT_UNKNOWN_KIND = 14,      /* unregistered kernel code, proj/src/exec.cpp:37-41 */
     EMT_NON_POSITIVE_INPUT = 20,/* steps < 0, width < 1, ... */
@@ -132,6 +133,26 @@ emt_status emt_engine_reserve(emt_engine* engine, int32_t capacity_steps);
  * synchronising call (emt_engine_sync / read / stats). */
 emt_status emt_engine_advance(emt_engine* engine, int32_t steps, int32_t sync);
 emt_status emt_engine_sync(emt_engine* engine);
+
+/* Reloads the resident batch from host buffers (H2D on the engine's stream,
+ * asynchronous w.r.t. the host when the buffers are pinned) and rewinds it to
+ * pass 0: `initial` is the whole batch's arena (extent*width doubles, the
+ * width the engine was created with; this engine copies its lane slice) and
+ * `const_table` (may be NULL = keep) its consts*width constant table. This is
+ * the per-job input of interpret() (proj/src/exec.cpp:358 copies `initial`)
+ * without re-running the code generator. A const table whose lane-invariant
+ * slots differ from the ones the specialised kernel compiled in is rejected
+ * with EMT_TOPOLOGY_MISMATCH (create a new engine for it). */
+emt_status emt_engine_load(emt_engine* engine, const double* initial, int64_t initial_len,
+                           const double* const_table);
+
+/* Runs `steps` passes in launches of `chunk` passes (<= 0: auto) and, when
+ * `waves` is not NULL, streams each finished chunk's rows to `waves`
+ * (steps*channels*lanes doubles, WaveformSet layout of this engine's lanes)
+ * on a copy stream while the next chunk computes. Returns after the last row
+ * has landed; errors as emt_engine_sync. Grows the waveform store as needed
+ * (SURVEY.md §8(b) emt_run). */
+emt_status emt_engine_run(emt_engine* engine, int32_t steps, int32_t chunk, double* waves);
 
 /* Host copies of recorded rows [row0, row0+rows) (WaveformSet layout, this
  * engine's lanes only) and their times. */

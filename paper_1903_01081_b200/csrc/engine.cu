@@ -428,7 +428,10 @@ struct emt_engine {
     int device = 0;
     int lane_begin = 0;
     int W = 1;  // lanes owned
+    int width = 1;  // lanes of the whole batch (the caller's arena / const-table width)
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // D2H of finished waveform chunks (emt_engine_run)
+    std::vector<cudaEvent_t> chunk_done;
     DevPlan plan{};
     std::vector<void*> allocations;
     size_t smem_bytes = 0;
@@ -457,6 +460,8 @@ struct emt_engine {
         for (void* p : allocations) cudaFree(p);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
+        for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -660,6 +665,31 @@ emt_status check_lane_errors(emt_engine* e) {
                                      std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
 }
 
+
+/// Grows the waveform store to `capacity_steps` rows, keeping recorded rows.
+emt_status emt_engine_reserve_keep(emt_engine* e, int capacity_steps) {
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
+    if (capacity_steps <= e->capacity) return EMT_OK;
+    const size_t row = static_cast<size_t>(e->plan.nch) * e->W;
+    double* w = nullptr;
+    unsigned char* f = nullptr;
+    CUDA_TRY(cudaMalloc(&w, std::max<size_t>(8, row * capacity_steps * sizeof(double))));
+    CUDA_TRY(cudaMalloc(&f, static_cast<size_t>(capacity_steps)));
+    CUDA_TRY(cudaMemset(f, 0, static_cast<size_t>(capacity_steps)));
+    if (e->rows > 0) {
+        CUDA_TRY(cudaMemcpy(w, e->d_waves, row * e->rows * sizeof(double), cudaMemcpyDeviceToDevice));
+        CUDA_TRY(cudaMemcpy(f, e->d_refactored, static_cast<size_t>(e->rows), cudaMemcpyDeviceToDevice));
+    }
+    if (e->d_waves) cudaFree(e->d_waves);
+    if (e->d_refactored) cudaFree(e->d_refactored);
+    e->d_waves = w;
+    e->d_refactored = f;
+    e->capacity = capacity_steps;
+    return EMT_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -688,6 +718,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     if (cfg != nullptr) c = *cfg;
     e->device = c.device;
     e->lane_begin = c.lane_begin;
+    e->width = width;
     e->W = c.lane_count > 0 ? c.lane_count : width - c.lane_begin;
     if (e->lane_begin < 0 || e->W < 1 || e->lane_begin + e->W > width)
         return set_error(EMT_NON_POSITIVE_INPUT, "lane range outside the batch");
@@ -891,6 +922,86 @@ emt_status emt_engine_stats(emt_engine* e, emt_exec_stats* stats) {
     stats->switch_events = n;
     stats->kernel_launches = e->launches;
     return EMT_OK;
+}
+
+emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial_len, const double* const_table) {
+    if (e == nullptr || initial == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    const Schedule& s = e->sched;
+    if (initial_len != static_cast<int64_t>(s.extent) * e->width)
+        return set_error(EMT_DIMENSION_MISMATCH, "initial state size " + std::to_string(initial_len) +
+                                                     " does not match extent " + std::to_string(s.extent) +
+                                                     " x width " + std::to_string(e->width));
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
+    const size_t W = static_cast<size_t>(e->W), width = static_cast<size_t>(e->width), lb = static_cast<size_t>(e->lane_begin);
+    if (const_table != nullptr) {
+        // The specialised kernel compiled every lane-invariant constant in as an
+        // immediate: a new batch may only change the lane-varying ones.
+        if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
+            for (int k = 0; k < s.consts; ++k) {
+                const double* old = e->host_ctab.data() + static_cast<size_t>(k) * W;
+                bool inv = true;
+                for (size_t l = 1; l < W && inv; ++l) inv = std::memcmp(&old[l], &old[0], sizeof(double)) == 0;
+                if (!inv) continue;
+                const double* row = const_table + static_cast<size_t>(k) * width + lb;
+                for (size_t l = 0; l < W; ++l)
+                    if (std::memcmp(&row[l], &old[0], sizeof(double)) != 0)
+                        return set_error(EMT_TOPOLOGY_MISMATCH, "constant slot " + std::to_string(k) +
+                                                                    " is compiled into the specialised kernel; "
+                                                                    "create a new engine for this batch");
+            }
+        }
+        for (int k = 0; k < s.consts; ++k)
+            std::memcpy(e->host_ctab.data() + static_cast<size_t>(k) * W, const_table + static_cast<size_t>(k) * width + lb,
+                        W * sizeof(double));
+        CUDA_TRY(cudaMemcpy2DAsync(const_cast<double*>(e->plan.ctab), W * sizeof(double), const_table + lb,
+                                   width * sizeof(double), W * sizeof(double), static_cast<size_t>(s.consts),
+                                   cudaMemcpyHostToDevice, e->stream));
+    }
+    // arena lane slice: one strided (2D) copy, contiguous when the engine owns every lane
+    CUDA_TRY(cudaMemcpy2DAsync(e->plan.arena, W * sizeof(double), initial + lb, width * sizeof(double),
+                               W * sizeof(double), static_cast<size_t>(s.extent), cudaMemcpyHostToDevice, e->stream));
+    for (size_t l = 0; l < W; ++l) e->initial_fcount[l] = initial[static_cast<size_t>(s.fcount) * width + lb + l];
+    e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
+    CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
+    CUDA_TRY(cudaMemsetAsync(e->plan.n_events, 0, sizeof(int), e->stream));
+    if (e->d_refactored) CUDA_TRY(cudaMemsetAsync(e->d_refactored, 0, static_cast<size_t>(std::max(1, e->capacity)), e->stream));
+    e->step = 0;
+    e->rows = 0;
+    e->failed = 0;
+    return EMT_OK;
+}
+
+emt_status emt_engine_run(emt_engine* e, int32_t steps, int32_t chunk, double* waves) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
+    if (e->rows + steps > e->capacity) EMT_TRY(emt_engine_reserve_keep(e, e->rows + steps));
+    if (chunk <= 0) chunk = std::max(1, std::min<int>(steps, 256));
+    CUDA_TRY(cudaSetDevice(e->device));
+    if (waves != nullptr && e->copy_stream == nullptr)
+        CUDA_TRY(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    const int nchunks = (steps + chunk - 1) / chunk;
+    while (waves != nullptr && static_cast<int>(e->chunk_done.size()) < std::min(nchunks, 64)) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        e->chunk_done.push_back(ev);
+    }
+    const size_t row = static_cast<size_t>(e->plan.nch) * e->W;
+    for (int c = 0; c < nchunks; ++c) {
+        const int n = std::min(chunk, steps - c * chunk);
+        const int r0 = e->rows;
+        EMT_TRY(emt_engine_advance(e, n, 0));
+        if (waves == nullptr) continue;
+        // chunk c's rows go to the host while chunk c+1 computes
+        cudaEvent_t ev = e->chunk_done[static_cast<size_t>(c) % e->chunk_done.size()];
+        CUDA_TRY(cudaEventRecord(ev, e->stream));
+        CUDA_TRY(cudaStreamWaitEvent(e->copy_stream, ev, 0));
+        CUDA_TRY(cudaMemcpyAsync(waves + row * static_cast<size_t>(c) * chunk, e->d_waves + row * r0,
+                                 row * n * sizeof(double), cudaMemcpyDeviceToHost, e->copy_stream));
+    }
+    if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
+    return emt_engine_sync(e);
 }
 
 emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,

@@ -109,6 +109,8 @@ def lib():
         L.emt_engine_stream.argtypes = [vp]
         L.emt_engine_stream.restype = vp
         L.emt_engine_read_refactor_steps.argtypes = [vp, ip, ctypes.c_int32, ip]
+        L.emt_engine_load.argtypes = [vp, dp, ctypes.c_int64, dp]
+        L.emt_engine_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
         L.emt_engine_kernel.argtypes = [vp]
         L.emt_engine_kernel.restype = ctypes.c_int32
         L.emt_engine_source.argtypes = [vp]
@@ -126,7 +128,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_reserve", "emt_engine_advance", "emt_engine_sync", "emt_engine_read_waves",
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
-    "emt_codegen", "emt_engine_read_refactor_steps",
+    "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
 ]
 
 
@@ -282,6 +284,23 @@ class Engine:
     def advance(self, steps: int, sync: bool = False) -> None:
         _check(lib().emt_engine_advance(self._h, int(steps), 1 if sync else 0))
         self.rows += steps
+
+    def load(self, initial: np.ndarray, const_table: Optional[np.ndarray] = None) -> None:
+        """New batch from host buffers (whole-batch arena / const table); rewinds to pass 0.
+        Pass pinned arrays (e.g. torch pin_memory().numpy()) for asynchronous H2D."""
+        init = np.ascontiguousarray(initial, dtype=np.float64)
+        ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
+        _check(lib().emt_engine_load(self._h, _dp(init), init.size, _dp(ct) if ct is not None else None))
+        self.rows = 0
+
+    def run(self, steps: int, out: Optional[np.ndarray] = None, chunk: int = 0) -> Optional[np.ndarray]:
+        """Advance `steps` passes, streaming waveform rows into `out` (steps x channels*lanes,
+        C-contiguous float64; pinned for overlap) chunk by chunk while the next chunk computes."""
+        if out is not None:
+            assert out.dtype == np.float64 and out.flags.c_contiguous and out.size >= steps * self.channels * self.lanes
+        _check(lib().emt_engine_run(self._h, int(steps), int(chunk), _dp(out) if out is not None else None))
+        self.rows += steps
+        return out
 
     def sync(self) -> None:
         _check(lib().emt_engine_sync(self._h))

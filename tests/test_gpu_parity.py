@@ -147,3 +147,57 @@ def test_shard_refactor_steps_union_is_global_factor_count():
         e.advance(g.steps, sync=True)
         parts.append(e.refactor_steps().tolist())
     assert sharding.combine_factor_counts(parts) == full.stats().factor_count == g.factor_count
+
+
+@pytest.mark.parametrize("kernel", sorted(KERNELS))
+def test_load_run_streams_same_waves_as_advance(kernel):
+    """emt_engine_load + emt_engine_run (chunked launches, D2H overlapped) == one-shot interpret."""
+    g = load_golden("feeder_w4")
+    one = engine.interpret(g.schedule, g.initial, 700, kernel=KERNELS[kernel])
+    eng = engine.Engine(g.schedule, g.initial, kernel=KERNELS[kernel])
+    out = np.zeros((700, eng.channels * eng.lanes))
+    eng.run(700, out, chunk=64)
+    assert bitwise_equal(out, one.values)
+    # reload the same batch: rewinds to pass 0, same bits again; odd chunking
+    eng.load(g.initial)
+    out2 = np.zeros_like(out)
+    eng.run(700, out2, chunk=333)
+    assert bitwise_equal(out2, one.values)
+
+
+def test_load_new_lane_varying_constants_equals_fresh_engine():
+    """A reloaded N-1 batch with other fault times (lane-varying constants) == a fresh engine on it."""
+    import bench
+    from paper_1903_01081_b200 import schedule as sch
+    s, st, ids = bench.load_case("ieee39")
+    pick = ["sw03", "sw07", "sw19", "sw40"] * 8
+    a = sch.n1_batch(s, st, ids, [(b, 0.004 + 0.0003 * k) for k, b in enumerate(pick)])
+    b = sch.n1_batch(s, st, ids, [(b, 0.011 + 0.0007 * k) for k, b in enumerate(pick)])
+    eng = engine.Engine(a.schedule, a.initial, const_table=a.const_table, width=a.width)
+    assert eng.kernel == engine.KERNEL_SPECIALISED
+    eng.load(b.initial, b.const_table)
+    out = np.zeros((1200, eng.channels * eng.lanes))
+    eng.run(1200, out, chunk=100)
+    fresh = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width)
+    fresh.reserve(1200)
+    fresh.advance(1200)
+    assert bitwise_equal(out, fresh.waves().values)
+    assert np.array_equal(eng.events(), fresh.events())
+    assert len(fresh.events()) == len(pick)
+    assert eng.stats().factor_count == fresh.stats().factor_count
+
+
+def test_load_rejects_changed_compiled_constant():
+    g = load_golden("ieee39_n1_w8")
+    eng = engine.Engine(g.schedule, g.initial)
+    assert eng.kernel == engine.KERNEL_SPECIALISED
+    ct = np.array([float(x) for ln in g.schedule.splitlines() if ln.startswith("CONST ") for x in ln.split()[2:]])
+    ct = ct.reshape(-1, g.width) if ct.size % g.width == 0 else None
+    if ct is None:
+        pytest.skip("const table layout not row-per-slot")
+    inv = [k for k in range(ct.shape[0]) if np.all(ct[k] == ct[k, 0])]
+    ct2 = ct.copy()
+    ct2[inv[0]] += 1.0
+    with pytest.raises(engine.EmtError) as ei:
+        eng.load(g.initial, ct2)
+    assert ei.value.code == "TopologyMismatch"
