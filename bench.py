@@ -50,18 +50,42 @@ def load_case(name="ieee39"):
     return s, st, ids
 
 
-def build_batch(scenarios: int, lo: int = 0, hi: int = -1):
-    """N-1 batch of lanes [lo, hi) of a `scenarios`-lane sweep (sharding.n1_sweep)."""
+WORKLOADS = {
+    "c3": ("ieee39-n1-sweep (BASELINE C3)", "ieee39", 1000),
+    "c5": ("feeder33-pv-sweep shared G (BASELINE C5)", "feeder33_pv3", 4096),
+    "c2": ("ieee39 single scenario (BASELINE C2)", "ieee39", 1),
+}
+
+
+METRIC = {"c3": "scenario-steps/sec for N-1 EMT batch", "c5": "scenario-steps/sec for shared-G EMT batch",
+          "c2": "us per time step on single case"}
+
+
+def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3"):
+    """Lanes [lo, hi) of a `scenarios`-lane sweep: C3 = N-1 breaker outages
+    (sharding.n1_sweep), C5 = PV irradiance x temperature grid (shared G,
+    gen_scenarios rows, proj/src/bench.cpp:119-149), C2 = the base case."""
     from paper_1903_01081_b200 import schedule as sch
     from paper_1903_01081_b200 import sharding
-    s, st, ids = load_case("ieee39")
     hi = scenarios if hi < 0 else hi
+    if workload == "c5":
+        s, st, _ = load_case("feeder33_pv3")
+        pvm = json.load(open(os.path.join(DATA, "feeder33_pv3.json")))["pv_sweep"]
+        n = max(1, int(round(scenarios ** 0.5)))
+        grid = sch.pv_grid(n, (scenarios + n - 1) // n)
+        while len(grid) < scenarios:  # weak scaling beyond a square grid: shifted repeats
+            grid += [(i + 1e-3 * len(grid), t) for i, t in grid[: scenarios - len(grid)]]
+        return sch.pv_sweep_batch(s, st, pvm, grid[lo:hi]), sch.parse_info(s)
+    s, st, ids = load_case("ieee39")
+    if workload == "c2":
+        return sch.n1_batch(s, st, ids, [("sw00", 1e9)] * (hi - lo)), sch.parse_info(s)
     scen = [(f"sw{b:02d}", tf) for b, tf in sharding.n1_sweep(scenarios)[lo:hi]]
     return sch.n1_batch(s, st, ids, scen), sch.parse_info(s)
 
 
-def algorithmic_bytes_per_scenario_step(info, batch) -> int:
-    """B = 8 [2 (n + m + S_blk + 2 N_sw + N_latch) + F_lane + C_var + K]."""
+def algorithmic_bytes_per_scenario_step(info, batch, shared_g: bool = False) -> float:
+    """SURVEY.md §8(d): B = 8 [2 (n + m + S_blk + 2 N_sw + N_latch) + F_lane + C_var + K];
+    F_lane = l_nnz + u_nnz for per-lane factors, else 0 plus the shared factor 8 (l+u) / W."""
     text = batch.schedule
     lines = text.splitlines()
     mat = next(l for l in lines if l.startswith("MATRIX")).split()
@@ -73,7 +97,9 @@ def algorithmic_bytes_per_scenario_step(info, batch) -> int:
     ct = batch.const_table
     c_var = int(np.sum(np.any(ct != ct[:, :1], axis=1)))
     k = len(info.channels)
-    return 8 * (2 * (info.nodes + info.comps + s_blk + 2 * n_sw + n_latch) + (lnnz + unnz) + c_var + k)
+    f_lane = 0 if shared_g else lnnz + unnz
+    shared = 8.0 * (lnnz + unnz) / batch.width if shared_g else 0.0
+    return 8 * (2 * (info.nodes + info.comps + s_blk + 2 * n_sw + n_latch) + f_lane + c_var + k) + shared
 
 
 class ClockSampler:
@@ -154,13 +180,17 @@ def run_ours(args):
     dev = local
 
     from paper_1903_01081_b200 import sharding
+    wl_name, _, _ = WORKLOADS[args.workload]
     W = args.scenarios * world  # weak scaling: `--scenarios` per GPU, contiguous shards
     lo, hi = sharding.shard_bounds(W, world, rank)
-    batch, info = build_batch(W, lo, hi)
+    batch, info = build_batch(W, lo, hi, args.workload)
     S = args.emt_steps
     total_steps = (args.warmup + args.steps) * S
 
-    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, device=dev)
+    kern = {"auto": engine.KERNEL_AUTO, "specialised": engine.KERNEL_SPECIALISED,
+            "generic": engine.KERNEL_GENERIC}[args.kernel]
+    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, device=dev,
+                        kernel=kern, warps=args.warps)
     eng.reserve(total_steps)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -196,25 +226,28 @@ def run_ours(args):
     # built once; every step then loads its batch from pinned host memory (H2D of the
     # whole arena + constant table), runs S passes and streams the waveform rows back
     # into pinned host memory chunk by chunk (D2H overlapped with the next chunk).
-    e2e_steps = max(3, min(5, args.steps))
-    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-    ct_host = pin(batch.const_table)
-    init_host = pin(batch.initial)
-    host_waves = torch.empty((S, len(info.channels) * (hi - lo)), dtype=torch.float64, pin_memory=True).numpy()
-    e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev)
-    e2.reserve(S)
-    e2e_s = []
-    for k in range(e2e_steps + 1):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e2.load(init_host, ct_host)
-        e2.run(S, host_waves, chunk=args.e2e_chunk)
-        t1 = time.perf_counter()
-        if k > 0:  # first call warms the copy stream / events
-            e2e_s.append(t1 - t0)
-    e2e_local = statistics.median(e2e_s)
-    e2e_digest_ok = bool(np.array_equal(host_waves, eng.waves(0, S).values))
-    e2.close()
+    e2e_local, e2e_digest_ok = float('nan'), None
+    if not args.skip_e2e:
+        e2e_steps = max(3, min(5, args.steps))
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        ct_host = pin(batch.const_table)
+        init_host = pin(batch.initial)
+        host_waves = torch.empty((S, len(info.channels) * (hi - lo)), dtype=torch.float64, pin_memory=True).numpy()
+        e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev,
+                           kernel=kern, warps=args.warps)
+        e2.reserve(S)
+        e2e_s = []
+        for k in range(e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2.load(init_host, ct_host)
+            e2.run(S, host_waves, chunk=args.e2e_chunk)
+            t1 = time.perf_counter()
+            if k > 0:  # first call warms the copy stream / events
+                e2e_s.append(t1 - t0)
+        e2e_local = statistics.median(e2e_s)
+        e2e_digest_ok = bool(np.array_equal(host_waves, eng.waves(0, S).values))
+        e2.close()
 
     last = eng.waves(total_steps - S, S).values
     if world > 1:
@@ -240,7 +273,7 @@ def run_ours(args):
     if rank == 0:
         peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
         peak = float(peaks.get("hbm_gbs", FALLBACK_HBM))
-        bytes_per = algorithmic_bytes_per_scenario_step(info, batch)
+        bytes_per = algorithmic_bytes_per_scenario_step(info, batch, shared_g=args.workload == "c5")
         avg_launch_s = (local_ms / args.steps) * 1e-3
         lanes_local = hi - lo
         achieved = bytes_per * lanes_local * S / avg_launch_s / 1e9
@@ -252,25 +285,29 @@ def run_ours(args):
         cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
         h2d = batch.const_table.nbytes + batch.initial.nbytes  # per bench step (S passes)
         d2h = S * len(info.channels) * (hi - lo) * 8
+        metric, unit, hib, val, e2e_val = (METRIC[args.workload], "scenario-steps/s", True, value, W * S / e2e_max)
+        if args.workload == "c2":  # latency of one scenario: µs per EMT time step
+            metric, unit, hib = "us per time step on single case", "us/step", False
+            val, e2e_val = 1e3 * max_ms / (args.steps * S), 1e6 * e2e_max / S
         out = {
-            "metric": "scenario-steps/sec for N-1 EMT batch",
-            "value": value,
-            "unit": "scenario-steps/s",
+            "metric": metric,
+            "value": val,
+            "unit": unit,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True,
+            "higher_is_better": hib,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "scenarios_per_gpu": args.scenarios,
+            "config": {"workload": wl_name, "scenarios": W, "scenarios_per_gpu": args.scenarios,
                        "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
-                       "components": info.comps, "case": "ieee39-synthetic (cases.py)",
+                       "components": info.comps, "case": WORKLOADS[args.workload][1],
                        "parallelism": f"scenario lanes sharded over {world} GPU(s), no per-step traffic",
                        "l2": "flushed (256 MiB write) between timed launches"},
-            "e2e": {"value": W * S / e2e_max, "unit": "scenario-steps/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "matches_device_run": e2e_digest_ok,
                     "note": "per step: Engine.load (H2D arena + const table from pinned host) + Engine.run "
                             f"(S passes, waveform rows D2H to pinned host in {args.e2e_chunk}-pass chunks overlapped "
@@ -309,11 +346,11 @@ def _shard(batch, lo, hi):
     return sch.widen_text(batch.schedule, ct), np.ascontiguousarray(init)
 
 
-def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: int):
+def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: int, workload: str = "c3"):
     """emtgrid::interpret (the reference, unmodified) on contiguous lane shards, one
     process per host core; returns (lanes, max step-loop seconds)."""
     import multiprocessing as mp
-    batch, info = build_batch(scenarios)
+    batch, info = build_batch(scenarios, workload=workload)
     W = batch.width
     procs = max(1, min(procs, W))
     bounds = [(p * W // procs, (p + 1) * W // procs) for p in range(procs)]
@@ -328,8 +365,12 @@ def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: in
 
 
 def cpu_baseline(args):
-    steps = args.cpu_emt_steps
-    W, secs, procs = reference_measure(args.scenarios, steps, 20, os.cpu_count() or 1)
+    steps = args.cpu_emt_steps if args.workload != "c2" else 20000
+    W, secs, procs = reference_measure(args.scenarios, steps, 20, os.cpu_count() or 1, args.workload)
+    if args.workload == "c2":
+        return {"value": 1e6 * secs / steps, "unit": "us/step", "cores": 1, "kind": "reference",
+                "sample": f"1 scenario x {steps} EMT steps (after 20 warm-up), emtgrid::interpret "
+                          "(oracle/_ref/libemtref.so), single thread"}
     return {"value": W * steps / secs, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
             "sample": f"{W} scenarios x {steps} EMT steps (after 20 warm-up), emtgrid::interpret on "
                       f"{procs} contiguous lane shards, one process per core (oracle/_ref/libemtref.so)"}
@@ -340,21 +381,24 @@ def run_reference(args):
     if rank != 0:
         return
     S = args.cpu_emt_steps_per_step
-    W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup, os.cpu_count() or 1)
-    value = W * S * args.steps / secs
+    W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup, os.cpu_count() or 1,
+                                       args.workload)
+    metric, unit, hib, value = METRIC[args.workload], "scenario-steps/s", True, W * S * args.steps / secs
+    if args.workload == "c2":
+        metric, unit, hib, value = "us per time step on single case", "us/step", False, 1e6 * secs / (S * args.steps)
     out = {
         "impl": "reference",
-        "metric": "scenario-steps/sec for N-1 EMT batch",
-        "value": value, "unit": "scenario-steps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+        "metric": metric,
+        "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": hib,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "ieee39-n1-sweep (BASELINE C3)", "scenarios": W, "scenarios_per_gpu": args.scenarios,
+        "config": {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": args.scenarios,
                    "emt_steps_per_bench_step": S,
                    "parallelism": f"{procs} host processes over contiguous lane shards"},
-        "cpu_baseline": {"value": value, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": "reference",
                          "sample": f"{W} scenarios x {S} EMT steps per bench step "
                                    f"({args.warmup} warm-up + {args.steps} timed), emtgrid::interpret"},
-        "e2e": {"value": value, "unit": "scenario-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
@@ -365,16 +409,23 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--scenarios", type=int, default=1000, help="scenarios per GPU (weak scaling)")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3",
+                    help="c3 = IEEE-39 N-1 sweep (headline), c5 = feeder PV shared-G sweep, c2 = single scenario")
+    ap.add_argument("--scenarios", type=int, default=None, help="scenarios per GPU (weak scaling)")
     ap.add_argument("--emt-steps", type=int, default=1000, help="EMT passes per bench step (one launch)")
     ap.add_argument("--cpu-emt-steps", type=int, default=8000, help="EMT passes in the cpu_baseline sample")
     ap.add_argument("--cpu-emt-steps-per-step", type=int, default=200,
                     help="EMT passes per bench step in the reference arm")
     ap.add_argument("--e2e-chunk", type=int, default=100, help="passes per launch in the e2e streaming run")
+    ap.add_argument("--kernel", choices=["auto", "specialised", "generic"], default="auto")
+    ap.add_argument("--warps", type=int, default=0, help="specialised kernel: warps per 32-lane group (0 = auto)")
+    ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.scenarios is None:
+        args.scenarios = WORKLOADS[args.workload][2]
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -32,7 +32,9 @@ enum {
 /* KernelId (proj/include/emtgrid/kernels.hpp:36-59) */
 enum {
     K_RES = 0, K_IND, K_CAP, K_SRL, K_VSRC, K_ISRC, K_CSRC, K_SW, K_INJ, K_FACT, K_SOLVE,
-    K_GAIN, K_SUM, K_INTEG, K_LAG, K_LIM, K_PI, K_CMP, K_CONST, K_DELAY, K_COUNT
+    K_GAIN, K_SUM, K_INTEG, K_LAG, K_LIM, K_PI, K_CMP, K_CONST, K_DELAY,
+    K_BERG, /* extension (not in the reference): Bergeron line end, see case K_BERG */
+    K_COUNT
 };
 
 typedef struct {
@@ -523,6 +525,38 @@ static int run_proc(eng_t* e, const proc_t* p, double t, int step, char* err, in
         for (int l = 0; l < w; ++l) {
             g[l] = 0.0;
             h[l] = par[l] * (p->in_count > 3 ? rd(e, in[3], l) : 0.0);
+        }
+        break;
+    }
+    case K_BERG: {
+        /* Lossless Bergeron line end (EXTENSION: the reference has no line model,
+         * SURVEY.md §0; parity unpinned, checked analytically in tests/test_bergeron.py).
+         * Norton form like a current source (g = 0 here; the surge conductance 1/Zc
+         * is a parallel resistor stamped by the compiler). With u = vs, i = u/Zc + h
+         * at both ends, the travelling-wave relation gives
+         *   beta_k(p) = (2/Zc) u_k(t_p) + h_k(t_p)   (pushed into this end's ring)
+         *   h_k(t_{p+1}) = -[(1-f) beta_m(p+1-K) + f beta_m(p-K)],  tau = (K+f) dt,
+         * beta_m read from the peer end's ring (peer lane / ring slot are constants,
+         * so line ends may couple scenario lanes: BASELINE C4 line-split systems).
+         * par = [2/Zc, 1-f, f, K, peer_lane, peer_ring_slot]; state = ring[L]. */
+        double* g = A + (size_t)p->out * W; double* h = A + (size_t)p->out2 * W;
+        const int L = p->state_len;
+        for (int l = 0; l < w; ++l) {
+            const double vs = rd(e, in[1], l) - rd(e, in[0], l);
+            const double beta = par[l] * vs + h[l];
+            st[(size_t)(step % L) * W + (size_t)l] = beta;
+        }
+        for (int l = 0; l < w; ++l) {
+            const int K = (int)par[3 * W + l];
+            const size_t pl = (size_t)par[4 * W + l];
+            const size_t pr = (size_t)par[5 * W + l];
+            int q1 = (step + 1 - K) % L;
+            if (q1 < 0) q1 += L;
+            const int q0 = q1 == 0 ? L - 1 : q1 - 1;
+            const double b1 = A[(pr + (size_t)q1) * W + pl];
+            const double b0 = A[(pr + (size_t)q0) * W + pl];
+            g[l] = 0.0;
+            h[l] = -(par[W + l] * b1 + par[2 * W + l] * b0);
         }
         break;
     }

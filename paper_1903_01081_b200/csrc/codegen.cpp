@@ -51,11 +51,11 @@ std::string lit(double v) {
 // Task kinds of the compact kernel; record strides in ints.
 enum Kind {
     K_IND, K_CAP, K_SRL, K_VSRC, K_ISRC, K_CSRC, K_SW, K_GATHER, K_FWD, K_BWD, K_FINC, K_FINS,
-    K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_NKINDS
+    K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_BERG, K_NKINDS
 };
 const char* const kKindName[K_NKINDS] = {"IND", "CAP", "SRL", "VSRC", "ISRC", "CSRC", "SW", "GATHER",
                                          "FWD", "BWD", "FINC", "FINS", "GAIN", "SUM", "INTEG", "LAG",
-                                         "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH"};
+                                         "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH", "BERG"};
 // kinds whose tasks never depend on another task of the same kind: eligible
 // for the unrolled (loads-first) loop when a segment has no internal edges
 bool unrollable(int k) { return k != K_SW; }
@@ -161,6 +161,10 @@ struct Gen {
                 derived_const[static_cast<size_t>(p.out)] =
                     (p.code == kNortonCurrentSource || p.code == kNortonControlledSource) ? -1 : p.par;
             }
+            if (p.code == kNortonBergeron && p.out >= 0) {  // g = 0 (the 1/Zc resistor is stamped separately)
+                cls[static_cast<size_t>(p.out)] = kDerived;
+                derived_const[static_cast<size_t>(p.out)] = -1;
+            }
             if ((p.code == kNortonResistor || p.code == kNortonSwitch) && p.out2 >= 0) {
                 cls[static_cast<size_t>(p.out2)] = kDerived;
                 derived_const[static_cast<size_t>(p.out2)] = -1;
@@ -229,6 +233,14 @@ struct Gen {
                 t.f = {off(p.out2), p.in_count > 3 ? off(IN(3)) : 0};
                 t.ck = {p.par};
                 t.cost = 6;
+                break;
+            case kNortonBergeron:  // line end (extension): oracle/emt_oracle.c case K_BERG
+                t.kind = K_BERG;
+                reads(t, {IN(0), IN(1), p.out2});
+                t.writes = {p.out2};  // + its ring in HBM (not a shared-memory slot: peers read it)
+                t.f = {off(IN(0)), off(IN(1)), off(p.out2), p.state, p.state_len};
+                for (int j = 0; j < 6; ++j) t.ck.push_back(p.par + j);
+                t.cost = 40;
                 break;
             case kNortonSwitch:  // exec.cpp:151-165
                 t.kind = K_SW;
@@ -779,6 +791,15 @@ const KindCode kCode[K_NKINDS] = {
     /*REC*/ {"const double y@ = LD({I1});", "",
              "if (live) a.waves[((size_t)(a.row0 + it) * NCH + {I0}) * W_ + gl] = y@;"},
     /*LATCH*/ {"const double y@ = LD({I0});", "", "ST({I1}, y@);"},
+    /*BERG*/ {"const double vs@ = LD({I1}) - LD({I0}); const double hp@ = LD({I2}); const double y2@ = {C0}; "
+             "const double c1@ = {C1}; const double c0@ = {C2}; const int K@ = (int)({C3}); "
+             "const long long pl@ = (long long)({C4}) - LB_; const long long pr@ = (long long)({C5});",
+             "const double be@ = y2@ * vs@ + hp@; int q1@ = (step + 1 - K@) % {I4}; if (q1@ < 0) q1@ += {I4}; "
+             "const int q0@ = q1@ == 0 ? {I4} - 1 : q1@ - 1; "
+             "const double b1@ = __ldcg(a.arena + (pr@ + q1@) * W_ + pl@); "
+             "const double b0@ = __ldcg(a.arena + (pr@ + q0@) * W_ + pl@); "
+             "const double h@ = -(c1@ * b1@ + c0@ * b0@);",
+             "ST({I2}, h@); if (live) A[(size_t)({I3} + step % {I4}) * W_] = be@;"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1112,7 +1133,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const long long Wl = lanes;
     o << "// generated by emtb200 codegen: " << s.nodes << " nodes, " << s.comps << " components, " << s.layers
       << " layers, " << lanes << " lanes, " << G << " warps, " << nt << " tasks, " << segs_total << " segments\n";
-    o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n";
+    o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {

@@ -21,6 +21,7 @@ struct CodegenOptions {
     size_t smem_budget = 227 * 1024;  // bytes of dynamic shared memory per CTA
     bool lu_in_smem = true;         // keep L/U factors on chip when they fit
     int mode = 0;                   // 0 auto, 1 straight-line tasks, 2 compact per-type loops
+    long long lane_begin = 0;       // first batch lane of the engine (line-end peer lanes are batch indices)
 };
 
 struct GeneratedKernel {

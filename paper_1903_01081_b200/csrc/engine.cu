@@ -56,6 +56,7 @@ struct CgArgs {
 
 struct DevPlan {
     int W;          // lanes owned by this engine
+    int lane_begin; // first owned lane of the batch (line-end peers are batch lane indices)
     int lpb;        // lanes (warps) per block
     int use_smem;   // arena + consts in shared memory (else lane-major global scratch)
     int lane_stride;  // doubles per lane in the working area
@@ -177,6 +178,26 @@ __device__ __forceinline__ void run_regular(const DevPlan& P, double* __restrict
                     P.events[3 * slot + 2] = __ldg(&P.proc_id[k]);
                 }
             }
+            break;
+        }
+        case kNortonBergeron: {  // line end (extension): oracle/emt_oracle.c case K_BERG
+            const double vs = rd(A, __ldg(in + 1)) - rd(A, __ldg(in + 0));
+            const double beta = par[0] * vs + A[a.z];
+            const int L = static_cast<int>(par[6]);
+            const int w = step % L;
+            st[w] = beta;  // resident copy (written back at launch end) ...
+            P.arena[static_cast<size_t>(a.w + w) * P.W + lane] = beta;  // ... and the copy peers read
+            const int K = static_cast<int>(par[3]);
+            const size_t pl = static_cast<size_t>(par[4]) - static_cast<size_t>(P.lane_begin);
+            const size_t pr = static_cast<size_t>(par[5]);
+            int q1 = (step + 1 - K) % L;
+            if (q1 < 0) q1 += L;
+            const int q0 = q1 == 0 ? L - 1 : q1 - 1;
+            // entries of earlier launches (launches span < K passes): L2, not a stale L1 line
+            const double b1 = __ldcg(P.arena + (pr + static_cast<size_t>(q1)) * P.W + pl);
+            const double b0 = __ldcg(P.arena + (pr + static_cast<size_t>(q0)) * P.W + pl);
+            A[a.y] = 0.0;
+            A[a.z] = -(par[1] * b1 + par[2] * b0);
             break;
         }
         case kInjectionPair: {
@@ -443,6 +464,7 @@ struct emt_engine {
     double* d_waves = nullptr;
     unsigned char* d_refactored = nullptr;
     int launches = 0;
+    int max_chunk = INT_MAX;  // passes per launch; < K when line ends couple lanes across CTAs
     int failed = 0;
     int max_events = 1 << 16;
     double divergence_limit = kDefaultDivergence;
@@ -506,6 +528,7 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
     DevPlan& P = e->plan;
     const int W = e->W;
     P.W = W;
+    P.lane_begin = e->lane_begin;
     P.extent = s.extent;
     P.consts = s.consts;
     P.nch = static_cast<int>(s.channel_slot.size());
@@ -587,6 +610,25 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
             arena[static_cast<size_t>(k) * W + l] =
                 initial[static_cast<size_t>(k) * width + static_cast<size_t>(e->lane_begin + l)];
     e->host_ctab = ctab;
+    // Bergeron line ends read peer rings written >= K-1 passes earlier: a launch
+    // may span at most K-1 passes so that every entry it reads was written by an
+    // earlier launch (the kernel boundary orders the cross-CTA stores), and the
+    // ring must hold the 2K-1 entries live across one launch.
+    for (const Proc& p : s.procs) {
+        if (p.code != kNortonBergeron) continue;
+        if (p.par_len < 7 || p.state < 0 || p.state_len < 1)
+            return set_error(EMT_MALFORMED_DOCUMENT, "line end " + std::to_string(p.id) + ": bad record");
+        for (int l = 0; l < W; ++l) {
+            auto c = [&](int j) { return ctab[static_cast<size_t>(p.par + j) * W + l]; };
+            const int K = static_cast<int>(c(3)), L = static_cast<int>(c(6));
+            const long long pl = static_cast<long long>(c(4)) - e->lane_begin;
+            if (K < 2 || L != p.state_len || L < 2 * K - 1 || pl < 0 || pl >= W)
+                return set_error(EMT_MALFORMED_DOCUMENT, "line end " + std::to_string(p.id) + " lane " +
+                                                             std::to_string(e->lane_begin + l) +
+                                                             ": needs K >= 2, ring L >= 2K-1 and a peer lane this engine owns");
+            e->max_chunk = std::min(e->max_chunk, K - 1);
+        }
+    }
     e->initial_fcount.resize(static_cast<size_t>(W));
     for (int l = 0; l < W; ++l) e->initial_fcount[static_cast<size_t>(l)] = arena[static_cast<size_t>(s.fcount) * W + l];
     e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
@@ -745,6 +787,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         Failure gf;
         std::string log;
         const auto t0 = std::chrono::steady_clock::now();
+        opt.lane_begin = e->lane_begin;
         bool ok = generate_kernel(e->sched, e->host_ctab, e->W, opt, e->gen, gf);
         const double gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         if (ok) ok = jit_load(e->gen.source, e->gen.name, e->device, e->jit, log);
@@ -818,6 +861,15 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
     if (e->rows + steps > e->capacity)
         return set_error(EMT_CAPACITY_EXCEEDED, "waveform store holds " + std::to_string(e->capacity) + " rows");
     CUDA_TRY(cudaSetDevice(e->device));
+    if (steps > e->max_chunk) {
+        for (int done = 0; done < steps;) {
+            const int n = std::min(e->max_chunk, steps - done);
+            EMT_TRY(emt_engine_advance(e, n, 0));
+            done += n;
+        }
+        if (sync) return emt_engine_sync(e);
+        return EMT_OK;
+    }
     if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit};

@@ -30,6 +30,10 @@ enum Kernel : int {
     kCtlComparator,
     kCtlConstant,
     kCtlDelay,
+    // Extension (no reference counterpart): lossless Bergeron
+    // transmission-line end. par = [2/Zc, 1-f, f, K, peer_lane, peer_ring, L],
+    // state = ring[L]; see oracle/emt_oracle.c case K_BERG for the semantics.
+    kNortonBergeron,
     kKernelCount
 };
 

@@ -156,3 +156,30 @@ def n1_batch(base_schedule: str, base_initial: np.ndarray, component_ids: Sequen
 
 def rows_json(rows) -> str:
     return json.dumps(rows)
+
+
+def pv_grid(n_irr: int = 64, n_temp: int = 64, irr=(400.0, 1100.0), temp=(5.0, 45.0)) -> List[Tuple[float, float]]:
+    """gen_scenarios row order (proj/src/bench.cpp:137-146): irradiance-major, temperature inner."""
+    return [(float(i), float(t)) for i in np.linspace(irr[0], irr[1], n_irr) for t in np.linspace(temp[0], temp[1], n_temp)]
+
+
+def pv_sweep_batch(base_schedule: str, base_initial: np.ndarray, pv_map: dict,
+                   scenarios: Sequence[Tuple[float, float]]) -> Batch:
+    """Shared-G batch (BASELINE C5): lane s sets every PV's (irradiance, temperature).
+
+    The override only changes the photocurrent J = 10 (irr/1000)(1 + 0.0004 (temp-25))
+    (proj/src/model.cpp:306-309) — each PV current source's magnitude constant and
+    +-J initial branch currents — so G is identical across lanes. `pv_map` (the case
+    data's "pv_sweep" record) names those slots; tools/make_fixtures.py derives it
+    from the reference's own vectorize and tests/test_schedule_host.py pins this
+    widening against it bit for bit."""
+    info = parse_info(base_schedule)
+    W = len(scenarios)
+    j = np.array([10.0 * (irr / 1000.0) * (1.0 + 0.0004 * (tmp - 25.0)) for irr, tmp in scenarios])
+    ct = np.repeat(info.const_table[:, :1], W, axis=1)
+    for k in pv_map["const_slots"]:
+        ct[k, :] = j
+    init = replicate_lanes(base_initial, info.extent, info.width, 0, W).reshape(info.extent, W)
+    for k, sign in pv_map["init_slots"]:
+        init[k, :] = j if sign > 0 else -j
+    return Batch(base_schedule, ct, init.reshape(-1), W)
