@@ -54,11 +54,12 @@ WORKLOADS = {
     "c3": ("ieee39-n1-sweep (BASELINE C3)", "ieee39", 1000),
     "c5": ("feeder33-pv-sweep shared G (BASELINE C5)", "feeder33_pv3", 4096),
     "c2": ("ieee39 single scenario (BASELINE C2)", "ieee39", 1),
+    "c4": ("ieee39 x120 line-coupled single system, split at Bergeron lines (BASELINE C4)", "ieee39_c4", 120),
 }
 
 
 METRIC = {"c3": "scenario-steps/sec for N-1 EMT batch", "c5": "scenario-steps/sec for shared-G EMT batch",
-          "c2": "us per time step on single case"}
+          "c2": "us per time step on single case", "c4": "us per time step on large single case"}
 
 
 def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3"):
@@ -76,6 +77,10 @@ def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3")
         while len(grid) < scenarios:  # weak scaling beyond a square grid: shifted repeats
             grid += [(i + 1e-3 * len(grid), t) for i, t in grid[: scenarios - len(grid)]]
         return sch.pv_sweep_batch(s, st, pvm, grid[lo:hi]), sch.parse_info(s)
+    if workload == "c4":  # one system of `scenarios` IEEE-39 copies (one lane each) coupled by lines
+        from paper_1903_01081_b200 import lines
+        s, st, ids = load_case("ieee39_c4")
+        return lines.c4_batch(s, st, ids, scenarios), sch.parse_info(s)
     s, st, ids = load_case("ieee39")
     if workload == "c2":
         return sch.n1_batch(s, st, ids, [("sw00", 1e9)] * (hi - lo)), sch.parse_info(s)
@@ -181,7 +186,9 @@ def run_ours(args):
 
     from paper_1903_01081_b200 import sharding
     wl_name, _, _ = WORKLOADS[args.workload]
-    W = args.scenarios * world  # weak scaling: `--scenarios` per GPU, contiguous shards
+    # weak scaling: `--scenarios` per GPU, contiguous shards; C4 is ONE system of
+    # `--scenarios` line-coupled copies split over the GPUs (strong scaling)
+    W = args.scenarios if args.workload == "c4" else args.scenarios * world
     lo, hi = sharding.shard_bounds(W, world, rank)
     batch, info = build_batch(W, lo, hi, args.workload)
     S = args.emt_steps
@@ -189,14 +196,20 @@ def run_ours(args):
 
     kern = {"auto": engine.KERNEL_AUTO, "specialised": engine.KERNEL_SPECIALISED,
             "generic": engine.KERNEL_GENERIC}[args.kernel]
-    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, device=dev,
-                        kernel=kern, warps=args.warps)
+    if args.workload == "c4":  # lane shard + line-end ring exchange every K-1 passes
+        runner = sharding.LineSplitShard(dist if world > 1 else None, batch, lo, hi, device=dev, kernel=kern,
+                                         warps=args.warps)
+        eng, adv = runner.eng, runner.advance
+    else:
+        eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width,
+                            device=dev, kernel=kern, warps=args.warps)
+        adv = eng.advance
     eng.reserve(total_steps)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
     flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     for _ in range(args.warmup):
-        eng.advance(S)
+        adv(S)
     eng.sync()
     if world > 1:
         dist.barrier()
@@ -209,7 +222,7 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 flush_l2(torch, flush)
                 starts[k].record(stream)
-            eng.advance(S)
+            adv(S)
             ends[k].record(stream)
         eng.sync()
         torch.cuda.synchronize()
@@ -227,7 +240,27 @@ def run_ours(args):
     # whole arena + constant table), runs S passes and streams the waveform rows back
     # into pinned host memory chunk by chunk (D2H overlapped with the next chunk).
     e2e_local, e2e_digest_ok = float('nan'), None
-    if not args.skip_e2e:
+    if not args.skip_e2e and args.workload == "c4" and world > 1:
+        # line-split across ranks: reload the shard from pinned host, step with the
+        # exchange, read the shard's waveform rows back
+        e2e_steps = max(3, min(5, args.steps))
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        ct_host, init_host = pin(batch.const_table), pin(batch.initial)
+        e2e_s = []
+        for k in range(e2e_steps + 1):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            eng.load(init_host, ct_host)
+            eng.reserve(S)
+            adv(S)
+            host_w = eng.waves(0, S).values
+            t1 = time.perf_counter()
+            if k > 0:
+                e2e_s.append(t1 - t0)
+        e2e_local = statistics.median(e2e_s)
+        e2e_digest_ok = None
+    elif not args.skip_e2e:
         e2e_steps = max(3, min(5, args.steps))
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         ct_host = pin(batch.const_table)
@@ -286,7 +319,7 @@ def run_ours(args):
         h2d = batch.const_table.nbytes + batch.initial.nbytes  # per bench step (S passes)
         d2h = S * len(info.channels) * (hi - lo) * 8
         metric, unit, hib, val, e2e_val = (METRIC[args.workload], "scenario-steps/s", True, value, W * S / e2e_max)
-        if args.workload == "c2":  # latency of one scenario: µs per EMT time step
+        if args.workload in ("c2", "c4"):  # latency of one system: µs per EMT time step
             metric, unit, hib = "us per time step on single case", "us/step", False
             val, e2e_val = 1e3 * max_ms / (args.steps * S), 1e6 * e2e_max / S
         out = {
@@ -298,7 +331,7 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": max_ms / args.steps,
             "higher_is_better": hib,
-            "scaling": "weak",
+            "scaling": "strong" if args.workload == "c4" else "weak",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
@@ -364,7 +397,26 @@ def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: in
     return W, max(res), procs
 
 
+def oracle_measure(scenarios: int, emt_steps: int, workload: str):
+    """C4 has no reference path (the reference has no line model): time the C
+    restatement (oracle/emt_oracle.c, the parity checker) on the whole coupled
+    system, one thread — the lanes are one system, so they cannot be sharded."""
+    from oracle import oracle
+    batch, info = build_batch(scenarios, workload=workload)
+    sched = oracle.Schedule(batch.text())
+    sched.interpret(batch.initial, 20)  # warm-up
+    t0 = time.perf_counter()
+    sched.interpret(batch.initial, emt_steps)
+    return batch.width, time.perf_counter() - t0
+
+
 def cpu_baseline(args):
+    if args.workload == "c4":
+        steps = 2000
+        W, secs = oracle_measure(args.scenarios, steps, "c4")
+        return {"value": 1e6 * secs / steps, "unit": "us/step", "cores": 1, "kind": "port",
+                "sample": f"{W}-copy line-coupled system x {steps} EMT steps, oracle/emt_oracle.c interpret "
+                          "(the reference has no line model), single thread"}
     steps = args.cpu_emt_steps if args.workload != "c2" else 20000
     W, secs, procs = reference_measure(args.scenarios, steps, 20, os.cpu_count() or 1, args.workload)
     if args.workload == "c2":
@@ -381,23 +433,31 @@ def run_reference(args):
     if rank != 0:
         return
     S = args.cpu_emt_steps_per_step
-    W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup, os.cpu_count() or 1,
-                                       args.workload)
+    kind = "reference"
+    if args.workload == "c4":
+        kind, procs = "port", 1
+        W, secs = oracle_measure(args.scenarios, S * args.steps, "c4")
+    else:
+        W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup,
+                                           os.cpu_count() or 1, args.workload)
     metric, unit, hib, value = METRIC[args.workload], "scenario-steps/s", True, W * S * args.steps / secs
-    if args.workload == "c2":
-        metric, unit, hib, value = "us per time step on single case", "us/step", False, 1e6 * secs / (S * args.steps)
+    if args.workload in ("c2", "c4"):
+        metric, unit, hib, value = METRIC[args.workload], "us/step", False, 1e6 * secs / (S * args.steps)
     out = {
         "impl": "reference",
         "metric": metric,
         "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": hib,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if args.workload == "c4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": args.scenarios,
                    "emt_steps_per_bench_step": S,
                    "parallelism": f"{procs} host processes over contiguous lane shards"},
-        "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": "reference",
-                         "sample": f"{W} scenarios x {S} EMT steps per bench step "
-                                   f"({args.warmup} warm-up + {args.steps} timed), emtgrid::interpret"},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": kind,
+                         "sample": f"{W} {'copies' if kind == 'port' else 'scenarios'} x {S} EMT steps per bench "
+                                   f"step ({args.warmup} warm-up + {args.steps} timed), "
+                                   + ("oracle/emt_oracle.c (no reference line model), one thread" if kind == "port"
+                                      else "emtgrid::interpret")},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)

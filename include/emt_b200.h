@@ -154,6 +154,20 @@ emt_status emt_engine_load(emt_engine* engine, const double* initial, int64_t in
  * (SURVEY.md §8(b) emt_run). */
 emt_status emt_engine_run(emt_engine* engine, int32_t steps, int32_t chunk, double* waves);
 
+/* Line-end history mirror (Bergeron extension, kernel code 20): a device array
+ * of `lanes` (= the whole batch width) x `cols` doubles, lane-major, holding
+ * every lane's ring slots [ring_lo, ring_lo+cols). Each launch writes this
+ * engine's lanes' rows and reads peer rows; an engine that owns a lane shard
+ * gets the other shards' rows from its peers between launches (the exchange
+ * of a line-split system over several GPUs). `max_chunk` = passes per launch
+ * (K-1 of the shortest line), 0 when unbounded. */
+emt_status emt_engine_ring(emt_engine* engine, void** device_ptr, int32_t* lanes, int32_t* cols,
+                           int32_t* max_chunk);
+/* Moves the mirror into caller-owned device memory (lanes*cols doubles, e.g. a
+ * buffer a collective library writes into); the engine copies its current
+ * contents there and uses it from then on. The buffer must outlive the engine. */
+emt_status emt_engine_attach_ring(emt_engine* engine, void* device_ptr);
+
 /* Host copies of recorded rows [row0, row0+rows) (WaveformSet layout, this
  * engine's lanes only) and their times. */
 emt_status emt_engine_read_waves(emt_engine* engine, int32_t row0, int32_t rows, double* waves,

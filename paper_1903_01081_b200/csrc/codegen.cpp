@@ -91,8 +91,28 @@ struct Gen {
     std::vector<int> chg_slots;
     std::vector<Task> tasks;
     int fact_layer = 0, solve_layer = 0;
+    std::set<int> iread;        // arena slots some process / channel / latch reads
+    std::vector<int> lazy_fin;  // components whose current no task reads: finalized once per launch
 
-    Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {}
+    bool lazy_i = true;
+    Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
+        lazy_i = knob("EMTB200_CG_LAZYI", 1) != 0;
+    }
+
+    /// Deferred finalize (exec.cpp:220-228) of the currents no task reads.
+    std::string emit_lazy_finalize() const {
+        std::ostringstream o;
+        for (int c : lazy_fin) {
+            const int* f = s.finalize.data() + 5 * c;
+            std::string gx;
+            if (f[1] < 0) gx = "(0.0)";
+            else if (cls[static_cast<size_t>(f[1])] == kDerived) gx = R(f[1]);
+            else gx = "S[" + std::to_string(hot_index[static_cast<size_t>(f[1])] * 32) + "]";
+            o << "      { const double vs = " << R(f[4]) << " - " << R(f[3]) << "; A[(size_t)" << f[0]
+              << " * W_] = " << gx << " * vs + " << R(f[2]) << "; }\n";
+        }
+        return o.str();
+    }
 
     bool invariant(int k) const {
         const double* row = ct.data() + static_cast<size_t>(k) * W;
@@ -140,6 +160,22 @@ struct Gen {
 
     void classify() {
         const size_t n = static_cast<size_t>(s.extent);
+        iread.clear();
+        for (const Proc& p : s.procs) {
+            // ports a kernel actually reads (exec.cpp:85-309): Norton records carry
+            // [v_a, v_b, i_prev(, actuator)] whatever the kind uses
+            int lo = 0, hi = p.in_count;
+            if (p.code == kNortonResistor || p.code == kNortonVoltageSource || p.code == kNortonCurrentSource ||
+                p.code == kNortonSwitch)
+                hi = 0;
+            else if (p.code == kNortonControlledSource)
+                lo = 3;
+            else if (p.code == kNortonBergeron)
+                hi = std::min(hi, 2);
+            for (int j = lo; j < hi; ++j) iread.insert(s.port_slot[static_cast<size_t>(p.in_base + j)]);
+        }
+        for (int x : s.channel_slot) iread.insert(x);
+        for (int x : s.latch_live) iread.insert(x);
         cls.assign(n, kNone);
         derived_const.assign(n, -2);
         contrib_h.assign(n, -1);
@@ -369,6 +405,12 @@ struct Gen {
         }
         for (int c = 0; c < s.comps; ++c) {  // i = g (v_b - v_a) + h
             const int* f = s.finalize.data() + 5 * c;
+            if (lazy_i && f[0] >= 0 && !iread.count(f[0])) {
+                // nothing reads this current inside a pass: computing it from the
+                // launch's final v, g, h gives the bits the last pass would have
+                lazy_fin.push_back(c);
+                continue;
+            }
             Task t;
             t.reads = {dep_slot(f[1]), dep_slot(f[2])};
             if (f[3] >= 0) t.reads.push_back(f[3]);
@@ -386,6 +428,7 @@ struct Gen {
 
     void emit_all(int& fact_count) {
         tasks.clear();
+        lazy_fin.clear();
         int region = 0;
         fact_count = 0;
         for (int L = 0; L < s.layers; ++L) {
@@ -793,13 +836,14 @@ const KindCode kCode[K_NKINDS] = {
     /*LATCH*/ {"const double y@ = LD({I0});", "", "ST({I1}, y@);"},
     /*BERG*/ {"const double vs@ = LD({I1}) - LD({I0}); const double hp@ = LD({I2}); const double y2@ = {C0}; "
              "const double c1@ = {C1}; const double c0@ = {C2}; const int K@ = (int)({C3}); "
-             "const long long pl@ = (long long)({C4}) - LB_; const long long pr@ = (long long)({C5});",
+             "const long long pl@ = (long long)({C4}); const long long pr@ = (long long)({C5}) - a.ring_lo;",
              "const double be@ = y2@ * vs@ + hp@; int q1@ = (step + 1 - K@) % {I4}; if (q1@ < 0) q1@ += {I4}; "
              "const int q0@ = q1@ == 0 ? {I4} - 1 : q1@ - 1; "
-             "const double b1@ = __ldcg(a.arena + (pr@ + q1@) * W_ + pl@); "
-             "const double b0@ = __ldcg(a.arena + (pr@ + q0@) * W_ + pl@); "
+             "const double b1@ = __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q1@); "
+             "const double b0@ = __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q0@); "
              "const double h@ = -(c1@ * b1@ + c0@ * b0@);",
-             "ST({I2}, h@); if (live) A[(size_t)({I3} + step % {I4}) * W_] = be@;"},
+             "ST({I2}, h@); if (live) { const int w@ = step % {I4}; A[(size_t)({I3} + w@) * W_] = be@; "
+             "a.ring[(LB_ + gl) * a.ring_cols + ({I3} - a.ring_lo) + w@] = be@; }"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1058,8 +1102,28 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * 256) + ")";
         return "__ldg(C + " + std::to_string(static_cast<long long>(k) * lanes) + ")";
     };
+    const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     auto region_code = [&](const Sched& sc) {
         std::ostringstream rc;
+        if (straight && warp_major) {
+            // One contiguous block per warp holding all of its phases, phases
+            // separated by bar.sync: a single warp-uniform dispatch per region
+            // (instead of an if/else chain per phase) and sequential code per
+            // warp for the instruction prefetcher.
+            rc << "    switch (warp) {\n";
+            for (int w = 0; w < G; ++w) {
+                rc << "    case " << w << ": {\n";
+                for (size_t p = 0; p < sc.phases.size(); ++p) {
+                    if (p > 0) rc << "      BAR();\n";
+                    std::vector<int> ordered;
+                    segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
+                    for (int id : ordered) rc << "      " << task_literal(g.tasks[static_cast<size_t>(id)], lctx) << "\n";
+                }
+                rc << "    } break;\n";
+            }
+            rc << "    }\n";
+            return rc.str();
+        }
         for (size_t p = 0; p < sc.phases.size(); ++p) {
             if (p > 0) rc << "    __syncthreads();\n";
             bool first = true;
@@ -1135,7 +1199,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << " layers, " << lanes << " lanes, " << G << " warps, " << nt << " tasks, " << segs_total << " segments\n";
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
-      << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit; };\n";
+      << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
+      << "  double* ring; long long ring_lo; long long ring_cols; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -1172,6 +1237,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     carr_i("__device__ const", "kConSlot", cslot);
     carr_i("__device__ const", "kConHot", chot);
     carr_i("__device__ const", "kConSign", csign);
+    o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
     o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
       << "#define ST(o, v) (*(double*)(Sb + (o)) = (v))\n"
       << "#define SGN(x, n) ((n) ? -(x) : (x))\n";
@@ -1265,6 +1331,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * 32]; "
       << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
       << "      for (int q = warp; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << G << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n"
+      << "      if (warp == " << (G - 1) << ") {\n" << g.emit_lazy_finalize() << "      }\n"
       << "    }\n"
       << "  }\n"
       << "}\n";

@@ -52,11 +52,15 @@ struct CgArgs {
     int max_events;
     int step0, nsteps, row0;
     double div_limit;
+    double* ring;  // line-end history mirror, lane-major [batch lane][ring slot - ring_lo]
+    long long ring_lo, ring_cols;
 };
 
 struct DevPlan {
     int W;          // lanes owned by this engine
     int lane_begin; // first owned lane of the batch (line-end peers are batch lane indices)
+    double* ring;   // line-end history mirror [batch lane][ring_cols], see emt_engine_ring
+    int ring_lo, ring_cols;
     int lpb;        // lanes (warps) per block
     int use_smem;   // arena + consts in shared memory (else lane-major global scratch)
     int lane_stride;  // doubles per lane in the working area
@@ -185,17 +189,18 @@ __device__ __forceinline__ void run_regular(const DevPlan& P, double* __restrict
             const double beta = par[0] * vs + A[a.z];
             const int L = static_cast<int>(par[6]);
             const int w = step % L;
-            st[w] = beta;  // resident copy (written back at launch end) ...
-            P.arena[static_cast<size_t>(a.w + w) * P.W + lane] = beta;  // ... and the copy peers read
+            st[w] = beta;  // the lane's arena copy (written back at launch end)
+            const size_t cols = static_cast<size_t>(P.ring_cols);
+            P.ring[static_cast<size_t>(P.lane_begin + lane) * cols + static_cast<size_t>(a.w - P.ring_lo + w)] = beta;
             const int K = static_cast<int>(par[3]);
-            const size_t pl = static_cast<size_t>(par[4]) - static_cast<size_t>(P.lane_begin);
-            const size_t pr = static_cast<size_t>(par[5]);
+            const size_t pl = static_cast<size_t>(par[4]);
+            const size_t pr = static_cast<size_t>(par[5]) - static_cast<size_t>(P.ring_lo);
             int q1 = (step + 1 - K) % L;
             if (q1 < 0) q1 += L;
             const int q0 = q1 == 0 ? L - 1 : q1 - 1;
-            // entries of earlier launches (launches span < K passes): L2, not a stale L1 line
-            const double b1 = __ldcg(P.arena + (pr + static_cast<size_t>(q1)) * P.W + pl);
-            const double b0 = __ldcg(P.arena + (pr + static_cast<size_t>(q0)) * P.W + pl);
+            // entries of earlier launches (a launch spans < K passes): read through L2
+            const double b1 = __ldcg(P.ring + pl * cols + pr + static_cast<size_t>(q1));
+            const double b0 = __ldcg(P.ring + pl * cols + pr + static_cast<size_t>(q0));
             A[a.y] = 0.0;
             A[a.z] = -(par[1] * b1 + par[2] * b0);
             break;
@@ -465,6 +470,8 @@ struct emt_engine {
     unsigned char* d_refactored = nullptr;
     int launches = 0;
     int max_chunk = INT_MAX;  // passes per launch; < K when line ends couple lanes across CTAs
+    double* d_ring = nullptr;   // line-end history mirror (owned unless attached)
+    bool ring_owned = true;
     int failed = 0;
     int max_events = 1 << 16;
     double divergence_limit = kDefaultDivergence;
@@ -480,6 +487,7 @@ struct emt_engine {
         if (device >= 0) cudaSetDevice(device);
         if (jit.module && driver()) driver()->ModuleUnload(jit.module);
         for (void* p : allocations) cudaFree(p);
+        if (d_ring && ring_owned) cudaFree(d_ring);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
@@ -612,22 +620,50 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
     e->host_ctab = ctab;
     // Bergeron line ends read peer rings written >= K-1 passes earlier: a launch
     // may span at most K-1 passes so that every entry it reads was written by an
-    // earlier launch (the kernel boundary orders the cross-CTA stores), and the
-    // ring must hold the 2K-1 entries live across one launch.
+    // earlier launch (the kernel boundary orders the cross-CTA stores; across
+    // GPUs the ring exchange between launches does), and the ring must hold the
+    // 2K-1 entries live across one launch. Peers may be any lane of the batch:
+    // their rings are read from the mirror, which emt_engine_ring exposes.
+    int ring_lo = INT_MAX, ring_hi = -1;
     for (const Proc& p : s.procs) {
         if (p.code != kNortonBergeron) continue;
         if (p.par_len < 7 || p.state < 0 || p.state_len < 1)
             return set_error(EMT_MALFORMED_DOCUMENT, "line end " + std::to_string(p.id) + ": bad record");
+        ring_lo = std::min(ring_lo, p.state);
+        ring_hi = std::max(ring_hi, p.state + p.state_len);
         for (int l = 0; l < W; ++l) {
             auto c = [&](int j) { return ctab[static_cast<size_t>(p.par + j) * W + l]; };
             const int K = static_cast<int>(c(3)), L = static_cast<int>(c(6));
-            const long long pl = static_cast<long long>(c(4)) - e->lane_begin;
-            if (K < 2 || L != p.state_len || L < 2 * K - 1 || pl < 0 || pl >= W)
+            const long long pl = static_cast<long long>(c(4));
+            if (K < 2 || L != p.state_len || L < 2 * K - 1 || pl < 0 || pl >= width)
                 return set_error(EMT_MALFORMED_DOCUMENT, "line end " + std::to_string(p.id) + " lane " +
                                                              std::to_string(e->lane_begin + l) +
-                                                             ": needs K >= 2, ring L >= 2K-1 and a peer lane this engine owns");
+                                                             ": needs K >= 2, ring L >= 2K-1 and a peer lane in the batch");
             e->max_chunk = std::min(e->max_chunk, K - 1);
         }
+    }
+    P.ring = nullptr;
+    P.ring_lo = 0;
+    P.ring_cols = 0;
+    if (ring_hi > ring_lo) {
+        for (const Proc& p : s.procs) {  // peer ring slots must lie in the mirrored range
+            if (p.code != kNortonBergeron) continue;
+            for (int l = 0; l < W; ++l) {
+                const int pr = static_cast<int>(ctab[static_cast<size_t>(p.par + 5) * W + l]);
+                if (pr < ring_lo || pr + p.state_len > ring_hi)
+                    return set_error(EMT_MALFORMED_DOCUMENT, "line end " + std::to_string(p.id) + ": peer ring slot");
+            }
+        }
+        P.ring_lo = ring_lo;
+        P.ring_cols = ring_hi - ring_lo;
+        std::vector<double> mirror(static_cast<size_t>(width) * P.ring_cols);
+        for (int l = 0; l < width; ++l)
+            for (int c = 0; c < P.ring_cols; ++c)
+                mirror[static_cast<size_t>(l) * P.ring_cols + c] =
+                    initial[static_cast<size_t>(ring_lo + c) * width + static_cast<size_t>(l)];
+        CUDA_TRY(cudaMalloc(&e->d_ring, mirror.size() * sizeof(double)));
+        CUDA_TRY(cudaMemcpy(e->d_ring, mirror.data(), mirror.size() * sizeof(double), cudaMemcpyHostToDevice));
+        P.ring = e->d_ring;
     }
     e->initial_fcount.resize(static_cast<size_t>(W));
     for (int l = 0; l < W; ++l) e->initial_fcount[static_cast<size_t>(l)] = arena[static_cast<size_t>(s.fcount) * W + l];
@@ -872,7 +908,8 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
     }
     if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
-                 e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit};
+                 e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
+                 e->plan.ring, e->plan.ring_lo, e->plan.ring_cols};
         void* params[] = {&a};
         const unsigned grid = static_cast<unsigned>((e->W + 31) / 32);
         const CUresult r = driver()->LaunchKernel(e->jit.function, grid, 1, 1, static_cast<unsigned>(32 * e->gen.warps), 1, 1,
@@ -1014,6 +1051,15 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     // arena lane slice: one strided (2D) copy, contiguous when the engine owns every lane
     CUDA_TRY(cudaMemcpy2DAsync(e->plan.arena, W * sizeof(double), initial + lb, width * sizeof(double),
                                W * sizeof(double), static_cast<size_t>(s.extent), cudaMemcpyHostToDevice, e->stream));
+    if (e->plan.ring != nullptr) {  // mirror = the new batch's ring slots, every lane, lane-major
+        std::vector<double> mirror(width * static_cast<size_t>(e->plan.ring_cols));
+        for (size_t l = 0; l < width; ++l)
+            for (int c = 0; c < e->plan.ring_cols; ++c)
+                mirror[l * e->plan.ring_cols + c] = initial[static_cast<size_t>(e->plan.ring_lo + c) * width + l];
+        CUDA_TRY(cudaMemcpyAsync(e->plan.ring, mirror.data(), mirror.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                 e->stream));
+        CUDA_TRY(cudaStreamSynchronize(e->stream));  // `mirror` is a pageable temporary
+    }
     for (size_t l = 0; l < W; ++l) e->initial_fcount[l] = initial[static_cast<size_t>(s.fcount) * width + lb + l];
     e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
     CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
@@ -1022,6 +1068,29 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     e->step = 0;
     e->rows = 0;
     e->failed = 0;
+    return EMT_OK;
+}
+
+emt_status emt_engine_ring(emt_engine* e, void** device_ptr, int32_t* lanes, int32_t* cols, int32_t* max_chunk) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (device_ptr) *device_ptr = e->plan.ring;
+    if (lanes) *lanes = e->plan.ring ? e->width : 0;
+    if (cols) *cols = e->plan.ring_cols;
+    if (max_chunk) *max_chunk = e->max_chunk == INT_MAX ? 0 : e->max_chunk;
+    return EMT_OK;
+}
+
+emt_status emt_engine_attach_ring(emt_engine* e, void* device_ptr) {
+    if (e == nullptr || device_ptr == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    if (e->plan.ring == nullptr) return set_error(EMT_NON_POSITIVE_INPUT, "schedule has no line ends");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    const size_t bytes = static_cast<size_t>(e->width) * e->plan.ring_cols * sizeof(double);
+    CUDA_TRY(cudaMemcpy(device_ptr, e->plan.ring, bytes, cudaMemcpyDeviceToDevice));
+    if (e->ring_owned && e->d_ring) cudaFree(e->d_ring);
+    e->d_ring = static_cast<double*>(device_ptr);
+    e->ring_owned = false;
+    e->plan.ring = e->d_ring;
     return EMT_OK;
 }
 

@@ -111,6 +111,8 @@ def lib():
         L.emt_engine_read_refactor_steps.argtypes = [vp, ip, ctypes.c_int32, ip]
         L.emt_engine_load.argtypes = [vp, dp, ctypes.c_int64, dp]
         L.emt_engine_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
+        L.emt_engine_ring.argtypes = [vp, ctypes.POINTER(vp), ip, ip, ip]
+        L.emt_engine_attach_ring.argtypes = [vp, vp]
         L.emt_engine_kernel.argtypes = [vp]
         L.emt_engine_kernel.restype = ctypes.c_int32
         L.emt_engine_source.argtypes = [vp]
@@ -129,6 +131,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
+    "emt_engine_ring", "emt_engine_attach_ring",
 ]
 
 
@@ -301,6 +304,16 @@ class Engine:
         _check(lib().emt_engine_run(self._h, int(steps), int(chunk), _dp(out) if out is not None else None))
         self.rows += steps
         return out
+
+    def ring(self):
+        """(device pointer, lanes, cols, max passes per launch) of the line-end history mirror."""
+        p = ctypes.c_void_p()
+        lanes, cols, mc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().emt_engine_ring(self._h, ctypes.byref(p), ctypes.byref(lanes), ctypes.byref(cols), ctypes.byref(mc)))
+        return int(p.value or 0), lanes.value, cols.value, mc.value
+
+    def attach_ring(self, device_ptr: int) -> None:
+        _check(lib().emt_engine_attach_ring(self._h, ctypes.c_void_p(device_ptr)))
 
     def sync(self) -> None:
         _check(lib().emt_engine_sync(self._h))

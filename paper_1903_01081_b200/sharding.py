@@ -63,3 +63,60 @@ def combine_factor_counts(per_rank_refactor_steps: Sequence[Sequence[int]]) -> i
     for s in per_rank_refactor_steps:
         steps.update(int(x) for x in s)
     return len(steps)
+
+
+# ---------------------------------------------------------------- line-split systems (C4)
+
+def exchange_rings(dist, mirror, lo: int, hi: int) -> None:
+    """Boundary exchange of a line-split system: every rank contributes its lanes'
+    rows [lo, hi) of the lane-major line-end history mirror (engine.ring()) and
+    receives everyone else's. One collective per launch of <= K-1 passes; the
+    Bergeron travel time gives those K-1 passes of slack."""
+    import torch
+    world = dist.get_world_size()
+    W = mirror.shape[0]
+    bounds = [shard_bounds(W, world, r) for r in range(world)]
+    width = max(b - a for a, b in bounds)
+    send = torch.zeros((width,) + tuple(mirror.shape[1:]), dtype=mirror.dtype, device=mirror.device)
+    send[: hi - lo] = mirror[lo:hi]
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send)
+    for r, (a, b) in enumerate(bounds):
+        if r != dist.get_rank():
+            mirror[a:b] = parts[r][: b - a]
+
+
+class LineSplitShard:
+    """One rank's lanes of a line-coupled batch: an Engine over [lo, hi) whose
+    line-end mirror lives in a torch tensor so collectives can fill peer rows.
+
+    advance(n) runs launches of at most `max_chunk` (= K-1) passes and exchanges
+    the mirror after each one (stream-ordered: engine sync -> collective -> next
+    launch). With world == 1 it is a plain engine advance."""
+
+    def __init__(self, dist, batch, lo: int, hi: int, device: int = 0, **engine_kw):
+        import torch
+        from . import engine
+        self.dist, self.lo, self.hi = dist, lo, hi
+        self.eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width,
+                                 device=device, lane_begin=lo, lane_count=hi - lo, **engine_kw)
+        ptr, lanes, cols, self.max_chunk = self.eng.ring()
+        self.mirror = None
+        if ptr:
+            self.mirror = torch.zeros((lanes, cols), dtype=torch.float64, device=torch.device("cuda", device))
+            self.eng.attach_ring(self.mirror.data_ptr())
+        self.world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+
+    def advance(self, steps: int) -> None:
+        import torch
+        if self.world == 1 or self.mirror is None or self.max_chunk <= 0:
+            self.eng.advance(steps)
+            return
+        done = 0
+        while done < steps:
+            n = min(self.max_chunk, steps - done)
+            self.eng.advance(n)
+            self.eng.sync()
+            exchange_rings(self.dist, self.mirror, self.lo, self.hi)
+            torch.cuda.current_stream().synchronize()
+            done += n

@@ -151,3 +151,46 @@ def test_engine_c4_kernels_agree_bitwise():
         eng.advance(700)
         out.append(eng.waves().values)
     assert bitwise_equal(out[0], out[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["auto", "generic"])
+def test_line_split_shards_with_ring_exchange_equal_one_engine(kernel):
+    """Two lane-shard engines (the 2-GPU split, here on one device) that swap
+    their mirror rows after every launch of K-1 passes == one engine on all lanes."""
+    import torch
+    from paper_1903_01081_b200 import engine
+    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}[kernel]
+    b = c4_case(40)
+    whole = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k)
+    whole.reserve(600)
+    whole.advance(600)
+    want = whole.waves().values
+    shards, mirrors = [], []
+    for lo, hi in ((0, 24), (24, 40)):
+        e = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k,
+                          lane_begin=lo, lane_count=hi - lo)
+        ptr, lanes, cols, mc = e.ring()
+        assert ptr and lanes == 40 and mc == 5
+        m = torch.zeros((lanes, cols), dtype=torch.float64, device="cuda")
+        e.attach_ring(m.data_ptr())
+        e.reserve(600)
+        shards.append((e, lo, hi))
+        mirrors.append(m)
+    done = 0
+    while done < 600:
+        n = min(5, 600 - done)
+        for e, _, _ in shards:
+            e.advance(n)
+        for e, _, _ in shards:
+            e.sync()
+        torch.cuda.synchronize()
+        mirrors[1][0:24] = mirrors[0][0:24]
+        mirrors[0][24:40] = mirrors[1][24:40]
+        torch.cuda.synchronize()
+        done += n
+    for (e, lo, hi) in shards:
+        got = e.waves().values
+        nch = len(e.channel_names)
+        for c in range(nch):
+            assert bitwise_equal(got[:, c * (hi - lo):(c + 1) * (hi - lo)], want[:, c * 40 + lo:c * 40 + hi])

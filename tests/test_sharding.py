@@ -60,3 +60,29 @@ def test_gloo_world2_reduce_and_gather():
         g = np.array(g)
         assert np.allclose(g[0], sharding.digest(np.arange(0, 5.0)))
         assert np.allclose(g[1], sharding.digest(np.arange(5, 10.0)))
+
+
+def _ring_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    W, cols = 10, 7
+    lo, hi = sharding.shard_bounds(W, world, rank)
+    mirror = torch.full((W, cols), -1.0, dtype=torch.float64)
+    mirror[lo:hi] = torch.arange(lo * cols, hi * cols, dtype=torch.float64).reshape(hi - lo, cols)
+    sharding.exchange_rings(dist, mirror, lo, hi)
+    out[rank] = mirror.numpy().copy()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_exchange_gloo(world):
+    """Line-split boundary exchange: after one exchange every rank holds every lane's rows."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = mp.Manager().dict()
+    mp.spawn(_ring_worker, args=(world, port, out), nprocs=world, join=True)
+    want = np.arange(10 * 7, dtype=np.float64).reshape(10, 7)
+    for r in range(world):
+        assert np.array_equal(out[r], want)
