@@ -925,6 +925,8 @@ void task_parts(int kind, int j, const SegLayout& L, const std::string& bi, cons
 // instruction cache.
 struct LitCtx {
     std::function<std::string(int)> cst;  // const slot -> expression
+    int sw_bit = -1;                       // >= 0: switch task writes its change flag to bit sw_bit of swbits
+    bool chg_flag = false;                 // switch "changed" slots collapsed into needS
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
@@ -961,6 +963,15 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         if (t.kind == K_BWD)
             o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
+    } else if (t.kind == K_SW && c.sw_bit >= 0) {
+        // change flag into the warp's bit mask; event logging, the refactor flag
+        // and wflag happen once per pass in the (rare) non-zero-mask path
+        o << "int now = " << c.cst(t.ck[2]) << " != 0.0 ? 1 : 0; ";
+        for (size_t j = 3; j < t.ck.size(); ++j) o << "if (t >= " << c.cst(t.ck[j]) << ") now ^= 1; ";
+        o << "const double chg = (double)now != LD(" << t.f[0] << ") ? 1.0 : 0.0; "
+          << (c.chg_flag ? std::string() : "ST(" + std::to_string(t.f[1]) + ", chg); ") << "ST(" << t.f[0]
+          << ", (double)now); ST(" << t.f[2] << ", now != 0 ? " << c.cst(t.ck[0]) << " : " << c.cst(t.ck[1])
+          << "); swbits |= (chg != 0.0 ? 1ull : 0ull) << " << c.sw_bit << ";";
     } else if (t.kind == K_SW) {
         o << "int now = " << c.cst(t.ck[2]) << " != 0.0 ? 1 : 0; ";
         for (size_t j = 3; j < t.ck.size(); ++j) o << "if (t >= " << c.cst(t.ck[j]) << ") now ^= 1; ";
@@ -1103,6 +1114,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         return "__ldg(C + " + std::to_string(static_cast<long long>(k) * lanes) + ")";
     };
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
+    const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
+    std::vector<std::pair<std::string, std::vector<int>>> sw_tables;
     auto region_code = [&](const Sched& sc) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -1113,11 +1126,29 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             rc << "    switch (warp) {\n";
             for (int w = 0; w < G; ++w) {
                 rc << "    case " << w << ": {\n";
+                std::vector<int> sw_ids;  // process id per swbits bit
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
                     if (p > 0) rc << "      BAR();\n";
                     std::vector<int> ordered;
                     segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
-                    for (int id : ordered) rc << "      " << task_literal(g.tasks[static_cast<size_t>(id)], lctx) << "\n";
+                    for (int id : ordered) {
+                        const Task& t = g.tasks[static_cast<size_t>(id)];
+                        LitCtx c = lctx;
+                        if (t.kind == K_SW && switch_bits && sw_ids.size() < 64) {
+                            c.sw_bit = static_cast<int>(sw_ids.size());
+                            c.chg_flag = g.chg_flag;
+                            sw_ids.push_back(t.f[3]);
+                        }
+                        rc << "      " << task_literal(t, c) << "\n";
+                    }
+                }
+                if (!sw_ids.empty()) {
+                    const std::string tab = "kSwIds" + std::to_string(sw_tables.size());
+                    sw_tables.push_back({tab, sw_ids});
+                    rc << "      if (swbits != 0ull) { wflag = 1;" << (g.chg_flag ? " needS[lane] = 1;" : "")
+                       << " if (live && a.events) { unsigned long long b = swbits; while (b) { const int j = __ffsll((long long)b) - 1; "
+                          "b &= b - 1; const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
+                          "a.events[3*e+1] = gl; a.events[3*e+2] = " << tab << "[j]; } } } }\n";
                 }
                 rc << "    } break;\n";
             }
@@ -1230,6 +1261,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             csign.push_back(g.contrib_sign[static_cast<size_t>(x)]);
         }
     }
+    for (const auto& tb : sw_tables) carr_i("__constant__", tb.first.c_str(), tb.second);
     carr_i("__device__ const", "kDerSlot", dslot);
     carr_i("__device__ const", "kVC", g.vc_slots);
     carr_i("__device__ const", "kChgSlot", g.chg_flag ? g.chg_slots : std::vector<int>());
@@ -1289,8 +1321,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
-      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1;\n"
-      << "    (void)t; (void)bad; (void)srow; (void)step;\n"
+      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull;\n"
+      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits;\n"
       << "    if (warp == 0) { ";
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
