@@ -617,7 +617,7 @@ struct Sched {
 // earliest-idle warp starves while enough work waits behind the barrier.
 Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& ids,
                       const std::vector<std::vector<int>>& deps, int G, double* makespan) {
-    const long kBarrier = 60;
+    const long kBarrier = knob("EMTB200_CG_BARRIER", 200);
     Sched out;
     const size_t n = ids.size();
     if (n == 0) {
@@ -927,6 +927,7 @@ struct LitCtx {
     std::function<std::string(int)> cst;  // const slot -> expression
     int sw_bit = -1;                       // >= 0: switch task writes its change flag to bit sw_bit of swbits
     bool chg_flag = false;                 // switch "changed" slots collapsed into needS
+    bool dok = true;                       // divergence as an AND-ed predicate (cold index scan)
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
@@ -961,7 +962,10 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         o << "double x = LD(" << t.f[0] << "); ";
         for (const auto& tm : t.terms) o << "x = x - LU(" << tm.first << ") * LD(" << tm.second << "); ";
         if (t.kind == K_BWD)
-            o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
+            if (c.dok)
+                o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= a.div_limit); ";
+            else
+                o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
     } else if (t.kind == K_SW && c.sw_bit >= 0) {
         // change flag into the warp's bit mask; event logging, the refactor flag
@@ -1101,6 +1105,25 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     double span_a = 0, span_b = 0;
     const Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
     const Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
+    if (knob("EMTB200_CG_DUMP", 0)) {  // schedule dump: per phase, per warp "kind x count (cost)"
+        for (const Sched* sc : {&sa, &sb}) {
+            std::fprintf(stderr, "region %s\n", sc == &sa ? "A" : "B");
+            for (size_t p = 0; p < sc->phases.size(); ++p) {
+                std::fprintf(stderr, " phase %zu:", p);
+                for (int w = 0; w < G; ++w) {
+                    std::map<int, std::pair<int, long>> k;
+                    for (int id : sc->phases[p][static_cast<size_t>(w)]) {
+                        auto& e = k[g.tasks[static_cast<size_t>(id)].kind];
+                        e.first += 1;
+                        e.second += g.tasks[static_cast<size_t>(id)].cost;
+                    }
+                    std::fprintf(stderr, " |w%d", w);
+                    for (auto& kv : k) std::fprintf(stderr, " %s%d(%ld)", kKindName[kv.first], kv.second.first, kv.second.second);
+                }
+                std::fprintf(stderr, "\n");
+            }
+        }
+    }
 
     // ---- tables (records: ints + doubles, terms) and per-(phase, warp) segment code
     std::vector<int> rki;
@@ -1108,6 +1131,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     int segs_total = 0;
     const bool straight = opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", opt.mode == 1 ? 1 : 1) != 0;
     LitCtx lctx;
+    const bool dok_mode = straight && knob("EMTB200_CG_DOK", 1) != 0;
+    lctx.dok = dok_mode;
     lctx.cst = [&](int k) -> std::string {
         if (g.invariant(k)) return "kC[" + std::to_string(k) + "]";
         if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * 256) + ")";
@@ -1321,8 +1346,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
-      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull;\n"
-      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits;\n"
+      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
+      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
       << "    if (warp == 0) { ";
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
@@ -1340,13 +1365,31 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      }\n"
       << "    }\n";
     o << code_b;
-    o << "    if (__syncthreads_or(bad != 0x7fffffff && live)) {\n"
-      << "      if (bad != 0x7fffffff) atomicMin(&serr[lane], bad);\n"
-      << "      __syncthreads();\n"
-      << "      if (warp == 0 && live && serr[lane] != 0x7fffffff) { a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = serr[lane]; a.lane_err[4*gl+3] = "
-      << g.solve_layer << "; }\n"
-      << "      return;\n"
-      << "    }\n"
+    if (dok_mode) {
+        // divergence (exec.cpp:229-237): rows only AND a NaN-safe predicate; the
+        // failing node index (the lowest) is found in the cold path
+        std::ostringstream tb;
+        for (int i = 0; i < s.nodes; ++i) tb << (i ? "," : "") << g.off(s.v_base + i);
+        if (s.nodes == 0) tb << "0";
+        o << "    if (__syncthreads_or(!dok && live)) {\n"
+          << "      const int kVoff[" << std::max(1, s.nodes) << "] = {" << tb.str() << "};\n"
+          << "      if (!dok) serr[lane] = 0;\n"
+          << "      __syncthreads();\n"
+          << "      if (warp == 0 && live && serr[lane] != 0x7fffffff) {\n"
+          << "        for (int i = 0; i < " << s.nodes << "; ++i) if (!(fabs(LD(kVoff[i])) <= a.div_limit)) { bad = i; break; }\n"
+          << "        a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
+          << g.solve_layer << ";\n"
+          << "      }\n"
+          << "      return;\n";
+    } else {
+        o << "    if (__syncthreads_or(bad != 0x7fffffff && live)) {\n"
+          << "      if (bad != 0x7fffffff) atomicMin(&serr[lane], bad);\n"
+          << "      __syncthreads();\n"
+          << "      if (warp == 0 && live && serr[lane] != 0x7fffffff) { a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = serr[lane]; a.lane_err[4*gl+3] = "
+          << g.solve_layer << "; }\n"
+          << "      return;\n";
+    }
+    o      << "    }\n"
       << "  }\n";
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
