@@ -65,7 +65,10 @@ typedef struct emt_config {
  * emit_source (proj/src/codegen.cpp:84-230) retargeted to sm_100a — and uses
  * the table-driven generic kernel only when the specialised one cannot be
  * built (e.g. the hot arena exceeds shared memory). Both run on the GPU. */
-enum { EMT_KERNEL_AUTO = 0, EMT_KERNEL_SPECIALISED = 1, EMT_KERNEL_GENERIC = 2 };
+enum { EMT_KERNEL_AUTO = 0, EMT_KERNEL_SPECIALISED = 1, EMT_KERNEL_GENERIC = 2, EMT_KERNEL_TSIMT = 3 };
+/* EMT_KERNEL_TSIMT: generated task-SIMT kernel — one CTA per scenario lane, one
+ * thread per task of a DAG wave (codegen.cpp, generate_tsimt); for few lanes
+ * (latency) and for batches that should spread over every SM. */
 
 /* ExecOptions (proj/include/emtgrid/exec.hpp:17-25). */
 typedef struct emt_exec_options {
@@ -194,7 +197,8 @@ int32_t emt_engine_kernel(const emt_engine* engine);
 const char* emt_engine_source(const emt_engine* engine);
 const char* emt_engine_summary(const emt_engine* engine);
 
-/* Generates the specialised kernel source for a schedule without touching a
+/* Generates the specialised kernel source (warps < 0: the task-SIMT kernel
+ * with -warps warps) for a schedule without touching a
  * device and, when `compile` != 0, compiles it with NVRTC for `arch`
  * (e.g. "sm_100a"). Returned strings stay valid until the next call on this
  * thread. Used by the build check and the CPU test-suite. */

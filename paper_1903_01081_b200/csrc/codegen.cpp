@@ -95,6 +95,8 @@ struct Gen {
     std::vector<int> lazy_fin;  // components whose current no task reads: finalized once per launch
 
     bool lazy_i = true;
+    int ls = 32;     // doubles between consecutive slots of one lane in S[] (32 lanes per CTA; 1 in task-SIMT)
+    int unit = 256;  // record offset units per slot (bytes of a 32-lane row; 1 = slot index in task-SIMT)
     Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
         lazy_i = knob("EMTB200_CG_LAZYI", 1) != 0;
     }
@@ -107,7 +109,7 @@ struct Gen {
             std::string gx;
             if (f[1] < 0) gx = "(0.0)";
             else if (cls[static_cast<size_t>(f[1])] == kDerived) gx = R(f[1]);
-            else gx = "S[" + std::to_string(hot_index[static_cast<size_t>(f[1])] * 32) + "]";
+            else gx = "S[" + std::to_string(hot_index[static_cast<size_t>(f[1])] * ls) + "]";
             o << "      { const double vs = " << R(f[4]) << " - " << R(f[3]) << "; A[(size_t)" << f[0]
               << " * W_] = " << gx << " * vs + " << R(f[2]) << "; }\n";
         }
@@ -126,14 +128,14 @@ struct Gen {
         if (slot < 0) return 0;  // ground sentinel reads the zero slot
         if (cls[static_cast<size_t>(slot)] == kDerived && derived_const[static_cast<size_t>(slot)] < 0) return 0;
         if (hot_index[static_cast<size_t>(slot)] < 0) return 0;  // pass 1 (offsets not assigned yet)
-        return hot_index[static_cast<size_t>(slot)] * 32 * 8;
+        return hot_index[static_cast<size_t>(slot)] * unit;
     }
     int dep_slot(int slot) const {
         if (slot >= 0 && cls[static_cast<size_t>(slot)] == kContrib) return contrib_h[static_cast<size_t>(slot)];
         return slot;
     }
-    int lu_l(int k) const { return l_base_smem >= 0 ? (l_base_smem + k) * 256 : s.l + k; }
-    int lu_u(int k) const { return u_base_smem >= 0 ? (u_base_smem + k) * 256 : s.u + k; }
+    int lu_l(int k) const { return l_base_smem >= 0 ? (l_base_smem + k) * unit : s.l + k; }
+    int lu_u(int k) const { return u_base_smem >= 0 ? (u_base_smem + k) * unit : s.u + k; }
 
     // ---- expressions for the straight-line refactorization
     std::string C(int k) const {
@@ -146,15 +148,15 @@ struct Gen {
             const int k = derived_const[static_cast<size_t>(slot)];
             return k < 0 ? std::string("(0.0)") : C(k);
         }
-        return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]";
+        return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * ls) + "]";
     }
-    std::string Wr(int slot) const { return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * 32) + "]"; }
+    std::string Wr(int slot) const { return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * ls) + "]"; }
     std::string Lw(int k, const std::string& v) const {
-        if (l_base_smem >= 0) return "S[" + std::to_string((l_base_smem + k) * 32) + "] = " + v + ";";
+        if (l_base_smem >= 0) return "S[" + std::to_string((l_base_smem + k) * ls) + "] = " + v + ";";
         return "if (live) A[" + std::to_string(static_cast<long long>(s.l + k) * W) + "] = " + v + ";";
     }
     std::string Uw(int k, const std::string& v) const {
-        if (u_base_smem >= 0) return "S[" + std::to_string((u_base_smem + k) * 32) + "] = " + v + ";";
+        if (u_base_smem >= 0) return "S[" + std::to_string((u_base_smem + k) * ls) + "] = " + v + ";";
         return "if (live) A[" + std::to_string(static_cast<long long>(s.u + k) * W) + "] = " + v + ";";
     }
 
@@ -502,8 +504,8 @@ struct Gen {
             hot_index[static_cast<size_t>(x)] = static_cast<int>(hot_slots.size());
             hot_slots.push_back(x);
         }
-        const size_t per_slot = 32 * sizeof(double);
-        const size_t fixed = 2 * 32 * sizeof(int);  // serr + refactor flags
+        const size_t per_slot = static_cast<size_t>(ls) * sizeof(double);
+        const size_t fixed = 2 * static_cast<size_t>(ls) * sizeof(int);  // serr + refactor flags
         size_t used = hot_slots.size() * per_slot + fixed;
         if (used > opt.smem_budget) return false;
         std::set<int> vc;
@@ -1046,6 +1048,42 @@ std::string segment_code(int kind, int N, bool indep, int bi0, int bd0, const Se
     return o.str();
 }
 
+
+// Task dependencies from the sequential process order (RAW, WAR, WAW), per region.
+std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
+    const size_t nt = tasks.size();
+    std::vector<std::vector<int>> deps(nt);
+    std::map<int, int> last_writer;
+    std::map<int, std::vector<int>> readers;
+    int cur_region = 0;
+    for (size_t i = 0; i < nt; ++i) {
+        const Task& t = tasks[i];
+        if (t.region != cur_region) {
+            last_writer.clear();
+            readers.clear();
+            cur_region = t.region;
+        }
+        std::set<int> d;
+        for (int r : t.reads) {
+            auto it = last_writer.find(r);
+            if (it != last_writer.end()) d.insert(it->second);
+        }
+        for (int w : t.writes) {
+            auto it = last_writer.find(w);
+            if (it != last_writer.end()) d.insert(it->second);
+            for (int rd : readers[w]) d.insert(rd);
+        }
+        d.erase(static_cast<int>(i));
+        deps[i].assign(d.begin(), d.end());
+        for (int r : t.reads) readers[r].push_back(static_cast<int>(i));
+        for (int w : t.writes) {
+            last_writer[w] = static_cast<int>(i);
+            readers[w].clear();
+        }
+    }
+    return deps;
+}
+
 }  // namespace
 
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
@@ -1425,6 +1463,370 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     sum << (straight ? "straight " : "compact ") << "tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
         << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
         << " est_span=" << static_cast<long>(span_a + span_b) << " est_work=" << work;
+    out.summary = sum.str();
+    return true;
+}
+
+}  // namespace emtb200
+
+// =============================================================================
+// Task-SIMT kernel: one CTA per scenario lane, one THREAD per task.
+//
+// The lane-SIMT kernel above puts 32 scenario lanes on the 32 threads of a warp
+// and gives every warp its own straight-line instruction stream; with only a
+// few hundred lanes it runs on a few dozen SMs and each step costs the full
+// instruction latency of one lane's DAG. Here a warp instead executes up to 32
+// *tasks of one kind* of one lane at once (a "wave"): task operands come from a
+// per-thread record table in global memory (L1-resident after the first step,
+// coalesced), lane state lives in the CTA's shared memory at one double per
+// arena slot, and a batch of W lanes is W small CTAs spread over every SM.
+// Waves are the DAG levels of each region split by kind; the list scheduler
+// places them on warps with bar.sync phases, __syncwarp between the waves of
+// one warp. Every task keeps the reference's floating-point operation order.
+// =============================================================================
+
+namespace emtb200 {
+namespace {
+
+struct TsCode {
+    const char* body;  // per-thread code; RI(n) = int record field n, KS(c) = S index of const c,
+                       // TA(j)/TB(j) = term j fields, NTERM = this thread's term count, NT_ = wave max
+};
+
+// Record layout per task: f fields, then ck (as S indices), then [n_terms, (a, b) pairs].
+const char* ts_body(int kind) {
+    switch (kind) {
+        case K_IND: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; S[RI(3)] = ip + g * vs;";
+        case K_CAP: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; S[RI(3)] = -ip - g * vs;";
+        case K_SRL: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; const double d = S[KS(1)]; S[RI(3)] = d * ip + g * vs;";
+        case K_VSRC: return "const double g = S[KS(0)]; const double m = S[KS(1)]; const double w = S[KS(2)]; const double p = S[KS(3)]; S[RI(0)] = g * (w == 0.0 ? m : m * cos(w * t + p));";
+        case K_ISRC: return "const double m = S[KS(0)]; const double w = S[KS(1)]; const double p = S[KS(2)]; S[RI(0)] = w == 0.0 ? m : m * cos(w * t + p);";
+        case K_CSRC: return "const double k = S[KS(0)]; const double x = S[RI(1)]; S[RI(0)] = k * x;";
+        case K_FINC: return "const double vs = S[RI(3)] - S[RI(2)]; const double h = S[RI(1)]; const double g = S[KS(0)]; S[RI(0)] = g * vs + h;";
+        case K_FINS: return "const double vs = S[RI(3)] - S[RI(2)]; const double h = S[RI(1)]; const double g = S[RI(4)]; S[RI(0)] = g * vs + h;";
+        case K_GAIN: return "const double x = S[RI(1)]; const double u = RI(2) ? -x : x; S[RI(0)] = S[KS(0)] * u;";
+        case K_INTEG: return "const double x = S[RI(1)]; const double u = RI(4) ? -x : x; const double s0 = S[RI(2)]; const double s1 = S[RI(3)]; const double c0 = S[KS(0)]; const double y = s0 + c0 * (u + s1); S[RI(2)] = y; S[RI(3)] = u; S[RI(0)] = y;";
+        case K_LAG: return "const double x = S[RI(1)]; const double u = RI(4) ? -x : x; const double s0 = S[RI(2)]; const double s1 = S[RI(3)]; const double c0 = S[KS(0)]; const double c1 = S[KS(1)]; const double y = c0 * s0 + c1 * (u + s1); S[RI(2)] = y; S[RI(3)] = u; S[RI(0)] = y;";
+        case K_PI: return "const double x = S[RI(1)]; const double u = RI(4) ? -x : x; const double s0 = S[RI(2)]; const double s1 = S[RI(3)]; const double kp = S[KS(0)]; const double ki = S[KS(1)]; const double y = s0 + ki * (u + s1); const double o = kp * u + y; S[RI(2)] = y; S[RI(3)] = u; S[RI(0)] = o;";
+        case K_LIM: return "const double x = S[RI(1)]; const double u = RI(2) ? -x : x; const double lo = S[KS(0)]; const double hi = S[KS(1)]; S[RI(0)] = u < lo ? lo : (u > hi ? hi : u);";
+        case K_CMP: return "const double x0 = S[RI(1)]; const double x1 = S[RI(2)]; const double p = RI(3) ? -x0 : x0; const double q = RI(4) ? -x1 : x1; S[RI(0)] = p >= q ? 1.0 : 0.0;";
+        case K_CONST: return "S[RI(0)] = S[KS(0)];";
+        case K_DELAY: return "const double x = S[RI(1)]; S[RI(0)] = RI(2) ? -x : x;";
+        case K_REC: return "a.waves[((size_t)(a.row0 + it) * NCH + RI(0)) * W_ + gl] = S[RI(1)];";
+        case K_LATCH: return "S[RI(1)] = S[RI(0)];";
+        case K_BERG: return "const double vs = S[RI(1)] - S[RI(0)]; const double hp = S[RI(2)]; const double y2 = S[KS(0)]; const double c1 = S[KS(1)]; const double c0 = S[KS(2)]; const int K = (int)S[KS(3)]; const long long pl = (long long)S[KS(4)]; const long long pr = (long long)S[KS(5)] - a.ring_lo; const int L = RI(4); "
+                            "const double be = y2 * vs + hp; int q1 = (step + 1 - K) % L; if (q1 < 0) q1 += L; const int q0 = q1 == 0 ? L - 1 : q1 - 1; "
+                            "const double b1 = __ldcg(a.ring + pl * a.ring_cols + pr + q1); const double b0 = __ldcg(a.ring + pl * a.ring_cols + pr + q0); "
+                            "S[RI(2)] = -(c1 * b1 + c0 * b0); const int w = step % L; A[(size_t)(RI(3) + w) * W_] = be; a.ring[(LB_ + gl) * a.ring_cols + (RI(3) - a.ring_lo) + w] = be;";
+        default: return nullptr;
+    }
+}
+
+struct Wave {
+    int region = 0, level = 0, kind = 0;
+    std::vector<int> tasks;
+    int nf = 0, nc = 0, maxt = 0, rec_base = 0;
+};
+
+}  // namespace
+
+bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
+                    GeneratedKernel& out, Failure& fail) {
+    Gen g(s, ctab, lanes, opt);
+    g.ls = 1;
+    g.unit = 1;
+    g.classify();
+    int facts = 0;
+    g.emit_all(facts);
+    if (facts != 1) {
+        fail = {13, "", "schedule must hold exactly one FactorizeSystem process"};
+        return false;
+    }
+    CodegenOptions o2 = opt;
+    o2.smem_budget = 200 * 1024;
+    o2.lu_in_smem = true;
+    g.opt = o2;
+    bool lu_smem = false;
+    size_t smem = 0;
+    if (!g.assign_hot(lu_smem, smem) || !lu_smem) {
+        fail = {13, "", "task-SIMT: lane state exceeds shared memory"};
+        return false;
+    }
+    g.emit_all(facts);
+    const size_t nt = g.tasks.size();
+    const std::vector<std::vector<int>> deps = task_deps(g.tasks);
+
+    // every constant a task reads gets an S slot, loaded from the lane's column once per launch
+    const int const_base = g.smem_slots();
+    std::map<int, int> cidx;
+    std::vector<int> cslots;
+    for (const Task& t : g.tasks)
+        for (int k : t.ck)
+            if (!cidx.count(k)) {
+                cidx[k] = const_base + static_cast<int>(cslots.size());
+                cslots.push_back(k);
+            }
+    const int nslots = const_base + static_cast<int>(cslots.size());
+
+    // ASAP levels per region; waves = (region, level, kind, #f, #ck, #terms class) chunks of 32
+    std::vector<int> level(nt, 0);
+    for (size_t i = 0; i < nt; ++i)
+        for (int d : deps[i])
+            if (g.tasks[static_cast<size_t>(d)].region == g.tasks[i].region)
+                level[i] = std::max(level[i], level[static_cast<size_t>(d)] + 1);
+    std::map<std::tuple<int, int, int, int, int>, std::vector<int>> groups;
+    for (size_t i = 0; i < nt; ++i) {
+        const Task& t = g.tasks[i];
+        groups[{t.region, level[i], t.kind, static_cast<int>(t.f.size()), static_cast<int>(t.ck.size())}].push_back(static_cast<int>(i));
+    }
+    std::vector<Wave> waves;
+    for (auto& kv : groups) {
+        std::vector<int> ids = kv.second;
+        std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) {
+            return g.tasks[static_cast<size_t>(a)].terms.size() < g.tasks[static_cast<size_t>(b)].terms.size();
+        });
+        for (size_t q = 0; q < ids.size(); q += 32) {
+            Wave w;
+            w.region = std::get<0>(kv.first);
+            w.level = std::get<1>(kv.first);
+            w.kind = std::get<2>(kv.first);
+            w.nf = std::get<3>(kv.first);
+            w.nc = std::get<4>(kv.first);
+            w.tasks.assign(ids.begin() + static_cast<long>(q), ids.begin() + static_cast<long>(std::min(ids.size(), q + 32)));
+            for (int id : w.tasks) w.maxt = std::max(w.maxt, static_cast<int>(g.tasks[static_cast<size_t>(id)].terms.size()));
+            waves.push_back(std::move(w));
+        }
+    }
+    // wave DAG (for the warp scheduler) + cost model (cycles)
+    std::vector<int> wave_of(nt, -1);
+    for (size_t w = 0; w < waves.size(); ++w)
+        for (int id : waves[w].tasks) wave_of[static_cast<size_t>(id)] = static_cast<int>(w);
+    std::vector<Task> wt(waves.size());
+    std::vector<std::vector<int>> wdeps(waves.size());
+    for (size_t w = 0; w < waves.size(); ++w) {
+        std::set<int> d;
+        for (int id : waves[w].tasks)
+            for (int x : deps[static_cast<size_t>(id)])
+                if (wave_of[static_cast<size_t>(x)] != static_cast<int>(w)) d.insert(wave_of[static_cast<size_t>(x)]);
+        wdeps[w].assign(d.begin(), d.end());
+        const int k = waves[w].kind;
+        int c = 90;  // record + operand loads, compute, store
+        if (k == K_VSRC || k == K_ISRC) c = 260;
+        if (k == K_SW) c = 110 + 12 * waves[w].nc;
+        if (k == K_GATHER || k == K_SUM) c = 80 + 10 * waves[w].maxt;
+        if (k == K_FWD) c = 80 + 18 * waves[w].maxt;
+        if (k == K_BWD) c = 130 + 18 * waves[w].maxt;
+        if (k == K_BERG) c = 200;
+        wt[w].cost = c;
+        wt[w].region = waves[w].region;
+    }
+    const int G = std::max(1, std::min(opt.warps, 32));
+    std::vector<int> wa, wb;
+    for (size_t w = 0; w < waves.size(); ++w) (waves[w].region == 0 ? wa : wb).push_back(static_cast<int>(w));
+    double span_a = 0, span_b = 0;
+    const Sched sa = schedule_region(wt, wa, wdeps, G, &span_a);
+    const Sched sb = schedule_region(wt, wb, wdeps, G, &span_b);
+
+    // record table: per wave, field-major [field][32 threads]
+    std::vector<int> rec;
+    for (Wave& w : waves) {
+        w.rec_base = static_cast<int>(rec.size());
+        const int nfield = w.nf + w.nc + (w.maxt > 0 ? 1 + 2 * w.maxt : 0);
+        rec.resize(rec.size() + static_cast<size_t>(nfield) * 32, 0);
+        for (size_t j = 0; j < w.tasks.size(); ++j) {
+            const Task& t = g.tasks[static_cast<size_t>(w.tasks[j])];
+            auto put = [&](int field, int v) { rec[static_cast<size_t>(w.rec_base + field * 32) + j] = v; };
+            for (int f = 0; f < w.nf; ++f) put(f, t.f[static_cast<size_t>(f)]);
+            for (int c = 0; c < w.nc; ++c) put(w.nf + c, cidx[t.ck[static_cast<size_t>(c)]]);
+            if (w.maxt > 0) {
+                put(w.nf + w.nc, static_cast<int>(t.terms.size()));
+                for (size_t q = 0; q < t.terms.size(); ++q) {
+                    put(w.nf + w.nc + 1 + 2 * static_cast<int>(q), t.terms[q].first);
+                    put(w.nf + w.nc + 2 + 2 * static_cast<int>(q), t.terms[q].second);
+                }
+            }
+        }
+    }
+
+    auto ks = [](std::string text, int nf) {
+        for (size_t pos; (pos = text.find("KS(")) != std::string::npos;)
+            text.replace(pos, 3, "RI(" + std::to_string(nf) + " + ");
+        return text;
+    };
+    auto wave_code = [&](const Wave& w) {
+        std::ostringstream c;
+        c << "      if (lane < " << w.tasks.size() << ") { const int rb = " << w.rec_base << " + lane; ";
+        const int tb = w.nf + w.nc;
+        if (w.kind == K_GATHER || w.kind == K_SUM) {
+            c << "const int n = RI(" << tb << "); double acc = 0.0; ";
+            for (int j = 0; j < w.maxt; ++j)
+                c << "if (" << j << " < n) { const double v = S[RI(" << tb + 1 + 2 * j << ")]; acc = acc + (RI(" << tb + 2 + 2 * j
+                  << ") ? -v : v); } ";
+            c << "S[RI(0)] = acc;";
+        } else if (w.kind == K_FWD || w.kind == K_BWD) {
+            c << "const int n = RI(" << tb << "); double x = S[RI(0)]; ";
+            for (int j = 0; j < w.maxt; ++j)
+                c << "if (" << j << " < n) x = x - S[RI(" << tb + 1 + 2 * j << ")] * S[RI(" << tb + 2 + 2 * j << ")]; ";
+            if (w.kind == K_BWD) c << "x = x / S[RI(1)]; dok = dok & (fabs(x) <= a.div_limit); ";
+            c << "S[RI(0)] = x;";
+        } else if (w.kind == K_SW) {
+            c << "int now = S[KS(2)] != 0.0 ? 1 : 0; ";
+            for (int j = 3; j < w.nc; ++j) c << "if (t >= S[KS(" << j << ")]) now ^= 1; ";
+            c << "const double chg = (double)now != S[RI(0)] ? 1.0 : 0.0; ";
+            if (!g.chg_flag) c << "S[RI(1)] = chg; ";
+            c << "S[RI(0)] = (double)now; S[RI(2)] = now != 0 ? S[KS(0)] : S[KS(1)]; "
+              << "if (chg != 0.0) { wflag = 1; " << (g.chg_flag ? "needS[0] = 1; " : "")
+              << "if (a.events) { const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
+                 "a.events[3*e+1] = gl; a.events[3*e+2] = RI(3); } } }";
+        } else {
+            const char* b = ts_body(w.kind);
+            if (b == nullptr) return std::string("#error unsupported task kind\n");
+            c << b;
+        }
+        c << " }\n";
+        return ks(c.str(), w.nf);
+    };
+    auto region_code = [&](const Sched& sc) {
+        std::ostringstream rc;
+        rc << "    switch (warp) {\n";
+        for (int wp = 0; wp < G; ++wp) {
+            rc << "    case " << wp << ": {\n";
+            for (size_t p = 0; p < sc.phases.size(); ++p) {
+                if (p > 0) rc << "      BAR();\n";
+                bool first = true;
+                for (int wid : sc.phases[p][static_cast<size_t>(wp)]) {
+                    if (!first) rc << "      __syncwarp();\n";
+                    first = false;
+                    rc << wave_code(waves[static_cast<size_t>(wid)]);
+                }
+            }
+            rc << "    } break;\n";
+        }
+        rc << "    }\n";
+        return rc.str();
+    };
+    const std::string code_a = region_code(sa);
+    const std::string code_b = region_code(sb);
+
+    std::ostringstream o;
+    const int nhot = static_cast<int>(g.hot_slots.size());
+    const int NTH = 32 * G;
+    o << "// generated by emtb200 codegen (task-SIMT): " << s.nodes << " nodes, " << s.comps << " components, " << lanes
+      << " lanes (one CTA each), " << G << " warps, " << nt << " tasks, " << waves.size() << " waves\n";
+    o << "#define W_ " << static_cast<long long>(lanes) << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ "
+      << opt.lane_begin << "LL\n";
+    o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
+      << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
+      << "  double* ring; long long ring_lo; long long ring_cols; };\n";
+    auto garr = [&](const char* name, const std::vector<int>& v) {
+        o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
+        for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
+        if (v.empty()) o << "0";
+        o << "};\n";
+    };
+    garr("kRec", rec);
+    std::vector<int> hot_arena(g.hot_slots.begin() + 1, g.hot_slots.end());
+    garr("kHot", hot_arena);
+    garr("kCst", cslots);
+    std::vector<int> dslot, dconst, cslot, chot, csign;
+    for (int x = 0; x < s.extent; ++x) {
+        if (g.cls[static_cast<size_t>(x)] == kDerived) {
+            dslot.push_back(x);
+            dconst.push_back(g.derived_const[static_cast<size_t>(x)]);
+        } else if (g.cls[static_cast<size_t>(x)] == kContrib) {
+            const int h = g.contrib_h[static_cast<size_t>(x)];
+            cslot.push_back(x);
+            chot.push_back(g.cls[static_cast<size_t>(h)] == kHot ? g.hot_index[static_cast<size_t>(h)] : -1);
+            csign.push_back(g.contrib_sign[static_cast<size_t>(x)]);
+        }
+    }
+    garr("kDerSlot", dslot);
+    garr("kDerConst", dconst);
+    garr("kConSlot", cslot);
+    garr("kConHot", chot);
+    garr("kConSign", csign);
+    garr("kChgSlot", g.chg_flag ? g.chg_slots : std::vector<int>());
+    o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n"
+      << "#define RI(n) __ldg(kRec + rb + (n) * 32)\n";
+    std::string refac = g.emit_refactor();
+    for (size_t pos; (pos = refac.find("needS[lane]")) != std::string::npos;) refac.replace(pos, 11, "needS[0]");
+    std::set<int> written_a;
+    for (const Task& t : g.tasks)
+        if (t.region == 0)
+            for (int w : t.writes) written_a.insert(w);
+    const int min_blocks = std::max(1, knob("EMTB200_TS_MINBLOCKS", 4));
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NTH << ", " << min_blocks << ") emt_ts_kernel(const KArgs a) {\n"
+      << "  extern __shared__ double S[];\n"
+      << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
+      << "  const int gl = blockIdx.x; const bool live = true; (void)live;\n"
+      << "  double* __restrict__ A = a.arena + gl;\n"
+      << "  const double* __restrict__ C = a.ctab + gl; (void)C;\n"
+      << "  int* needS = (int*)(S + " << nslots << ");\n"
+      << "  for (int q = threadIdx.x; q < " << nhot - 1 << "; q += " << NTH << ") S[q + 1] = A[(size_t)kHot[q] * W_];\n"
+      << "  for (int q = threadIdx.x; q < " << s.l_col.size() << "; q += " << NTH << ") S[" << g.l_base_smem << " + q] = A[(size_t)("
+      << s.l << " + q) * W_];\n"
+      << "  for (int q = threadIdx.x; q < " << s.u_col.size() << "; q += " << NTH << ") S[" << g.u_base_smem << " + q] = A[(size_t)("
+      << s.u << " + q) * W_];\n"
+      << "  for (int q = threadIdx.x; q < " << cslots.size() << "; q += " << NTH << ") S[" << const_base << " + q] = __ldg(C + (size_t)kCst[q] * W_);\n"
+      << "  if (threadIdx.x == 0) { S[0] = 0.0; needS[0] = 0; }\n"
+      << "  __syncthreads();\n"
+      << "  for (int it = 0; it < a.nsteps; ++it) {\n"
+      << "    const int step = a.step0 + it;\n"
+      << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
+      << "    int wflag = 0; int srow = -1; bool dok = true;\n"
+      << "    (void)t; (void)srow; (void)step; (void)dok;\n"
+      << "    if (threadIdx.x == 0) { ";
+    for (int x : s.watch)
+        if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
+    o << "}\n" << code_a
+      << "    if (__syncthreads_or(wflag)) {\n"
+      << "      if (threadIdx.x == 0) {\n" << refac
+      << "        a.refac[a.row0 + it] = 1;\n"
+      << "      }\n"
+      << "      if (__syncthreads_or(srow >= 0)) {\n"
+      << "        if (threadIdx.x == 0 && srow >= 0) { a.lane_err[4*gl] = 8; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = srow; a.lane_err[4*gl+3] = "
+      << g.fact_layer << "; }\n"
+      << "        return;\n"
+      << "      }\n"
+      << "    }\n"
+      << code_b;
+    std::ostringstream tb;
+    for (int i = 0; i < s.nodes; ++i) tb << (i ? "," : "") << g.off(s.v_base + i);
+    if (s.nodes == 0) tb << "0";
+    o << "    if (__syncthreads_or(!dok)) {\n"
+      << "      const int kVoff[" << std::max(1, s.nodes) << "] = {" << tb.str() << "};\n"
+      << "      if (threadIdx.x == 0) { int bad = 0; for (int i = 0; i < " << s.nodes << "; ++i) if (!(fabs(S[kVoff[i]]) <= a.div_limit)) { bad = i; break; }\n"
+      << "        a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = " << g.solve_layer << "; }\n"
+      << "      return;\n"
+      << "    }\n"
+      << "  }\n"
+      << "  __syncthreads();\n"
+      << "  for (int q = threadIdx.x; q < " << nhot - 1 << "; q += " << NTH << ") A[(size_t)kHot[q] * W_] = S[q + 1];\n"
+      << "  for (int q = threadIdx.x; q < " << s.l_col.size() << "; q += " << NTH << ") A[(size_t)(" << s.l << " + q) * W_] = S["
+      << g.l_base_smem << " + q];\n"
+      << "  for (int q = threadIdx.x; q < " << s.u_col.size() << "; q += " << NTH << ") A[(size_t)(" << s.u << " + q) * W_] = S["
+      << g.u_base_smem << " + q];\n"
+      << "  if (a.nsteps > 0) {\n"
+      << "    for (int q = threadIdx.x; q < " << dslot.size() << "; q += " << NTH << ") A[(size_t)kDerSlot[q] * W_] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * W_];\n"
+      << "    for (int q = threadIdx.x; q < " << cslot.size() << "; q += " << NTH << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q]]; "
+      << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
+      << "    for (int q = threadIdx.x; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << NTH << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n"
+      << "    if (threadIdx.x == 0) {\n" << g.emit_lazy_finalize() << "    }\n"
+      << "  }\n"
+      << "}\n";
+    out.source = o.str();
+    out.name = "emt_ts_kernel";
+    out.warps = G;
+    out.smem_bytes = static_cast<size_t>(nslots) * sizeof(double) + 16;
+    out.hot_slots = nhot;
+    out.lu_smem = 1;
+    out.phases_a = static_cast<int>(sa.phases.size());
+    out.phases_b = static_cast<int>(sb.phases.size());
+    out.tasks = static_cast<int>(nt);
+    std::ostringstream sum;
+    sum << "task-simt tasks=" << nt << " waves=" << waves.size() << " slots=" << nslots << " smem=" << out.smem_bytes
+        << " rec=" << rec.size() * 4 << "B phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
+        << " est_span=" << static_cast<long>(span_a + span_b);
     out.summary = sum.str();
     return true;
 }

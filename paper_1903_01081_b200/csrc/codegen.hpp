@@ -41,4 +41,10 @@ struct GeneratedKernel {
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                      GeneratedKernel& out, Failure& fail);
 
+/// Task-SIMT variant: one CTA per scenario lane, one thread per task of a
+/// DAG wave (see codegen.cpp); `out.name` = "emt_ts_kernel", launch with
+/// grid = lanes, block = 32 * out.warps, dynamic smem = out.smem_bytes.
+bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
+                    GeneratedKernel& out, Failure& fail);
+
 }  // namespace emtb200

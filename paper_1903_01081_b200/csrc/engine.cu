@@ -20,6 +20,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -814,6 +815,37 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     }
     e->kernel_mode = EMT_KERNEL_GENERIC;
     e->summary = "generic table-driven kernel, grid=" + std::to_string(e->grid) + " block=" + std::to_string(e->block);
+    const char* kenv = std::getenv("EMTB200_KERNEL");
+    if (c.kernel == EMT_KERNEL_AUTO && kenv && std::strcmp(kenv, "tsimt") == 0) c.kernel = EMT_KERNEL_TSIMT;
+    if (c.kernel == EMT_KERNEL_TSIMT) {
+        CodegenOptions opt;
+        opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 4;
+        opt.lane_begin = e->lane_begin;
+        Failure gf;
+        std::string log;
+        const auto t0 = std::chrono::steady_clock::now();
+        bool ok = generate_tsimt(e->sched, e->host_ctab, e->W, opt, e->gen, gf);
+        const double gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (ok) ok = jit_load(e->gen.source, e->gen.name, e->device, e->jit, log);
+        if (ok && driver()->FuncSetAttribute(e->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                             static_cast<int>(e->gen.smem_bytes)) != CUDA_SUCCESS) {
+            ok = false;
+            log = "cuFuncSetAttribute(max dynamic smem) failed";
+        }
+        if (ok) {  // record tables are read through L1: leave it most of the SRAM
+            const int carve = std::getenv("EMTB200_TS_CARVEOUT") ? std::atoi(std::getenv("EMTB200_TS_CARVEOUT")) : 25;
+            driver()->FuncSetAttribute(e->jit.function, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carve);
+        }
+        if (!ok)
+            return set_error(gf.code ? gf.code : EMT_CUDA_ERROR,
+                             "task-SIMT kernel unavailable: " + (gf.message.empty() ? log.substr(0, 2000) : gf.message));
+        e->kernel_mode = EMT_KERNEL_TSIMT;
+        char b[160];
+        std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s", gen_s, e->jit.compile_seconds, e->jit.cached ? " (cached)" : "");
+        e->summary = "task-SIMT kernel: " + e->gen.summary + b;
+        *out = e.release();
+        return EMT_OK;
+    }
     if (c.kernel != EMT_KERNEL_GENERIC) {
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
@@ -906,12 +938,13 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         if (sync) return emt_engine_sync(e);
         return EMT_OK;
     }
-    if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
+    if (e->kernel_mode == EMT_KERNEL_SPECIALISED || e->kernel_mode == EMT_KERNEL_TSIMT) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols};
         void* params[] = {&a};
-        const unsigned grid = static_cast<unsigned>((e->W + 31) / 32);
+        const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
+        const unsigned grid = static_cast<unsigned>(ts ? e->W : (e->W + 31) / 32);
         const CUresult r = driver()->LaunchKernel(e->jit.function, grid, 1, 1, static_cast<unsigned>(32 * e->gen.warps), 1, 1,
                                           static_cast<unsigned>(e->gen.smem_bytes), reinterpret_cast<CUstream>(e->stream),
                                           params, nullptr);
@@ -1140,7 +1173,10 @@ emt_status emt_codegen(const char* schedule_text, const double* const_table, int
     CodegenOptions opt;
     opt.warps = warps > 0 ? warps : 4;
     GeneratedKernel g;
-    if (!generate_kernel(s, ct, width, opt, g, f)) return set_error(f.code, f.message);
+    const bool ts = warps < 0;  // negative warp count selects the task-SIMT generator
+    if (ts) opt.warps = -warps;
+    if (!(ts ? generate_tsimt(s, ct, width, opt, g, f) : generate_kernel(s, ct, width, opt, g, f)))
+        return set_error(f.code, f.message);
     src_out = g.source;
     sum_out = g.summary;
     if (compile) {

@@ -52,7 +52,7 @@ class _Config(ctypes.Structure):
                 ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
-KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC = 0, 1, 2
+KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT = 0, 1, 2, 3
 
 
 class _Options(ctypes.Structure):

@@ -110,11 +110,11 @@ def test_c4_oracle_runs_and_lines_carry_power():
 # ------------------------------------------------------------------ GPU parity
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "tsimt"])
 @pytest.mark.parametrize("name,tau", [("line_open", 10 * DT), ("line_open", 6.6 * DT), ("line_matched", 3 * DT)])
 def test_engine_line_bitwise_equals_oracle(name, tau, kernel):
     from paper_1903_01081_b200 import engine
-    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}[kernel]
+    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}[kernel]
     b = line_case(name, tau)
     want = run_oracle(b, 400)
     eng = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k)
@@ -125,11 +125,11 @@ def test_engine_line_bitwise_equals_oracle(name, tau, kernel):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "tsimt"])
 def test_engine_c4_matches_oracle(kernel):
     """C4 line-split batch (cross-lane, cross-CTA ring reads; launches capped at K-1 passes)."""
     from paper_1903_01081_b200 import engine
-    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}[kernel]
+    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}[kernel]
     b = c4_case(40)  # 2 CTAs of 32 lanes for the specialised kernel
     want = run_oracle(b, 900)
     eng = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k)
@@ -145,22 +145,22 @@ def test_engine_c4_kernels_agree_bitwise():
     from paper_1903_01081_b200 import engine
     b = c4_case(40)
     out = []
-    for k in (engine.KERNEL_SPECIALISED, engine.KERNEL_GENERIC):
+    for k in (engine.KERNEL_SPECIALISED, engine.KERNEL_GENERIC, engine.KERNEL_TSIMT):
         eng = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k)
         eng.reserve(700)
         eng.advance(700)
         out.append(eng.waves().values)
-    assert bitwise_equal(out[0], out[1])
+    assert bitwise_equal(out[0], out[1]) and bitwise_equal(out[0], out[2])
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kernel", ["auto", "generic"])
+@pytest.mark.parametrize("kernel", ["auto", "generic", "tsimt"])
 def test_line_split_shards_with_ring_exchange_equal_one_engine(kernel):
     """Two lane-shard engines (the 2-GPU split, here on one device) that swap
     their mirror rows after every launch of K-1 passes == one engine on all lanes."""
     import torch
     from paper_1903_01081_b200 import engine
-    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}[kernel]
+    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}[kernel]
     b = c4_case(40)
     whole = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, kernel=k)
     whole.reserve(600)

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 BITWISE = {"rc_discharge", "switched_dc_w3", "control_only", "diverging", "singular_islands"}
 
 
-KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC}
+KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}
 
 
 @pytest.mark.parametrize("kernel", sorted(KERNELS))
@@ -117,19 +117,20 @@ def test_auto_selects_specialised_kernel(name):
 
 
 def test_specialised_equals_generic_bitwise_full_n1_sample():
-    """Both device kernels run the same operation order: identical bits on a 64-lane N-1 batch."""
+    """All device kernels run the same operation order: identical bits on a 64-lane N-1 batch."""
     import bench
     batch, info = bench.build_batch(64)
     out = []
-    for k in (engine.KERNEL_SPECIALISED, engine.KERNEL_GENERIC):
+    for k in (engine.KERNEL_SPECIALISED, engine.KERNEL_GENERIC, engine.KERNEL_TSIMT):
         eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, kernel=k)
         eng.reserve(3000)
         eng.advance(3000)
         out.append((eng.waves().values, eng.stats().factor_count, eng.events(), eng.state()))
-    assert bitwise_equal(out[0][0], out[1][0])
-    assert out[0][1] == out[1][1]
-    assert np.array_equal(out[0][2], out[1][2])
-    assert bitwise_equal(out[0][3], out[1][3])
+    for other in out[1:]:
+        assert bitwise_equal(out[0][0], other[0])
+        assert out[0][1] == other[1]
+        assert np.array_equal(out[0][2], other[2])
+        assert bitwise_equal(out[0][3], other[3])
 
 
 def test_shard_refactor_steps_union_is_global_factor_count():
