@@ -1294,7 +1294,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -1333,6 +1333,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     carr_i("__device__ const", "kConHot", chot);
     carr_i("__device__ const", "kConSign", csign);
     o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
+    // a failing CTA leaves the step loop: release CTAs waiting on its progress word
+    o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + blockIdx.x, 0x3fffffffu); } while (0)\n";
     o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
       << "#define ST(o, v) (*(double*)(Sb + (o)) = (v))\n"
       << "#define SGN(x, n) ((n) ? -(x) : (x))\n";
@@ -1379,13 +1381,33 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (const Task& t : g.tasks)
         if (t.region == 0)
             for (int w : t.writes) written_a.insert(w);
-    o << "  __syncthreads();\n"
+    o << "  __shared__ int s_cmin;\n"
+      << "  if (threadIdx.x == 0) s_cmin = -0x3fffffff;\n"
+      << "  __syncthreads();\n"
       << "  int it = 0;\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
       << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
+      << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
+      << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
+      << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
+      << "      __syncthreads();\n"
+      << "      if (threadIdx.x == 0) {\n"
+      << "        const long long t0 = clock64(); int m;\n"
+      << "        for (;;) {\n"
+      << "          m = 0x7fffffff;\n"
+      << "          for (int c = 0; c < a.nblocks; ++c) { unsigned int v; asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
+      << "          if (m >= step + 2 - a.min_k) break;\n"
+      << "          if (clock64() - t0 > 8000000000LL) { m = -1; break; }\n"
+      << "        }\n"
+      << "        __threadfence();\n"
+      << "        s_cmin = m;\n"
+      << "      }\n"
+      << "      __syncthreads();\n"
+      << "      if (s_cmin < 0) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
+      << "    }\n"
       << "    if (warp == 0) { ";
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
@@ -1399,7 +1421,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      if (__syncthreads_or(srow >= 0 && live)) {\n"
       << "        if (warp == 0 && live && srow >= 0) { a.lane_err[4*gl] = 8; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = srow; a.lane_err[4*gl+3] = "
       << g.fact_layer << "; }\n"
-      << "        return;\n"
+      << "        FAILPUB(); return;\n"
       << "      }\n"
       << "    }\n";
     o << code_b;
@@ -1418,16 +1440,20 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "        a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
           << g.solve_layer << ";\n"
           << "      }\n"
-          << "      return;\n";
+          << "      FAILPUB(); return;\n";
     } else {
         o << "    if (__syncthreads_or(bad != 0x7fffffff && live)) {\n"
           << "      if (bad != 0x7fffffff) atomicMin(&serr[lane], bad);\n"
           << "      __syncthreads();\n"
           << "      if (warp == 0 && live && serr[lane] != 0x7fffffff) { a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = serr[lane]; a.lane_err[4*gl+3] = "
           << g.solve_layer << "; }\n"
-          << "      return;\n";
+          << "      FAILPUB(); return;\n";
     }
     o      << "    }\n"
+      << "    if (a.progress != nullptr && threadIdx.x == 0) {\n"
+      << "      __threadfence();\n"
+      << "      asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\");\n"
+      << "    }\n"
       << "  }\n";
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
@@ -1717,7 +1743,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; };\n";
     auto garr = [&](const char* name, const std::vector<int>& v) {
         o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];

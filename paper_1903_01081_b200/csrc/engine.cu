@@ -55,6 +55,8 @@ struct CgArgs {
     double div_limit;
     double* ring;  // line-end history mirror, lane-major [batch lane][ring slot - ring_lo]
     long long ring_lo, ring_cols;
+    unsigned int* progress;  // persistent line-coupled run: passes completed per CTA (else null)
+    int min_k, nblocks;
 };
 
 struct DevPlan {
@@ -473,6 +475,9 @@ struct emt_engine {
     int max_chunk = INT_MAX;  // passes per launch; < K when line ends couple lanes across CTAs
     double* d_ring = nullptr;   // line-end history mirror (owned unless attached)
     bool ring_owned = true;
+    unsigned int* d_progress = nullptr;  // persistent line-coupled mode: per-CTA pass counters
+    bool persistent_lines = false;
+    int min_k = 0;
     int failed = 0;
     int max_events = 1 << 16;
     double divergence_limit = kDefaultDivergence;
@@ -489,6 +494,7 @@ struct emt_engine {
         if (jit.module && driver()) driver()->ModuleUnload(jit.module);
         for (void* p : allocations) cudaFree(p);
         if (d_ring && ring_owned) cudaFree(d_ring);
+        if (d_progress) cudaFree(d_progress);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
@@ -868,6 +874,20 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         }
         if (ok) {
             e->kernel_mode = EMT_KERNEL_SPECIALISED;
+            // Line-coupled lanes in one engine: one persistent launch with per-CTA
+            // progress words instead of relaunching every K-1 passes (all CTAs must
+            // be co-resident: one 32-lane CTA per SM at most).
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
+            const char* pe = std::getenv("EMTB200_LINE_PERSISTENT");
+            if (e->plan.ring != nullptr && e->max_chunk != INT_MAX && (e->W + 31) / 32 <= sms &&
+                !(pe && std::strcmp(pe, "0") == 0)) {
+                CUDA_TRY(cudaMalloc(&e->d_progress, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32)));
+                CUDA_TRY(cudaMemset(e->d_progress, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32)));
+                e->min_k = e->max_chunk + 1;
+                e->max_chunk = INT_MAX;
+                e->persistent_lines = true;
+            }
             char b[160];
             std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s", gen_s, e->jit.compile_seconds,
                           e->jit.cached ? " (cached)" : "");
@@ -941,7 +961,8 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
     if (e->kernel_mode == EMT_KERNEL_SPECIALISED || e->kernel_mode == EMT_KERNEL_TSIMT) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
-                 e->plan.ring, e->plan.ring_lo, e->plan.ring_cols};
+                 e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
+                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32)};
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
         const unsigned grid = static_cast<unsigned>(ts ? e->W : (e->W + 31) / 32);
@@ -1097,6 +1118,8 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
     CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
     CUDA_TRY(cudaMemsetAsync(e->plan.n_events, 0, sizeof(int), e->stream));
+    if (e->d_progress)
+        CUDA_TRY(cudaMemsetAsync(e->d_progress, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32), e->stream));
     if (e->d_refactored) CUDA_TRY(cudaMemsetAsync(e->d_refactored, 0, static_cast<size_t>(std::max(1, e->capacity)), e->stream));
     e->step = 0;
     e->rows = 0;
@@ -1109,7 +1132,7 @@ emt_status emt_engine_ring(emt_engine* e, void** device_ptr, int32_t* lanes, int
     if (device_ptr) *device_ptr = e->plan.ring;
     if (lanes) *lanes = e->plan.ring ? e->width : 0;
     if (cols) *cols = e->plan.ring_cols;
-    if (max_chunk) *max_chunk = e->max_chunk == INT_MAX ? 0 : e->max_chunk;
+    if (max_chunk) *max_chunk = e->persistent_lines ? e->min_k - 1 : (e->max_chunk == INT_MAX ? 0 : e->max_chunk);
     return EMT_OK;
 }
 
@@ -1123,6 +1146,10 @@ emt_status emt_engine_attach_ring(emt_engine* e, void* device_ptr) {
     if (e->ring_owned && e->d_ring) cudaFree(e->d_ring);
     e->d_ring = static_cast<double*>(device_ptr);
     e->ring_owned = false;
+    if (e->persistent_lines) {  // peers on other GPUs: back to launches of K-1 passes + host exchange
+        e->persistent_lines = false;
+        e->max_chunk = e->min_k - 1;
+    }
     e->plan.ring = e->d_ring;
     return EMT_OK;
 }

@@ -101,11 +101,11 @@ class LineSplitShard:
         self.eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width,
                                  device=device, lane_begin=lo, lane_count=hi - lo, **engine_kw)
         ptr, lanes, cols, self.max_chunk = self.eng.ring()
+        self.world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
         self.mirror = None
-        if ptr:
+        if ptr and self.world > 1:  # peers on other ranks: the collective writes into this buffer
             self.mirror = torch.zeros((lanes, cols), dtype=torch.float64, device=torch.device("cuda", device))
             self.eng.attach_ring(self.mirror.data_ptr())
-        self.world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
 
     def advance(self, steps: int) -> None:
         import torch
