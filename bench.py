@@ -180,7 +180,16 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_DIST_BACKEND=gloo + BENCH_SHARE_GPU=1 lets the multi-rank control flow be
+        # exercised with several ranks on one GPU (NCCL refuses duplicate devices)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        local = 0
+    cdev = None if world > 1 and dist.get_backend() == "gloo" else local  # collectives' tensor device
     torch.cuda.set_device(local)
     dev = local
 
@@ -232,6 +241,8 @@ def run_ours(args):
     per_launch_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     local_ms = sum(per_launch_ms)
     st = eng.stats()
+    last = eng.waves(total_steps - S, S).values
+    fc_local, steps_local = st.factor_count, eng.refactor_steps()
 
     # ---- e2e through the public API with HOST buffers, rank-local shard. The engine
     # (schedule parse + code generation + JIT, the analogue of compile_task, which the
@@ -282,22 +293,20 @@ def run_ours(args):
         e2e_digest_ok = bool(np.array_equal(host_waves, eng.waves(0, S).values))
         e2.close()
 
-    last = eng.waves(total_steps - S, S).values
     if world > 1:
-        max_ms = sharding.reduce_max(dist, local_ms, device=dev)
-        e2e_max = sharding.reduce_max(dist, e2e_local, device=dev)
+        max_ms = sharding.reduce_max(dist, local_ms, device=cdev)
+        e2e_max = sharding.reduce_max(dist, e2e_local, device=cdev)
         # final result gather (the only inter-GPU traffic): per-rank digests + refactor steps
-        digests = sharding.gather_digests(dist, sharding.digest(last), world, device=dev)
-        steps_local = eng.refactor_steps()
-        mx = int(sharding.reduce_max(dist, float(len(steps_local)), device=dev))
+        digests = sharding.gather_digests(dist, sharding.digest(last), world, device=cdev)
+        mx = int(sharding.reduce_max(dist, float(len(steps_local)), device=cdev))
         pad = np.full(max(mx, 1), -1.0)
         pad[: len(steps_local)] = steps_local
-        tt = torch.tensor(pad, dtype=torch.float64, device=dev)
+        tt = torch.tensor(pad, dtype=torch.float64, device=cdev)
         parts = [torch.zeros_like(tt) for _ in range(world)]
         dist.all_gather(parts, tt)
         fc = sharding.combine_factor_counts([[int(x) for x in p.cpu().numpy() if x >= 0] for p in parts])
     else:
-        max_ms, e2e_max, fc = local_ms, e2e_local, st.factor_count
+        max_ms, e2e_max, fc = local_ms, e2e_local, fc_local
         digests = sharding.digest(last)[None, :]
 
     scen_steps = W * S * args.steps  # all ranks' lanes
@@ -320,7 +329,7 @@ def run_ours(args):
         d2h = S * len(info.channels) * (hi - lo) * 8
         metric, unit, hib, val, e2e_val = (METRIC[args.workload], "scenario-steps/s", True, value, W * S / e2e_max)
         if args.workload in ("c2", "c4"):  # latency of one system: µs per EMT time step
-            metric, unit, hib = "us per time step on single case", "us/step", False
+            metric, unit, hib = METRIC[args.workload], "us/step", False
             val, e2e_val = 1e3 * max_ms / (args.steps * S), 1e6 * e2e_max / S
         out = {
             "metric": metric,

@@ -73,6 +73,11 @@ def exchange_rings(dist, mirror, lo: int, hi: int) -> None:
     receives everyone else's. One collective per launch of <= K-1 passes; the
     Bergeron travel time gives those K-1 passes of slack."""
     import torch
+    if mirror.is_cuda and dist.get_backend() == "gloo":  # host-staged (tests: several ranks, one GPU)
+        host = mirror.cpu()
+        exchange_rings(dist, host, lo, hi)
+        mirror.copy_(host)
+        return
     world = dist.get_world_size()
     W = mirror.shape[0]
     bounds = [shard_bounds(W, world, r) for r in range(world)]
