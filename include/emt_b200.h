@@ -149,6 +149,15 @@ emt_status emt_engine_sync(emt_engine* engine);
 emt_status emt_engine_load(emt_engine* engine, const double* initial, int64_t initial_len,
                            const double* const_table);
 
+/* emt_engine_load in two halves, for pipelining batches: `stage` starts the
+ * H2D of the next batch into device staging buffers on a separate stream
+ * (returns at once for pinned buffers; it may overlap a running batch), and
+ * `commit` makes the staged batch current (device-to-device, ordered after
+ * everything already issued on the engine's stream) and rewinds to pass 0. */
+emt_status emt_engine_stage(emt_engine* engine, const double* initial, int64_t initial_len,
+                            const double* const_table);
+emt_status emt_engine_commit(emt_engine* engine);
+
 /* Runs `steps` passes in launches of `chunk` passes (<= 0: auto) and, when
  * `waves` is not NULL, streams each finished chunk's rows to `waves`
  * (steps*channels*lanes doubles, WaveformSet layout of this engine's lanes)

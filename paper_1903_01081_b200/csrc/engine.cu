@@ -460,6 +460,17 @@ struct emt_engine {
     int width = 1;  // lanes of the whole batch (the caller's arena / const-table width)
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // D2H of finished waveform chunks (emt_engine_run)
+    cudaStream_t h2d_stream = nullptr;   // staged batch uploads (emt_engine_stage)
+    cudaEvent_t stage_done = nullptr, commit_done = nullptr;
+    double* d_stage_arena = nullptr;     // next batch, lane slice (extent x W)
+    double* d_stage_ctab = nullptr;      // next batch constants (consts x W)
+    double* d_stage_ring = nullptr;      // next batch ring mirror (width x cols)
+    std::vector<double> stage_ring_host;
+    bool staged = false, staged_ctab = false;
+    std::vector<double> staged_fcount;
+    int staged_base_fc = 0;
+    std::vector<int> inv_slots;          // constant slots compiled in as immediates ...
+    std::vector<double> inv_vals;        // ... and their values (emt_engine_load checks them)
     std::vector<cudaEvent_t> chunk_done;
     DevPlan plan{};
     std::vector<void*> allocations;
@@ -499,6 +510,12 @@ struct emt_engine {
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
         if (copy_stream) cudaStreamDestroy(copy_stream);
+        if (h2d_stream) cudaStreamDestroy(h2d_stream);
+        if (stage_done) cudaEventDestroy(stage_done);
+        if (commit_done) cudaEventDestroy(commit_done);
+        if (d_stage_arena) cudaFree(d_stage_arena);
+        if (d_stage_ctab) cudaFree(d_stage_ctab);
+        if (d_stage_ring) cudaFree(d_stage_ring);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -625,6 +642,15 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
             arena[static_cast<size_t>(k) * W + l] =
                 initial[static_cast<size_t>(k) * width + static_cast<size_t>(e->lane_begin + l)];
     e->host_ctab = ctab;
+    for (int k = 0; k < s.consts; ++k) {
+        const double* row = ctab.data() + static_cast<size_t>(k) * W;
+        bool inv = true;
+        for (int l = 1; l < W && inv; ++l) inv = std::memcmp(&row[l], &row[0], sizeof(double)) == 0;
+        if (inv) {
+            e->inv_slots.push_back(k);
+            e->inv_vals.push_back(row[0]);
+        }
+    }
     // Bergeron line ends read peer rings written >= K-1 passes earlier: a launch
     // may span at most K-1 passes so that every entry it reads was written by an
     // earlier launch (the kernel boundary orders the cross-CTA stores; across
@@ -1067,55 +1093,95 @@ emt_status emt_engine_stats(emt_engine* e, emt_exec_stats* stats) {
     return EMT_OK;
 }
 
-emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial_len, const double* const_table) {
+emt_status emt_engine_stage(emt_engine* e, const double* initial, int64_t initial_len, const double* const_table) {
     if (e == nullptr || initial == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
     const Schedule& s = e->sched;
     if (initial_len != static_cast<int64_t>(s.extent) * e->width)
         return set_error(EMT_DIMENSION_MISMATCH, "initial state size " + std::to_string(initial_len) +
                                                      " does not match extent " + std::to_string(s.extent) +
                                                      " x width " + std::to_string(e->width));
-    CUDA_TRY(cudaSetDevice(e->device));
-    CUDA_TRY(cudaStreamSynchronize(e->stream));
-    if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
+    if (e->staged) return set_error(EMT_NON_POSITIVE_INPUT, "a staged batch is waiting for emt_engine_commit");
     const size_t W = static_cast<size_t>(e->W), width = static_cast<size_t>(e->width), lb = static_cast<size_t>(e->lane_begin);
-    if (const_table != nullptr) {
-        // The specialised kernel compiled every lane-invariant constant in as an
-        // immediate: a new batch may only change the lane-varying ones.
-        if (e->kernel_mode == EMT_KERNEL_SPECIALISED) {
-            for (int k = 0; k < s.consts; ++k) {
-                const double* old = e->host_ctab.data() + static_cast<size_t>(k) * W;
-                bool inv = true;
-                for (size_t l = 1; l < W && inv; ++l) inv = std::memcmp(&old[l], &old[0], sizeof(double)) == 0;
-                if (!inv) continue;
-                const double* row = const_table + static_cast<size_t>(k) * width + lb;
-                for (size_t l = 0; l < W; ++l)
-                    if (std::memcmp(&row[l], &old[0], sizeof(double)) != 0)
-                        return set_error(EMT_TOPOLOGY_MISMATCH, "constant slot " + std::to_string(k) +
-                                                                    " is compiled into the specialised kernel; "
-                                                                    "create a new engine for this batch");
+    if (const_table != nullptr && e->kernel_mode != EMT_KERNEL_GENERIC) {
+        // constants compiled in as immediates must keep their values (an isomorphic batch)
+        for (size_t q = 0; q < e->inv_slots.size(); ++q) {
+            const double* row = const_table + static_cast<size_t>(e->inv_slots[q]) * width + lb;
+            for (size_t l = 0; l < W; ++l)
+                if (std::memcmp(&row[l], &e->inv_vals[q], sizeof(double)) != 0)
+                    return set_error(EMT_TOPOLOGY_MISMATCH, "constant slot " + std::to_string(e->inv_slots[q]) +
+                                                                " is compiled into the specialised kernel; "
+                                                                "create a new engine for this batch");
+        }
+    }
+    if (const_table != nullptr && e->plan.ring != nullptr) {  // line ends: same ring geometry and K bounds
+        for (const Proc& p : s.procs) {
+            if (p.code != kNortonBergeron) continue;
+            for (size_t l = 0; l < W; ++l) {
+                auto c = [&](int j) { return const_table[static_cast<size_t>(p.par + j) * width + lb + l]; };
+                const int K = static_cast<int>(c(3)), pr = static_cast<int>(c(5));
+                const long long pl = static_cast<long long>(c(4));
+                if (K < 2 || static_cast<int>(c(6)) != p.state_len || K - 1 < (e->persistent_lines ? e->min_k : e->max_chunk + 1) - 1 ||
+                    pl < 0 || pl >= e->width || pr < e->plan.ring_lo || pr + p.state_len > e->plan.ring_lo + e->plan.ring_cols)
+                    return set_error(EMT_TOPOLOGY_MISMATCH, "line end " + std::to_string(p.id) + ": the new batch changes the line geometry");
             }
         }
-        for (int k = 0; k < s.consts; ++k)
-            std::memcpy(e->host_ctab.data() + static_cast<size_t>(k) * W, const_table + static_cast<size_t>(k) * width + lb,
-                        W * sizeof(double));
-        CUDA_TRY(cudaMemcpy2DAsync(const_cast<double*>(e->plan.ctab), W * sizeof(double), const_table + lb,
-                                   width * sizeof(double), W * sizeof(double), static_cast<size_t>(s.consts),
-                                   cudaMemcpyHostToDevice, e->stream));
     }
+    CUDA_TRY(cudaSetDevice(e->device));
+    if (e->h2d_stream == nullptr) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&e->h2d_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&e->stage_done, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&e->commit_done, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(e->commit_done, e->stream));
+        CUDA_TRY(cudaMalloc(&e->d_stage_arena, static_cast<size_t>(s.extent) * W * sizeof(double)));
+        CUDA_TRY(cudaMalloc(&e->d_stage_ctab, std::max<size_t>(1, static_cast<size_t>(s.consts)) * W * sizeof(double)));
+        if (e->plan.ring != nullptr)
+            CUDA_TRY(cudaMalloc(&e->d_stage_ring, width * static_cast<size_t>(e->plan.ring_cols) * sizeof(double)));
+    }
+    // staging buffers are free once the previous commit's device copies ran
+    CUDA_TRY(cudaStreamWaitEvent(e->h2d_stream, e->commit_done, 0));
+    if (const_table != nullptr)
+        CUDA_TRY(cudaMemcpy2DAsync(e->d_stage_ctab, W * sizeof(double), const_table + lb, width * sizeof(double),
+                                   W * sizeof(double), static_cast<size_t>(s.consts), cudaMemcpyHostToDevice, e->h2d_stream));
     // arena lane slice: one strided (2D) copy, contiguous when the engine owns every lane
-    CUDA_TRY(cudaMemcpy2DAsync(e->plan.arena, W * sizeof(double), initial + lb, width * sizeof(double),
-                               W * sizeof(double), static_cast<size_t>(s.extent), cudaMemcpyHostToDevice, e->stream));
+    CUDA_TRY(cudaMemcpy2DAsync(e->d_stage_arena, W * sizeof(double), initial + lb, width * sizeof(double), W * sizeof(double),
+                               static_cast<size_t>(s.extent), cudaMemcpyHostToDevice, e->h2d_stream));
     if (e->plan.ring != nullptr) {  // mirror = the new batch's ring slots, every lane, lane-major
-        std::vector<double> mirror(width * static_cast<size_t>(e->plan.ring_cols));
+        CUDA_TRY(cudaStreamSynchronize(e->h2d_stream));  // the host staging vector is reused
+        e->stage_ring_host.assign(width * static_cast<size_t>(e->plan.ring_cols), 0.0);
         for (size_t l = 0; l < width; ++l)
             for (int c = 0; c < e->plan.ring_cols; ++c)
-                mirror[l * e->plan.ring_cols + c] = initial[static_cast<size_t>(e->plan.ring_lo + c) * width + l];
-        CUDA_TRY(cudaMemcpyAsync(e->plan.ring, mirror.data(), mirror.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                 e->stream));
-        CUDA_TRY(cudaStreamSynchronize(e->stream));  // `mirror` is a pageable temporary
+                e->stage_ring_host[l * e->plan.ring_cols + c] = initial[static_cast<size_t>(e->plan.ring_lo + c) * width + l];
+        CUDA_TRY(cudaMemcpyAsync(e->d_stage_ring, e->stage_ring_host.data(), e->stage_ring_host.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, e->h2d_stream));
     }
-    for (size_t l = 0; l < W; ++l) e->initial_fcount[l] = initial[static_cast<size_t>(s.fcount) * width + lb + l];
-    e->base_factor_count = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
+    CUDA_TRY(cudaEventRecord(e->stage_done, e->h2d_stream));
+    e->staged_fcount.resize(W);
+    for (size_t l = 0; l < W; ++l) e->staged_fcount[l] = initial[static_cast<size_t>(s.fcount) * width + lb + l];
+    e->staged_base_fc = static_cast<int>(initial[static_cast<size_t>(s.fcount) * width]);
+    e->staged_ctab = const_table != nullptr;
+    e->staged = true;
+    return EMT_OK;
+}
+
+emt_status emt_engine_commit(emt_engine* e) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (!e->staged) return set_error(EMT_NON_POSITIVE_INPUT, "no staged batch");
+    const Schedule& s = e->sched;
+    const size_t W = static_cast<size_t>(e->W);
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamWaitEvent(e->stream, e->stage_done, 0));
+    CUDA_TRY(cudaMemcpyAsync(e->plan.arena, e->d_stage_arena, static_cast<size_t>(s.extent) * W * sizeof(double),
+                             cudaMemcpyDeviceToDevice, e->stream));
+    if (e->staged_ctab)
+        CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(e->plan.ctab), e->d_stage_ctab, static_cast<size_t>(s.consts) * W * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, e->stream));
+    if (e->plan.ring != nullptr)
+        CUDA_TRY(cudaMemcpyAsync(e->plan.ring, e->d_stage_ring,
+                                 static_cast<size_t>(e->width) * e->plan.ring_cols * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 e->stream));
+    CUDA_TRY(cudaEventRecord(e->commit_done, e->stream));
+    e->initial_fcount = e->staged_fcount;
+    e->base_factor_count = e->staged_base_fc;
     CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
     CUDA_TRY(cudaMemsetAsync(e->plan.n_events, 0, sizeof(int), e->stream));
     if (e->d_progress)
@@ -1124,7 +1190,17 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     e->step = 0;
     e->rows = 0;
     e->failed = 0;
+    e->staged = false;
     return EMT_OK;
+}
+
+emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial_len, const double* const_table) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
+    EMT_TRY(emt_engine_stage(e, initial, initial_len, const_table));
+    return emt_engine_commit(e);
 }
 
 emt_status emt_engine_ring(emt_engine* e, void** device_ptr, int32_t* lanes, int32_t* cols, int32_t* max_chunk) {

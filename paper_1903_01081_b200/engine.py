@@ -110,6 +110,8 @@ def lib():
         L.emt_engine_stream.restype = vp
         L.emt_engine_read_refactor_steps.argtypes = [vp, ip, ctypes.c_int32, ip]
         L.emt_engine_load.argtypes = [vp, dp, ctypes.c_int64, dp]
+        L.emt_engine_stage.argtypes = [vp, dp, ctypes.c_int64, dp]
+        L.emt_engine_commit.argtypes = [vp]
         L.emt_engine_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
         L.emt_engine_ring.argtypes = [vp, ctypes.POINTER(vp), ip, ip, ip]
         L.emt_engine_attach_ring.argtypes = [vp, vp]
@@ -131,7 +133,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
-    "emt_engine_ring", "emt_engine_attach_ring",
+    "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
 ]
 
 
@@ -294,6 +296,18 @@ class Engine:
         init = np.ascontiguousarray(initial, dtype=np.float64)
         ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
         _check(lib().emt_engine_load(self._h, _dp(init), init.size, _dp(ct) if ct is not None else None))
+        self.rows = 0
+
+    def stage(self, initial: np.ndarray, const_table: Optional[np.ndarray] = None) -> None:
+        """Start uploading the next batch (pinned host arrays: asynchronous); see commit()."""
+        init = np.ascontiguousarray(initial, dtype=np.float64)
+        ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
+        self._staged = (init, ct)  # keep the host buffers alive until the copy ran
+        _check(lib().emt_engine_stage(self._h, _dp(init), init.size, _dp(ct) if ct is not None else None))
+
+    def commit(self) -> None:
+        """Make the staged batch current (device copy, stream-ordered) and rewind to pass 0."""
+        _check(lib().emt_engine_commit(self._h))
         self.rows = 0
 
     def run(self, steps: int, out: Optional[np.ndarray] = None, chunk: int = 0) -> Optional[np.ndarray]:

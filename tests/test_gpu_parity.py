@@ -202,3 +202,30 @@ def test_load_rejects_changed_compiled_constant():
     with pytest.raises(engine.EmtError) as ei:
         eng.load(g.initial, ct2)
     assert ei.value.code == "TopologyMismatch"
+
+
+def test_staged_batches_pipeline_equals_fresh_engines():
+    """stage(next) while the current batch runs, then commit: each batch == a fresh engine on it."""
+    import bench
+    from paper_1903_01081_b200 import schedule as sch
+    s, st, ids = bench.load_case("ieee39")
+    pick = ["sw01", "sw09", "sw22", "sw37"] * 8
+    batches = [sch.n1_batch(s, st, ids, [(b, t0 + 0.0005 * k) for k, b in enumerate(pick)]) for t0 in (0.003, 0.009, 0.015)]
+    eng = engine.Engine(batches[0].schedule, batches[0].initial, const_table=batches[0].const_table,
+                        width=batches[0].width)
+    outs = []
+    eng.stage(batches[0].initial, batches[0].const_table)
+    for k, b in enumerate(batches):
+        eng.commit()
+        if k + 1 < len(batches):
+            eng.stage(batches[k + 1].initial, batches[k + 1].const_table)
+        out = np.zeros((900, eng.channels * eng.lanes))
+        eng.run(900, out, chunk=128)
+        outs.append((out, eng.events(), eng.stats().factor_count))
+    for b, (out, ev, fc) in zip(batches, outs):
+        fresh = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width)
+        fresh.reserve(900)
+        fresh.advance(900)
+        assert bitwise_equal(out, fresh.waves().values)
+        assert np.array_equal(ev, fresh.events())
+        assert fc == fresh.stats().factor_count
