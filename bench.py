@@ -211,7 +211,7 @@ def run_ours(args):
         eng, adv = runner.eng, runner.advance
     else:
         eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width,
-                            device=dev, kernel=kern, warps=args.warps)
+                            device=dev, kernel=kern, warps=args.warps, tensor_solve=args.tensor_solve)
         adv = eng.advance
     eng.reserve(total_steps)
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
@@ -278,7 +278,7 @@ def run_ours(args):
         init_host = pin(batch.initial)
         host_waves = torch.empty((S, len(info.channels) * (hi - lo)), dtype=torch.float64, pin_memory=True).numpy()
         e2 = engine.Engine(batch.schedule, init_host, const_table=ct_host, width=batch.width, device=dev,
-                           kernel=kern, warps=args.warps)
+                           kernel=kern, warps=args.warps, tensor_solve=args.tensor_solve)
         e2.reserve(S)
         # pipelined: step k+1's H2D (stage) runs while step k computes and streams its rows out
         e2.load(init_host, ct_host)
@@ -492,6 +492,8 @@ def main():
     ap.add_argument("--kernel", choices=["auto", "specialised", "generic"], default="auto")
     ap.add_argument("--warps", type=int, default=0, help="specialised kernel: warps per 32-lane group (0 = auto)")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--tensor-solve", action="store_true",
+                    help="shared-G batches (C5): V = G^-1 I on the FP64 tensor cores (amplitude-relative parity)")
     ap.add_argument("--skip-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -56,9 +56,17 @@ typedef struct emt_config {
     int32_t lane_count;      /* lanes owned; 0 = all lanes from lane_begin */
     int32_t lanes_per_block; /* generic kernel: warps (= lanes) per CTA, 0 = auto */
     int32_t warps_per_group; /* specialised kernel: warps sharing one 32-lane group, 0 = auto (8) */
-    int32_t kernel;          /* EMT_KERNEL_AUTO / _SPECIALISED / _GENERIC */
-    int32_t reserved[2];
+    int32_t kernel;          /* EMT_KERNEL_AUTO / _SPECIALISED / _GENERIC / _TSIMT */
+    int32_t flags;           /* EMT_FLAG_* */
+    int32_t reserved;
 } emt_config;
+
+/* Shared-G batches (no switches; every conductance a lane-invariant constant):
+ * replace the sparse forward/backward sweeps by V = G^-1 I on the FP64 tensor
+ * cores (mma.sync m8n8k4, specialised kernel). Reassociates the solve: results
+ * agree to ~1e-15 of the signal amplitude, not bit-for-bit.
+ * Ignored (exact LU solve) when the batch is not shared-G. */
+enum { EMT_FLAG_TENSOR_SOLVE = 1 };
 
 /* Step-loop kernel selection. AUTO generates and JIT-compiles (NVRTC) a kernel
  * specialised to the schedule — the code generator of the reference's

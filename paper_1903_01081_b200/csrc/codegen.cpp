@@ -95,10 +95,69 @@ struct Gen {
     std::vector<int> lazy_fin;  // components whose current no task reads: finalized once per launch
 
     bool lazy_i = true;
+    bool dmma = false;  // shared-G tensor-core solve: the triangular sweeps become V = G^-1 I (DMMA)
     int ls = 32;     // doubles between consecutive slots of one lane in S[] (32 lanes per CTA; 1 in task-SIMT)
     int unit = 256;  // record offset units per slot (bytes of a 32-lane row; 1 = slot index in task-SIMT)
     Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
         lazy_i = knob("EMTB200_CG_LAZYI", 1) != 0;
+    }
+
+    /// Shared-G check for the tensor-core solve: no switches, the dirty flag is
+    /// the only watch slot, and every conductance term of G is a lane-invariant
+    /// constant — then G (and G^-1) is the same for every lane and every pass.
+    bool shared_g() const {
+        if (s.nodes <= 0 || s.dim != s.nodes || s.nodes > 64) return false;
+        for (const Proc& p : s.procs)
+            if (p.code == kNortonSwitch) return false;
+        for (int x : s.watch)
+            if (x != s.dirty) return false;
+        for (int x : s.mentry_slot) {
+            if (x < 0 || cls[static_cast<size_t>(x)] != kDerived) return false;
+            const int k = derived_const[static_cast<size_t>(x)];
+            if (k >= 0 && !invariant(k)) return false;
+        }
+        return true;
+    }
+
+    /// G^-1 (row-major, dim x dim): G assembled as FactorizeSystem does
+    /// (exec.cpp:185-192), inverted by Gauss-Jordan with partial pivoting in
+    /// long double and rounded once to double.
+    bool g_inverse(std::vector<double>& inv) const {
+        const int n = s.dim;
+        std::vector<long double> a(static_cast<size_t>(n) * 2 * n, 0.0L);
+        for (int i = 0; i < n; ++i) {
+            for (int k = s.row_ptr[static_cast<size_t>(i)]; k < s.row_ptr[static_cast<size_t>(i) + 1]; ++k) {
+                double gk = 0.0;
+                for (int q = s.mentry_ptr[static_cast<size_t>(k)]; q < s.mentry_ptr[static_cast<size_t>(k) + 1]; ++q) {
+                    const int x = s.mentry_slot[static_cast<size_t>(q)];
+                    const int c = derived_const[static_cast<size_t>(x)];
+                    gk = gk + s.mentry_sign[static_cast<size_t>(q)] * (c < 0 ? 0.0 : c0(c));
+                }
+                a[static_cast<size_t>(i) * 2 * n + static_cast<size_t>(s.col_idx[static_cast<size_t>(k)])] = gk;
+            }
+            a[static_cast<size_t>(i) * 2 * n + static_cast<size_t>(n + i)] = 1.0L;
+        }
+        for (int c = 0; c < n; ++c) {
+            int piv = c;
+            for (int r = c + 1; r < n; ++r)
+                if (fabsl(a[static_cast<size_t>(r) * 2 * n + c]) > fabsl(a[static_cast<size_t>(piv) * 2 * n + c])) piv = r;
+            if (a[static_cast<size_t>(piv) * 2 * n + c] == 0.0L) return false;
+            if (piv != c)
+                for (int j = 0; j < 2 * n; ++j) std::swap(a[static_cast<size_t>(c) * 2 * n + j], a[static_cast<size_t>(piv) * 2 * n + j]);
+            const long double d = a[static_cast<size_t>(c) * 2 * n + c];
+            for (int j = 0; j < 2 * n; ++j) a[static_cast<size_t>(c) * 2 * n + j] /= d;
+            for (int r = 0; r < n; ++r) {
+                if (r == c) continue;
+                const long double f = a[static_cast<size_t>(r) * 2 * n + c];
+                if (f == 0.0L) continue;
+                for (int j = 0; j < 2 * n; ++j) a[static_cast<size_t>(r) * 2 * n + j] -= f * a[static_cast<size_t>(c) * 2 * n + j];
+            }
+        }
+        inv.assign(static_cast<size_t>(n) * n, 0.0);
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j)
+                inv[static_cast<size_t>(i) * n + j] = static_cast<double>(a[static_cast<size_t>(i) * 2 * n + n + j]);
+        return true;
     }
 
     /// Deferred finalize (exec.cpp:220-228) of the currents no task reads.
@@ -372,7 +431,8 @@ struct Gen {
             t.cost = 8 + 4 * static_cast<int>(t.terms.size());
             add(std::move(t), region);
         }
-        if (s.nodes > 0) {
+        if (dmma) region = 2;  // finalize and everything after reads V from the DMMA block
+        if (s.nodes > 0 && !dmma) {
             for (int i = 0; i < s.dim; ++i) {  // forward, unit L (sparse.cpp:152-160)
                 const int lb = s.l_row_ptr[static_cast<size_t>(i)], le = s.l_row_ptr[static_cast<size_t>(i) + 1];
                 if (lb == le) continue;
@@ -445,6 +505,7 @@ struct Gen {
                 if (p.code == kSolveSystem) {
                     solve_layer = L;
                     emit_solve(region);
+                    if (dmma) region = 2;
                     continue;
                 }
                 emit_proc(p, region);
@@ -457,7 +518,7 @@ struct Gen {
             if (slot >= 0) t.reads.push_back(dep_slot(slot));
             t.f = {static_cast<int>(ch), off(slot)};
             t.cost = 4;
-            add(std::move(t), 1);
+            add(std::move(t), dmma ? 2 : 1);
         }
         for (size_t q = 0; q < s.latch_live.size(); ++q) {  // latch (exec.cpp:323-329)
             Task t;
@@ -466,7 +527,7 @@ struct Gen {
             t.writes = {s.latch_shadow[q]};
             t.f = {off(s.latch_live[q]), off(s.latch_shadow[q])};
             t.cost = 3;
-            add(std::move(t), 1);
+            add(std::move(t), dmma ? 2 : 1);
         }
     }
 
@@ -1090,6 +1151,14 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
     g.classify();
+    std::vector<double> ginv;
+    if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
+        g.dmma = true;
+        g.opt.lu_in_smem = false;  // the sweeps are gone; L/U stay in HBM for refactor + state
+    }
+    const int MT = (s.dim + 7) / 8, KT = (s.dim + 3) / 4;  // DMMA m8n8k4 tiles of G^-1
+    const size_t ginv_bytes = g.dmma ? static_cast<size_t>(MT) * 8 * KT * 4 * sizeof(double) : 0;
+    g.opt.smem_budget = opt.smem_budget > ginv_bytes ? opt.smem_budget - ginv_bytes : 0;
     int facts = 0;
     g.emit_all(facts);  // pass 1: slot sets
     if (facts != 1) {
@@ -1137,12 +1206,15 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             }
         }
     }
-    std::vector<int> ids_a, ids_b;
-    for (size_t i = 0; i < nt; ++i) (g.tasks[i].region == 0 ? ids_a : ids_b).push_back(static_cast<int>(i));
+    std::vector<int> ids_a, ids_b, ids_c;
+    for (size_t i = 0; i < nt; ++i)
+        (g.tasks[i].region == 0 ? ids_a : g.tasks[i].region == 1 ? ids_b : ids_c).push_back(static_cast<int>(i));
     const int G = std::max(1, std::min(opt.warps, 32));
     double span_a = 0, span_b = 0;
     const Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
     const Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
+    double span_c = 0;
+    const Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
     if (knob("EMTB200_CG_DUMP", 0)) {  // schedule dump: per phase, per warp "kind x count (cost)"
         for (const Sched* sc : {&sa, &sb}) {
             std::fprintf(stderr, "region %s\n", sc == &sa ? "A" : "B");
@@ -1169,7 +1241,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     int segs_total = 0;
     const bool straight = opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", opt.mode == 1 ? 1 : 1) != 0;
     LitCtx lctx;
-    const bool dok_mode = straight && knob("EMTB200_CG_DOK", 1) != 0;
+    const bool dok_mode = straight && (knob("EMTB200_CG_DOK", 1) != 0 || g.dmma);
     lctx.dok = dok_mode;
     lctx.cst = [&](int k) -> std::string {
         if (g.invariant(k)) return "kC[" + std::to_string(k) + "]";
@@ -1279,12 +1351,69 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     };
     const std::string code_a = region_code(sa);
     const std::string code_b = region_code(sb);
+    const std::string code_c = g.dmma ? region_code(sc3) : std::string();
     const size_t const_bytes = rki.size() * 4 + rkd.size() * 8 + static_cast<size_t>(s.consts) * 8;
     if (const_bytes > 62 * 1024) {
         fail = {13, "", "task tables (" + std::to_string(const_bytes) + " B) exceed constant memory"};
         return false;
     }
 
+
+    // ---- shared-G tensor-core solve: V = G^-1 I with DMMA (mma.sync m8n8k4 f64)
+    std::string dmma_prologue, dmma_block, dmma_tables;
+    if (g.dmma) {
+        const int MP = MT * 8, KP = KT * 4;
+        std::vector<double> gi(static_cast<size_t>(MP) * KP, 0.0);
+        for (int i = 0; i < s.dim; ++i)
+            for (int j = 0; j < s.dim; ++j) gi[static_cast<size_t>(i) * KP + j] = ginv[static_cast<size_t>(i) * s.dim + j];
+        std::vector<int> vrow(static_cast<size_t>(std::max(MP, KP)), 0);  // S row (double offset) of node k, 0 = zero slot
+        for (int k = 0; k < s.dim; ++k) vrow[static_cast<size_t>(k)] = g.hot_index[static_cast<size_t>(s.v_base + k)] * 32;
+        std::ostringstream tb;
+        tb << "__device__ const double kGinv[" << gi.size() << "] = {";
+        for (size_t q = 0; q < gi.size(); ++q) tb << (q ? "," : "") << lit(gi[q]);
+        tb << "};\n__constant__ int kVrow[" << vrow.size() << "] = {";
+        for (size_t q = 0; q < vrow.size(); ++q) tb << (q ? "," : "") << vrow[q];
+        tb << "};\n";
+        dmma_tables = tb.str();
+        const long long gi_off = static_cast<long long>(g.smem_slots()) * 32 + 32;  // after serr/needS (64 ints)
+        std::ostringstream pr;
+        pr << "  double* __restrict__ GI = sm + " << gi_off << ";\n"
+           << "  for (int q = threadIdx.x; q < " << gi.size() << "; q += " << 32 * G << ") GI[q] = kGinv[q];\n";
+        dmma_prologue = pr.str();
+        const int ntile = MT * 4;  // 4 n-tiles of 8 lanes
+        std::ostringstream blk;
+        blk << "    __syncthreads();  // every gather (I = the v slots) is in shared memory\n"
+            << "    switch (warp) {\n";
+        for (int w = 0; w < G; ++w) {
+            std::vector<int> tiles;
+            for (int t = w; t < ntile; t += G) tiles.push_back(t);
+            blk << "    case " << w << ": {\n";
+            for (size_t j = 0; j < tiles.size(); ++j) blk << "      double d" << j << "a = 0.0, d" << j << "b = 0.0;\n";
+            for (int kk = 0; kk < KT; ++kk) {
+                blk << "      { const int vr = kVrow[" << kk * 4 << " + (lane & 3)];\n";
+                for (size_t j = 0; j < tiles.size(); ++j) {
+                    const int mt = tiles[j] / 4, ntl = tiles[j] % 4;
+                    blk << "        { const double av = GI[(" << mt * 8 << " + (lane >> 2)) * " << KP << " + " << kk * 4
+                        << " + (lane & 3)]; const double bv = sm[vr + " << ntl * 8 << " + (lane >> 2)]; "
+                        << "asm volatile(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\" "
+                        << ": \"+d\"(d" << j << "a), \"+d\"(d" << j << "b) : \"d\"(av), \"d\"(bv)); }\n";
+                }
+                blk << "      }\n";
+            }
+            blk << "      BAR();  // all reads of I done before V overwrites the v slots\n";
+            for (size_t j = 0; j < tiles.size(); ++j) {
+                const int mt = tiles[j] / 4, ntl = tiles[j] % 4;
+                blk << "      { const int m = " << mt * 8 << " + (lane >> 2); if (m < " << s.dim << ") { const int o = kVrow[m] + "
+                    << ntl * 8 << " + (lane & 3) * 2; sm[o] = d" << j << "a; sm[o + 1] = d" << j << "b; "
+                    << "dok = dok & (fabs(d" << j << "a) <= a.div_limit) & (fabs(d" << j << "b) <= a.div_limit); } }\n";
+            }
+            blk << "    } break;\n";
+        }
+        blk << "    }\n"
+            << "    __syncthreads();  // V visible to finalize / control\n";
+        dmma_block = blk.str();
+        smem += ginv_bytes + 32 * sizeof(int);
+    }
     // ---- source
     std::ostringstream o;
     const int nhot = static_cast<int>(g.hot_slots.size());
@@ -1325,6 +1454,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
     }
     for (const auto& tb : sw_tables) carr_i("__constant__", tb.first.c_str(), tb.second);
+    o << dmma_tables;
     carr_i("__device__ const", "kDerSlot", dslot);
     carr_i("__device__ const", "kVC", g.vc_slots);
     carr_i("__device__ const", "kChgSlot", g.chg_flag ? g.chg_slots : std::vector<int>());
@@ -1368,6 +1498,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
       << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+      << dmma_prologue
       << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * 32] = __ldg(C + (size_t)kVC[q] * W_);\n"
       << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * 32] = A[(size_t)kHot[q] * W_];\n";
     if (lu_smem) {
@@ -1424,7 +1555,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "        FAILPUB(); return;\n"
       << "      }\n"
       << "    }\n";
-    o << code_b;
+    o << code_b << dmma_block << code_c;
     if (dok_mode) {
         // divergence (exec.cpp:229-237): rows only AND a NaN-safe predicate; the
         // failing node index (the lowest) is found in the cold path
@@ -1488,7 +1619,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     std::ostringstream sum;
     sum << (straight ? "straight " : "compact ") << "tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
         << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
-        << " est_span=" << static_cast<long>(span_a + span_b) << " est_work=" << work;
+        << " est_span=" << static_cast<long>(span_a + span_b + span_c) << " est_work=" << work
+        << (g.dmma ? " solve=dmma(G^-1 " + std::to_string(s.dim) + "x" + std::to_string(s.dim) + ")" : std::string(opt.tensor_solve ? " solve=lu(shared-G ineligible)" : ""));
     out.summary = sum.str();
     return true;
 }

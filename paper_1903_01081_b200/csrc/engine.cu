@@ -881,6 +881,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     if (c.kernel != EMT_KERNEL_GENERIC) {
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
+        opt.tensor_solve = (c.flags & EMT_FLAG_TENSOR_SOLVE) != 0;
         int dev_smem = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
         opt.smem_budget = static_cast<size_t>(dev_smem);
@@ -1276,8 +1277,12 @@ emt_status emt_codegen(const char* schedule_text, const double* const_table, int
     CodegenOptions opt;
     opt.warps = warps > 0 ? warps : 4;
     GeneratedKernel g;
-    const bool ts = warps < 0;  // negative warp count selects the task-SIMT generator
+    const bool ts = warps < 0 && warps > -100;  // negative warp count selects the task-SIMT generator
     if (ts) opt.warps = -warps;
+    if (warps <= -100) {  // -100 - w: lane-SIMT kernel with the shared-G tensor-core solve
+        opt.warps = -100 - warps > 0 ? -100 - warps : 8;
+        opt.tensor_solve = true;
+    }
     if (!(ts ? generate_tsimt(s, ct, width, opt, g, f) : generate_kernel(s, ct, width, opt, g, f)))
         return set_error(f.code, f.message);
     src_out = g.source;

@@ -49,10 +49,11 @@ class EmtError(RuntimeError):
 class _Config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("lane_begin", ctypes.c_int32), ("lane_count", ctypes.c_int32),
                 ("lanes_per_block", ctypes.c_int32), ("warps_per_group", ctypes.c_int32),
-                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT = 0, 1, 2, 3
+FLAG_TENSOR_SOLVE = 1
 
 
 class _Options(ctypes.Structure):
@@ -201,10 +202,10 @@ class WaveformSet:
 
 
 def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per_block: int = 0,
-            warps: int = 0, kernel: int = KERNEL_AUTO) -> _Config:
+            warps: int = 0, kernel: int = KERNEL_AUTO, flags: int = 0) -> _Config:
     c = _Config()
     c.device, c.lane_begin, c.lane_count, c.lanes_per_block = device, lane_begin, lane_count, lanes_per_block
-    c.warps_per_group, c.kernel = warps, kernel
+    c.warps_per_group, c.kernel, c.flags = warps, kernel, flags
     return c
 
 
@@ -256,12 +257,13 @@ class Engine:
 
     def __init__(self, schedule: str, initial: np.ndarray, const_table: Optional[np.ndarray] = None,
                  width: int = 0, device: int = 0, lane_begin: int = 0, lane_count: int = 0,
-                 lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO):
+                 lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO, tensor_solve: bool = False):
         L = lib()
         self._h = ctypes.c_void_p()
         init = np.ascontiguousarray(initial, dtype=np.float64)
         ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
-        cfg = _config(device, lane_begin, lane_count, lanes_per_block, warps, kernel)
+        cfg = _config(device, lane_begin, lane_count, lanes_per_block, warps, kernel,
+                      FLAG_TENSOR_SOLVE if tensor_solve else 0)
         _check(L.emt_engine_create(schedule.encode(), _dp(ct) if ct is not None else None, int(width), _dp(init),
                                    init.size, ctypes.byref(cfg), ctypes.byref(self._h)))
         vals = [ctypes.c_int32() for _ in range(9)]

@@ -229,3 +229,35 @@ def test_staged_batches_pipeline_equals_fresh_engines():
         assert bitwise_equal(out, fresh.waves().values)
         assert np.array_equal(ev, fresh.events())
         assert fc == fresh.stats().factor_count
+
+
+def _pv_batch(n):
+    import bench
+    return bench.build_batch(n, workload="c5")[0]
+
+
+def test_tensor_solve_shared_g_matches_oracle_to_amplitude_tolerance():
+    """Shared-G tensor-core solve (V = G^-1 I via DMMA) reassociates the triangular
+    solve: every sample within 1e-9 of its channel's amplitude (not bit-exact)."""
+    b = _pv_batch(64)
+    steps = 3000
+    want = oracle.Schedule(b.text()).interpret(b.initial, steps)
+    eng = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, tensor_solve=True)
+    assert "solve=dmma" in eng.summary, eng.summary
+    eng.reserve(steps)
+    eng.advance(steps)
+    got = eng.waves().values
+    amp = np.abs(want.waves).max(axis=0)
+    err = np.abs(got - want.waves)
+    assert np.all(err <= 1e-9 * amp + 1e-12), float((err / (amp + 1e-300)).max())
+    assert eng.stats().factor_count == want.factor_count
+
+
+def test_tensor_solve_ignored_when_g_is_not_shared():
+    g = load_golden("ieee39_n1_w8")  # breakers switch: G differs per lane and over time
+    base = engine.interpret(g.schedule, g.initial, 600)
+    eng = engine.Engine(g.schedule, g.initial, tensor_solve=True)
+    assert "ineligible" in eng.summary, eng.summary
+    eng.reserve(600)
+    eng.advance(600)
+    assert bitwise_equal(eng.waves().values, base.values)
