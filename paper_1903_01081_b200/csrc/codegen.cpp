@@ -1251,6 +1251,53 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
     std::vector<std::pair<std::string, std::vector<int>>> sw_tables;
+    // One same-kind segment as a loop over a constant-memory record table
+    // (warp-uniform records: LDCU + LDS [lane base + uniform offset]).
+    auto emit_compact = [&](const Segment& sg, const std::vector<int>& ordered) {
+        SegLayout L;
+        const Task& t0 = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first)])];
+        L.nI = static_cast<int>(t0.f.size());
+        L.nC = static_cast<int>(t0.ck.size());
+        L.TC = static_cast<int>(t0.terms.size());
+        L.cmode.assign(static_cast<size_t>(L.nC), 0);
+        for (int c = 0; c < L.nC; ++c) {
+            bool all_inv = true, all_cached = true;
+            for (int q = 0; q < sg.count; ++q) {
+                const int k = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])].ck[static_cast<size_t>(c)];
+                all_inv = all_inv && g.invariant(k);
+                all_cached = all_cached && g.vc_index[static_cast<size_t>(k)] >= 0;
+            }
+            L.cmode[static_cast<size_t>(c)] = all_inv ? 0 : (all_cached ? 2 : 1);
+        }
+        L.SI = L.nI + 2 * L.TC;
+        L.SD = 0;
+        L.cpos.assign(static_cast<size_t>(L.nC), 0);
+        for (int c = 0; c < L.nC; ++c) L.cpos[static_cast<size_t>(c)] = L.cmode[static_cast<size_t>(c)] ? L.SI++ : L.SD++;
+        const int bi0 = static_cast<int>(rki.size()), bd0 = static_cast<int>(rkd.size());
+        for (int q = 0; q < sg.count; ++q) {
+            const Task& t = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])];
+            std::vector<int> rec(static_cast<size_t>(L.SI), 0);
+            std::copy(t.f.begin(), t.f.end(), rec.begin());
+            for (int j = 0; j < L.TC; ++j) {
+                rec[static_cast<size_t>(L.nI + 2 * j)] = t.terms[static_cast<size_t>(j)].first;
+                rec[static_cast<size_t>(L.nI + 2 * j + 1)] = t.terms[static_cast<size_t>(j)].second;
+            }
+            for (int c = 0; c < L.nC; ++c) {
+                const int k = t.ck[static_cast<size_t>(c)];
+                const int m = L.cmode[static_cast<size_t>(c)];
+                if (m == 0) rkd.push_back(g.c0(k));
+                else rec[static_cast<size_t>(L.cpos[static_cast<size_t>(c)])] = m == 2 ? g.vc_index[static_cast<size_t>(k)] * 256 : k;
+            }
+            rki.insert(rki.end(), rec.begin(), rec.end());
+        }
+        ++segs_total;
+        return segment_code(sg.kind, sg.count, sg.indep != 0, bi0, bd0, L, "      ");
+    };
+    // hybrid: in the straight-line form, long independent same-kind runs become loops
+    const int loop_min = knob("EMTB200_CG_LOOPMIN", 0);
+    auto loopable = [](int kind) {
+        return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
+    };
     auto region_code = [&](const Sched& sc) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -1265,8 +1312,17 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
                     if (p > 0) rc << "      BAR();\n";
                     std::vector<int> ordered;
-                    segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
-                    for (int id : ordered) {
+                    const auto segs = segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
+                    std::vector<int> seg_of(ordered.size(), -1);
+                    for (size_t si = 0; si < segs.size(); ++si)
+                        for (int q = 0; q < segs[si].count; ++q) seg_of[static_cast<size_t>(segs[si].first + q)] = static_cast<int>(si);
+                    for (size_t oi = 0; oi < ordered.size(); ++oi) {
+                        const Segment& sg = segs[static_cast<size_t>(seg_of[oi])];
+                        if (loop_min > 0 && sg.count >= loop_min && sg.indep && loopable(sg.kind)) {
+                            if (static_cast<int>(oi) == sg.first) rc << emit_compact(sg, ordered);  // tasks in order
+                            continue;
+                        }
+                        const int id = ordered[oi];
                         const Task& t = g.tasks[static_cast<size_t>(id)];
                         LitCtx c = lctx;
                         if (t.kind == K_SW && switch_bits && sw_ids.size() < 64) {
@@ -1304,46 +1360,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                     rc << "    }\n";
                     continue;
                 }
-                for (const Segment& sg : segs) {
-                    SegLayout L;
-                    const Task& t0 = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first)])];
-                    L.nI = static_cast<int>(t0.f.size());
-                    L.nC = static_cast<int>(t0.ck.size());
-                    L.TC = static_cast<int>(t0.terms.size());
-                    L.cmode.assign(static_cast<size_t>(L.nC), 0);
-                    for (int c = 0; c < L.nC; ++c) {
-                        bool all_inv = true, all_cached = true;
-                        for (int q = 0; q < sg.count; ++q) {
-                            const int k = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])].ck[static_cast<size_t>(c)];
-                            all_inv = all_inv && g.invariant(k);
-                            all_cached = all_cached && g.vc_index[static_cast<size_t>(k)] >= 0;
-                        }
-                        L.cmode[static_cast<size_t>(c)] = all_inv ? 0 : (all_cached ? 2 : 1);
-                    }
-                    L.SI = L.nI + 2 * L.TC;
-                    L.SD = 0;
-                    L.cpos.assign(static_cast<size_t>(L.nC), 0);
-                    for (int c = 0; c < L.nC; ++c) L.cpos[static_cast<size_t>(c)] = L.cmode[static_cast<size_t>(c)] ? L.SI++ : L.SD++;
-                    const int bi0 = static_cast<int>(rki.size()), bd0 = static_cast<int>(rkd.size());
-                    for (int q = 0; q < sg.count; ++q) {
-                        const Task& t = g.tasks[static_cast<size_t>(ordered[static_cast<size_t>(sg.first + q)])];
-                        std::vector<int> rec(static_cast<size_t>(L.SI), 0);
-                        std::copy(t.f.begin(), t.f.end(), rec.begin());
-                        for (int j = 0; j < L.TC; ++j) {
-                            rec[static_cast<size_t>(L.nI + 2 * j)] = t.terms[static_cast<size_t>(j)].first;
-                            rec[static_cast<size_t>(L.nI + 2 * j + 1)] = t.terms[static_cast<size_t>(j)].second;
-                        }
-                        for (int c = 0; c < L.nC; ++c) {
-                            const int k = t.ck[static_cast<size_t>(c)];
-                            const int m = L.cmode[static_cast<size_t>(c)];
-                            if (m == 0) rkd.push_back(g.c0(k));
-                            else rec[static_cast<size_t>(L.cpos[static_cast<size_t>(c)])] = m == 2 ? g.vc_index[static_cast<size_t>(k)] * 256 : k;
-                        }
-                        rki.insert(rki.end(), rec.begin(), rec.end());
-                    }
-                    rc << segment_code(sg.kind, sg.count, sg.indep != 0, bi0, bd0, L, "      ");
-                    ++segs_total;
-                }
+                for (const Segment& sg : segs) rc << emit_compact(sg, ordered);
                 rc << "    }\n";
             }
         }
