@@ -188,6 +188,12 @@ emt_status emt_engine_ring(emt_engine* engine, void** device_ptr, int32_t* lanes
  * contents there and uses it from then on. The buffer must outlive the engine. */
 emt_status emt_engine_attach_ring(emt_engine* engine, void* device_ptr);
 
+/* Phase profiler of the specialised kernel (engine created with the
+ * environment variable EMTB200_CG_PROF=1): cycles summed over the passes run
+ * so far, CTA 0, per warp (32) x marker (64), marker 2p = phase p's compute,
+ * 2p+1 = the barrier wait after it, numbered region by region. */
+emt_status emt_engine_profile(emt_engine* engine, int64_t* cycles, int32_t n);
+
 /* Host copies of recorded rows [row0, row0+rows) (WaveformSet layout, this
  * engine's lanes only) and their times. */
 emt_status emt_engine_read_waves(emt_engine* engine, int32_t row0, int32_t rows, double* waves,

@@ -17,6 +17,8 @@
 #include "codegen.hpp"
 
 #include <algorithm>
+#include <climits>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -51,11 +53,13 @@ std::string lit(double v) {
 // Task kinds of the compact kernel; record strides in ints.
 enum Kind {
     K_IND, K_CAP, K_SRL, K_VSRC, K_ISRC, K_CSRC, K_SW, K_GATHER, K_FWD, K_BWD, K_FINC, K_FINS,
-    K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_BERG, K_NKINDS
+    K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_BERG,
+    K_VSRCP, K_ISRCP, K_SRCPRE, K_NKINDS
 };
 const char* const kKindName[K_NKINDS] = {"IND", "CAP", "SRL", "VSRC", "ISRC", "CSRC", "SW", "GATHER",
                                          "FWD", "BWD", "FINC", "FINS", "GAIN", "SUM", "INTEG", "LAG",
-                                         "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH", "BERG"};
+                                         "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH", "BERG",
+                                         "VSRCP", "ISRCP", "SRCPRE"};
 // kinds whose tasks never depend on another task of the same kind: eligible
 // for the unrolled (loads-first) loop when a segment has no internal edges
 bool unrollable(int k) { return k != K_SW; }
@@ -96,6 +100,13 @@ struct Gen {
 
     bool lazy_i = true;
     bool dmma = false;  // shared-G tensor-core solve: the triangular sweeps become V = G^-1 I (DMMA)
+    // AC sources (lane-invariant omega != 0): m cos(w t + p) for pass n+1 is computed
+    // during pass n's solve, off the Norton phase's critical path; virtual slots
+    // extent + j hold the values (shared memory only, never in the arena)
+    bool presrc = false;
+    std::map<int, int> pre_of;   // source process id -> j
+    std::vector<std::array<int, 3>> pre_ck;  // j -> const slots (m, w, p)
+    int pre_base = 0;
     int ls = 32;     // doubles between consecutive slots of one lane in S[] (32 lanes per CTA; 1 in task-SIMT)
     int unit = 256;  // record offset units per slot (bytes of a 32-lane row; 1 = slot index in task-SIMT)
     Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
@@ -185,6 +196,7 @@ struct Gen {
     /// shared-memory byte offset of an arena slot relative to the lane base
     int off(int slot) const {
         if (slot < 0) return 0;  // ground sentinel reads the zero slot
+        if (slot >= s.extent) return (pre_base + slot - s.extent) * unit;  // precomputed source value
         if (cls[static_cast<size_t>(slot)] == kDerived && derived_const[static_cast<size_t>(slot)] < 0) return 0;
         if (hot_index[static_cast<size_t>(slot)] < 0) return 0;  // pass 1 (offsets not assigned yet)
         return hot_index[static_cast<size_t>(slot)] * unit;
@@ -221,6 +233,16 @@ struct Gen {
 
     void classify() {
         const size_t n = static_cast<size_t>(s.extent);
+        pre_of.clear();
+        pre_ck.clear();
+        if (presrc)
+            for (const Proc& p : s.procs) {
+                const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
+                if (wk < 0 || !invariant(wk) || c0(wk) == 0.0) continue;
+                const int mk = wk - 1;
+                pre_of[p.id] = static_cast<int>(pre_ck.size());
+                pre_ck.push_back({mk, wk, wk + 1});
+            }
         iread.clear();
         for (const Proc& p : s.procs) {
             // ports a kernel actually reads (exec.cpp:85-309): Norton records carry
@@ -310,6 +332,16 @@ struct Gen {
                 t.cost = 10;
                 break;
             case kNortonVoltageSource:
+                if (pre_of.count(p.id)) {
+                    const int vs = s.extent + pre_of.at(p.id);
+                    t.kind = K_VSRCP;
+                    t.reads = {vs};
+                    t.writes = {p.out2};
+                    t.f = {off(p.out2), off(vs)};
+                    t.ck = {p.par};
+                    t.cost = 8;
+                    break;
+                }
                 t.kind = K_VSRC;
                 t.writes = {p.out2};
                 t.f = {off(p.out2)};
@@ -317,6 +349,15 @@ struct Gen {
                 t.cost = invariant(p.par + 2) && c0(p.par + 2) == 0.0 ? 6 : 90;
                 break;
             case kNortonCurrentSource:
+                if (pre_of.count(p.id)) {
+                    const int vs = s.extent + pre_of.at(p.id);
+                    t.kind = K_ISRCP;
+                    t.reads = {vs};
+                    t.writes = {p.out2};
+                    t.f = {off(p.out2), off(vs)};
+                    t.cost = 6;
+                    break;
+                }
                 t.kind = K_ISRC;
                 t.writes = {p.out2};
                 t.f = {off(p.out2)};
@@ -511,6 +552,16 @@ struct Gen {
                 emit_proc(p, region);
             }
         }
+        for (size_t j = 0; j < pre_ck.size(); ++j) {  // next pass's source values
+            Task t;
+            t.kind = K_SRCPRE;
+            const int vs = s.extent + static_cast<int>(j);
+            t.writes = {vs};
+            t.f = {off(vs)};
+            t.ck = {pre_ck[j][0], pre_ck[j][1], pre_ck[j][2]};
+            t.cost = 90;
+            add(std::move(t), dmma ? 2 : 1);
+        }
         for (size_t ch = 0; ch < s.channel_slot.size(); ++ch) {  // record (exec.cpp:313-321)
             Task t;
             t.kind = K_REC;
@@ -551,9 +602,9 @@ struct Gen {
         std::set<int> need;
         for (const Task& t : tasks) {
             for (int x : t.reads)
-                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+                if (x >= 0 && x < s.extent && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
             for (int x : t.writes)
-                if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
+                if (x >= 0 && x < s.extent && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
         }
         for (int x : s.watch)
             if (x >= 0 && cls[static_cast<size_t>(x)] == kNone) need.insert(x);
@@ -567,7 +618,8 @@ struct Gen {
         }
         const size_t per_slot = static_cast<size_t>(ls) * sizeof(double);
         const size_t fixed = 2 * static_cast<size_t>(ls) * sizeof(int);  // serr + refactor flags
-        size_t used = hot_slots.size() * per_slot + fixed;
+        pre_base = static_cast<int>(hot_slots.size());
+        size_t used = (hot_slots.size() + pre_ck.size()) * per_slot + fixed;
         if (used > opt.smem_budget) return false;
         std::set<int> vc;
         for (const Task& t : tasks)
@@ -575,7 +627,7 @@ struct Gen {
                 if (!invariant(k)) vc.insert(k);
         vc_index.assign(static_cast<size_t>(s.consts), -1);
         vc_slots.clear();
-        vc_base = static_cast<int>(hot_slots.size());
+        vc_base = static_cast<int>(hot_slots.size() + pre_ck.size());
         if (used + vc.size() * per_slot <= opt.smem_budget) {
             for (int k : vc) {
                 vc_index[static_cast<size_t>(k)] = vc_base + static_cast<int>(vc_slots.size());
@@ -907,6 +959,11 @@ const KindCode kCode[K_NKINDS] = {
              "const double h@ = -(c1@ * b1@ + c0@ * b0@);",
              "ST({I2}, h@); if (live) { const int w@ = step % {I4}; A[(size_t)({I3} + w@) * W_] = be@; "
              "a.ring[(LB_ + gl) * a.ring_cols + ({I3} - a.ring_lo) + w@] = be@; }"},
+    // sources whose m*cos(w t + p) was computed during the previous pass (K_SRCPRE)
+    /*VSRCP*/ {"const double g@ = {C0}; const double v@ = LD({I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
+    /*ISRCP*/ {"const double v@ = LD({I1});", "", "ST({I0}, v@);"},
+    /*SRCPRE*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
+               "const double v@ = m@ * cos(w@ * tn + p@);", "ST({I0}, v@);"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1150,6 +1207,7 @@ std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
+    g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;  // measured 3% slower: moves cos, does not remove it
     g.classify();
     std::vector<double> ginv;
     if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
@@ -1206,18 +1264,48 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             }
         }
     }
-    std::vector<int> ids_a, ids_b, ids_c;
-    for (size_t i = 0; i < nt; ++i)
+    std::vector<int> ids_a, ids_b, ids_c, fillers;
+    for (size_t i = 0; i < nt; ++i) {
+        if (g.tasks[i].kind == K_SRCPRE) {  // dependency-free: placed into idle warp time afterwards
+            fillers.push_back(static_cast<int>(i));
+            continue;
+        }
         (g.tasks[i].region == 0 ? ids_a : g.tasks[i].region == 1 ? ids_b : ids_c).push_back(static_cast<int>(i));
+    }
     const int G = std::max(1, std::min(opt.warps, 32));
     double span_a = 0, span_b = 0;
     const Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
-    const Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
+    Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
     double span_c = 0;
-    const Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
+    Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
+    {
+        // filler tasks go where a warp idles longest before a barrier of the last region
+        Sched& host = g.dmma ? sc3 : sb;
+        if (host.phases.empty()) host.phases.assign(1, std::vector<std::vector<int>>(static_cast<size_t>(G)));
+        std::vector<std::vector<long>> load(host.phases.size(), std::vector<long>(static_cast<size_t>(G), 0));
+        std::vector<long> pmax(host.phases.size(), 0);
+        for (size_t p = 0; p < host.phases.size(); ++p)
+            for (int w = 0; w < G; ++w) {
+                for (int id : host.phases[p][static_cast<size_t>(w)]) load[p][static_cast<size_t>(w)] += g.tasks[static_cast<size_t>(id)].cost;
+                pmax[p] = std::max(pmax[p], load[p][static_cast<size_t>(w)]);
+            }
+        for (int id : fillers) {
+            size_t bp = 0;
+            int bw = 0;
+            long best = LONG_MIN;
+            for (size_t p = 0; p < host.phases.size(); ++p)
+                for (int w = 0; w < G; ++w) {
+                    const long slack = pmax[p] - load[p][static_cast<size_t>(w)];
+                    if (slack > best) { best = slack; bp = p; bw = w; }
+                }
+            host.phases[bp][static_cast<size_t>(bw)].push_back(id);
+            load[bp][static_cast<size_t>(bw)] += g.tasks[static_cast<size_t>(id)].cost;
+            pmax[bp] = std::max(pmax[bp], load[bp][static_cast<size_t>(bw)]);
+        }
+    }
     if (knob("EMTB200_CG_DUMP", 0)) {  // schedule dump: per phase, per warp "kind x count (cost)"
-        for (const Sched* sc : {&sa, &sb}) {
-            std::fprintf(stderr, "region %s\n", sc == &sa ? "A" : "B");
+        for (const Sched* sc : std::initializer_list<const Sched*>{&sa, &sb, &sc3}) {
+            std::fprintf(stderr, "region %s\n", sc == &sa ? "A" : sc == &sb ? "B" : "C");
             for (size_t p = 0; p < sc->phases.size(); ++p) {
                 std::fprintf(stderr, " phase %zu:", p);
                 for (int w = 0; w < G; ++w) {
@@ -1295,6 +1383,14 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     };
     // hybrid: in the straight-line form, long independent same-kind runs become loops
     const int loop_min = knob("EMTB200_CG_LOOPMIN", 0);
+    // phase profiler (EMTB200_CG_PROF=1): CTA 0, lane 0 of each warp adds the cycles
+    // since its previous marker to a.prof[warp * 64 + marker] (compute, then barrier wait)
+    const bool prof = knob("EMTB200_CG_PROF", 0) != 0;
+    int prof_base = 0;  // first marker id of the region being emitted
+    auto mark = [&](int id) {
+        if (!prof) return std::string();
+        return "      PROF(" + std::to_string(id) + ");\n";
+    };
     auto loopable = [](int kind) {
         return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
     };
@@ -1310,7 +1406,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 rc << "    case " << w << ": {\n";
                 std::vector<int> sw_ids;  // process id per swbits bit
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
-                    if (p > 0) rc << "      BAR();\n";
+                    if (p > 0) rc << mark(prof_base + 2 * static_cast<int>(p) - 2) << "      BAR();\n"
+                                  << mark(prof_base + 2 * static_cast<int>(p) - 1);
                     std::vector<int> ordered;
                     const auto segs = segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
                     std::vector<int> seg_of(ordered.size(), -1);
@@ -1341,9 +1438,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                           "b &= b - 1; const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
                           "a.events[3*e+1] = gl; a.events[3*e+2] = " << tab << "[j]; } } } }\n";
                 }
-                rc << "    } break;\n";
+                rc << mark(prof_base + 2 * static_cast<int>(sc.phases.size()) - 2) << "    } break;\n";
             }
             rc << "    }\n";
+            prof_base += 2 * static_cast<int>(sc.phases.size());
             return rc.str();
         }
         for (size_t p = 0; p < sc.phases.size(); ++p) {
@@ -1376,6 +1474,16 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
 
 
+    std::string pre_prologue;
+    if (!g.pre_ck.empty()) {  // the launch's first pass: source values computed here
+        std::ostringstream pp;
+        pp << "  if (warp == 0) { const double tn = (double)(a.step0 + 1) * " << lit(s.dt) << ";\n";
+        for (size_t j = 0; j < g.pre_ck.size(); ++j)
+            pp << "    S[" << (g.pre_base + static_cast<int>(j)) * 32 << "] = " << g.C(g.pre_ck[j][0]) << " * cos(" << g.C(g.pre_ck[j][1])
+               << " * tn + " << g.C(g.pre_ck[j][2]) << ");\n";
+        pp << "  }\n";
+        pre_prologue = pp.str();
+    }
     // ---- shared-G tensor-core solve: V = G^-1 I with DMMA (mma.sync m8n8k4 f64)
     std::string dmma_prologue, dmma_block, dmma_tables;
     if (g.dmma) {
@@ -1440,7 +1548,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -1480,6 +1588,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     carr_i("__device__ const", "kConHot", chot);
     carr_i("__device__ const", "kConSign", csign);
     o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
+    if (knob("EMTB200_CG_FAKECOS", 0)) o << "#define cos(x) (x)\n";  // timing experiment only: wrong numerics
+    o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
+         "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
     o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + blockIdx.x, 0x3fffffffu); } while (0)\n";
     o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
@@ -1515,6 +1626,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
       << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+      << pre_prologue
       << dmma_prologue
       << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * 32] = __ldg(C + (size_t)kVC[q] * W_);\n"
       << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * 32] = A[(size_t)kHot[q] * W_];\n";
@@ -1533,9 +1645,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  if (threadIdx.x == 0) s_cmin = -0x3fffffff;\n"
       << "  __syncthreads();\n"
       << "  int it = 0;\n"
+      << "  long long prof_t = clock64(); (void)prof_t;\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
+      << "    const double tn = (double)(step + 2) * " << lit(s.dt) << "; (void)tn;\n"
       << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
       << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
       << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
@@ -1892,7 +2006,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; };\n";
     auto garr = [&](const char* name, const std::vector<int>& v) {
         o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];

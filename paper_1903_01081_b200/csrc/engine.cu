@@ -57,6 +57,7 @@ struct CgArgs {
     long long ring_lo, ring_cols;
     unsigned int* progress;  // persistent line-coupled run: passes completed per CTA (else null)
     int min_k, nblocks;
+    long long* prof;         // phase profiler accumulators (EMTB200_CG_PROF=1), else null
 };
 
 struct DevPlan {
@@ -487,6 +488,7 @@ struct emt_engine {
     double* d_ring = nullptr;   // line-end history mirror (owned unless attached)
     bool ring_owned = true;
     unsigned int* d_progress = nullptr;  // persistent line-coupled mode: per-CTA pass counters
+    long long* d_prof = nullptr;         // 32 warps x 64 markers of cycle sums (profiling builds)
     bool persistent_lines = false;
     int min_k = 0;
     int failed = 0;
@@ -506,6 +508,7 @@ struct emt_engine {
         for (void* p : allocations) cudaFree(p);
         if (d_ring && ring_owned) cudaFree(d_ring);
         if (d_progress) cudaFree(d_progress);
+        if (d_prof) cudaFree(d_prof);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
@@ -901,6 +904,11 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         }
         if (ok) {
             e->kernel_mode = EMT_KERNEL_SPECIALISED;
+            const char* pf = std::getenv("EMTB200_CG_PROF");
+            if (pf && std::strcmp(pf, "0") != 0) {
+                CUDA_TRY(cudaMalloc(&e->d_prof, 32 * 64 * sizeof(long long)));
+                CUDA_TRY(cudaMemset(e->d_prof, 0, 32 * 64 * sizeof(long long)));
+            }
             // Line-coupled lanes in one engine: one persistent launch with per-CTA
             // progress words instead of relaunching every K-1 passes (all CTAs must
             // be co-resident: one 32-lane CTA per SM at most).
@@ -989,7 +997,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
-                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32)};
+                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32), e->d_prof};
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
         const unsigned grid = static_cast<unsigned>(ts ? e->W : (e->W + 31) / 32);
@@ -1202,6 +1210,15 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
     EMT_TRY(emt_engine_stage(e, initial, initial_len, const_table));
     return emt_engine_commit(e);
+}
+
+emt_status emt_engine_profile(emt_engine* e, int64_t* cycles, int32_t n) {
+    if (e == nullptr || cycles == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    if (e->d_prof == nullptr) return set_error(EMT_NON_POSITIVE_INPUT, "engine built without EMTB200_CG_PROF=1");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    CUDA_TRY(cudaMemcpy(cycles, e->d_prof, sizeof(long long) * static_cast<size_t>(std::min(n, 32 * 64)), cudaMemcpyDeviceToHost));
+    return EMT_OK;
 }
 
 emt_status emt_engine_ring(emt_engine* e, void** device_ptr, int32_t* lanes, int32_t* cols, int32_t* max_chunk) {

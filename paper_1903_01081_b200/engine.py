@@ -114,6 +114,7 @@ def lib():
         L.emt_engine_stage.argtypes = [vp, dp, ctypes.c_int64, dp]
         L.emt_engine_commit.argtypes = [vp]
         L.emt_engine_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
+        L.emt_engine_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
         L.emt_engine_ring.argtypes = [vp, ctypes.POINTER(vp), ip, ip, ip]
         L.emt_engine_attach_ring.argtypes = [vp, vp]
         L.emt_engine_kernel.argtypes = [vp]
@@ -135,6 +136,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
+    "emt_engine_profile",
 ]
 
 
@@ -320,6 +322,12 @@ class Engine:
         _check(lib().emt_engine_run(self._h, int(steps), int(chunk), _dp(out) if out is not None else None))
         self.rows += steps
         return out
+
+    def profile(self) -> np.ndarray:
+        """(32 warps x 64 markers) cycle sums of the phase profiler (EMTB200_CG_PROF=1 builds)."""
+        buf = np.zeros(32 * 64, dtype=np.int64)
+        _check(lib().emt_engine_profile(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), buf.size))
+        return buf.reshape(32, 64)
 
     def ring(self):
         """(device pointer, lanes, cols, max passes per launch) of the line-end history mirror."""
