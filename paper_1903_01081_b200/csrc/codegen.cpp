@@ -54,12 +54,12 @@ std::string lit(double v) {
 enum Kind {
     K_IND, K_CAP, K_SRL, K_VSRC, K_ISRC, K_CSRC, K_SW, K_GATHER, K_FWD, K_BWD, K_FINC, K_FINS,
     K_GAIN, K_SUM, K_INTEG, K_LAG, K_PI, K_LIM, K_CMP, K_CONST, K_DELAY, K_REC, K_LATCH, K_BERG,
-    K_VSRCP, K_ISRCP, K_SRCPRE, K_NKINDS
+    K_VSRCP, K_ISRCP, K_SRCPRE, K_VSRCT, K_ISRCT, K_NKINDS
 };
 const char* const kKindName[K_NKINDS] = {"IND", "CAP", "SRL", "VSRC", "ISRC", "CSRC", "SW", "GATHER",
                                          "FWD", "BWD", "FINC", "FINS", "GAIN", "SUM", "INTEG", "LAG",
                                          "PI", "LIM", "CMP", "CONST", "DELAY", "REC", "LATCH", "BERG",
-                                         "VSRCP", "ISRCP", "SRCPRE"};
+                                         "VSRCP", "ISRCP", "SRCPRE", "VSRCT", "ISRCT"};
 // kinds whose tasks never depend on another task of the same kind: eligible
 // for the unrolled (loads-first) loop when a segment has no internal edges
 bool unrollable(int k) { return k != K_SW; }
@@ -107,6 +107,10 @@ struct Gen {
     std::map<int, int> pre_of;   // source process id -> j
     std::vector<std::array<int, 3>> pre_ck;  // j -> const slots (m, w, p)
     int pre_base = 0;
+    // lane-invariant AC sources tabulated per launch (emt_src_kernel): process id -> table column
+    bool srctab = false;
+    std::map<int, int> tab_of;
+    std::vector<std::array<int, 3>> tab_ck;  // column -> const slots (m, w, p)
     int ls = 32;     // doubles between consecutive slots of one lane in S[] (32 lanes per CTA; 1 in task-SIMT)
     int unit = 256;  // record offset units per slot (bytes of a 32-lane row; 1 = slot index in task-SIMT)
     Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
@@ -235,6 +239,15 @@ struct Gen {
         const size_t n = static_cast<size_t>(s.extent);
         pre_of.clear();
         pre_ck.clear();
+        tab_of.clear();
+        tab_ck.clear();
+        if (srctab)
+            for (const Proc& p : s.procs) {
+                const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
+                if (wk < 0 || !invariant(wk) || c0(wk) == 0.0 || !invariant(wk - 1) || !invariant(wk + 1)) continue;
+                tab_of[p.id] = static_cast<int>(tab_ck.size());
+                tab_ck.push_back({wk - 1, wk, wk + 1});
+            }
         if (presrc)
             for (const Proc& p : s.procs) {
                 const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
@@ -332,6 +345,14 @@ struct Gen {
                 t.cost = 10;
                 break;
             case kNortonVoltageSource:
+                if (tab_of.count(p.id)) {
+                    t.kind = K_VSRCT;
+                    t.writes = {p.out2};
+                    t.f = {off(p.out2), tab_of.at(p.id)};
+                    t.ck = {p.par};
+                    t.cost = 30;
+                    break;
+                }
                 if (pre_of.count(p.id)) {
                     const int vs = s.extent + pre_of.at(p.id);
                     t.kind = K_VSRCP;
@@ -349,6 +370,13 @@ struct Gen {
                 t.cost = invariant(p.par + 2) && c0(p.par + 2) == 0.0 ? 6 : 90;
                 break;
             case kNortonCurrentSource:
+                if (tab_of.count(p.id)) {
+                    t.kind = K_ISRCT;
+                    t.writes = {p.out2};
+                    t.f = {off(p.out2), tab_of.at(p.id)};
+                    t.cost = 30;
+                    break;
+                }
                 if (pre_of.count(p.id)) {
                     const int vs = s.extent + pre_of.at(p.id);
                     t.kind = K_ISRCP;
@@ -964,6 +992,9 @@ const KindCode kCode[K_NKINDS] = {
     /*ISRCP*/ {"const double v@ = LD({I1});", "", "ST({I0}, v@);"},
     /*SRCPRE*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
                "const double v@ = m@ * cos(w@ * tn + p@);", "ST({I0}, v@);"},
+    // sources read from the launch's value table (emt_src_kernel computes m*cos(w t + p))
+    /*VSRCT*/ {"const double g@ = {C0}; const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + {I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
+    /*ISRCT*/ {"const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + {I1});", "", "ST({I0}, v@);"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1207,7 +1238,8 @@ std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
-    g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;  // measured 3% slower: moves cos, does not remove it
+    g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
+    g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;  // measured 3% slower: moves cos, does not remove it
     g.classify();
     std::vector<double> ginv;
     if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
@@ -1545,10 +1577,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const long long Wl = lanes;
     o << "// generated by emtb200 codegen: " << s.nodes << " nodes, " << s.comps << " components, " << s.layers
       << " layers, " << lanes << " lanes, " << G << " warps, " << nt << " tasks, " << segs_total << " segments\n";
+    o << "#define NSRC_ " << std::max<size_t>(1, g.tab_ck.size()) << "\n";
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -1737,6 +1770,22 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  }\n"
       << "}\n";
 
+    if (!g.tab_ck.empty()) {
+        // per-launch table of the lane-invariant AC source values: the same expression,
+        // operands and time base as the inline form (bit-identical), computed once for
+        // all lanes instead of by every lane group's instruction stream
+        o << "extern \"C\" __global__ void emt_src_kernel(double* tab, int step0, int nsteps) {\n"
+          << "  const int i = blockIdx.x * blockDim.x + threadIdx.x;\n"
+          << "  if (i >= nsteps * NSRC_) return;\n"
+          << "  const int it = i / NSRC_, j = i - it * NSRC_;\n"
+          << "  const double t = (double)(step0 + it + 1) * " << lit(s.dt) << ";\n"
+          << "  double v = 0.0;\n  switch (j) {\n";
+        for (size_t j = 0; j < g.tab_ck.size(); ++j)
+            o << "    case " << j << ": v = " << lit(g.c0(g.tab_ck[j][0])) << " * cos(" << lit(g.c0(g.tab_ck[j][1])) << " * t + "
+              << lit(g.c0(g.tab_ck[j][2])) << "); break;\n";
+        o << "  }\n  tab[i] = v;\n}\n";
+    }
+    out.nsrc = static_cast<int>(g.tab_ck.size());
     out.source = o.str();
     out.warps = G;
     out.smem_bytes = smem;
@@ -2006,7 +2055,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab; };\n";
     auto garr = [&](const char* name, const std::vector<int>& v) {
         o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];

@@ -34,6 +34,7 @@ struct GeneratedKernel {
     int lu_smem = 0;        // 1 when L/U live in shared memory
     int phases_a = 0, phases_b = 0;
     int tasks = 0;
+    int nsrc = 0;           // AC source values tabulated per launch by emt_src_kernel (srctab)
     std::string summary;
 };
 

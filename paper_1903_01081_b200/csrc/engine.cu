@@ -58,6 +58,7 @@ struct CgArgs {
     unsigned int* progress;  // persistent line-coupled run: passes completed per CTA (else null)
     int min_k, nblocks;
     long long* prof;         // phase profiler accumulators (EMTB200_CG_PROF=1), else null
+    const double* srctab;    // this launch's AC source values [pass][source] (emt_src_kernel)
 };
 
 struct DevPlan {
@@ -489,6 +490,8 @@ struct emt_engine {
     bool ring_owned = true;
     unsigned int* d_progress = nullptr;  // persistent line-coupled mode: per-CTA pass counters
     long long* d_prof = nullptr;         // 32 warps x 64 markers of cycle sums (profiling builds)
+    double* d_srctab = nullptr;          // per-launch AC source table (gen.nsrc columns)
+    size_t srctab_cap = 0;               // doubles
     bool persistent_lines = false;
     int min_k = 0;
     int failed = 0;
@@ -509,6 +512,7 @@ struct emt_engine {
         if (d_ring && ring_owned) cudaFree(d_ring);
         if (d_progress) cudaFree(d_progress);
         if (d_prof) cudaFree(d_prof);
+        if (d_srctab) cudaFree(d_srctab);
         if (d_waves) cudaFree(d_waves);
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
@@ -997,7 +1001,24 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
-                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32), e->d_prof};
+                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32), e->d_prof,
+                 e->d_srctab};
+        if (e->gen.nsrc > 0 && e->jit.function2 != nullptr) {  // the launch's source value table first
+            const size_t need = static_cast<size_t>(steps) * e->gen.nsrc;
+            if (need > e->srctab_cap) {
+                if (e->d_srctab) cudaFree(e->d_srctab);
+                e->d_srctab = nullptr;
+                CUDA_TRY(cudaMalloc(&e->d_srctab, need * sizeof(double)));
+                e->srctab_cap = need;
+            }
+            a.srctab = e->d_srctab;
+            double* tab = e->d_srctab;
+            int s0 = e->step, ns = steps;
+            void* tp[] = {&tab, &s0, &ns};
+            const CUresult r2 = driver()->LaunchKernel(e->jit.function2, static_cast<unsigned>((need + 255) / 256), 1, 1, 256, 1, 1, 0,
+                                                       reinterpret_cast<CUstream>(e->stream), tp, nullptr);
+            if (r2 != CUDA_SUCCESS) return set_error(EMT_CUDA_ERROR, "cuLaunchKernel(emt_src_kernel) failed");
+        }
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
         const unsigned grid = static_cast<unsigned>(ts ? e->W : (e->W + 31) / 32);

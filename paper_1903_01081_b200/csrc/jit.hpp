@@ -12,6 +12,7 @@ namespace emtb200 {
 struct JitModule {
     CUmodule module = nullptr;
     CUfunction function = nullptr;
+    CUfunction function2 = nullptr;  // optional "emt_src_kernel" of the same module
     double compile_seconds = 0.0;  // 0 when served from a cache
     bool cached = false;
 };
