@@ -110,7 +110,15 @@ struct Gen {
     // lane-invariant AC sources tabulated per launch (emt_src_kernel): process id -> table column
     bool srctab = false;
     std::map<int, int> tab_of;
-    std::vector<std::array<int, 3>> tab_ck;  // column -> const slots (m, w, p)
+    std::vector<std::array<int, 3>> tab_ck;  // source -> const slots (m, w, p)
+    std::vector<int> tab_var;                // source -> 1 when its value differs per lane
+    int tab_shared() const { int n = 0; for (int v : tab_var) n += v == 0; return n; }
+    /// table column of source j for this thread's lane (row = one pass)
+    std::string tab_col(int j) const {
+        const int ns = tab_shared();
+        if (tab_var[static_cast<size_t>(j)] == 0) return std::to_string(j);
+        return "(" + std::to_string(ns) + " + " + std::to_string(j - ns) + " * W_ + gl)";
+    }
     int ls = 32;     // doubles between consecutive slots of one lane in S[] (32 lanes per CTA; 1 in task-SIMT)
     int unit = 256;  // record offset units per slot (bytes of a 32-lane row; 1 = slot index in task-SIMT)
     Gen(const Schedule& sc, const std::vector<double>& c, int w, const CodegenOptions& o) : s(sc), ct(c), W(w), opt(o) {
@@ -241,13 +249,21 @@ struct Gen {
         pre_ck.clear();
         tab_of.clear();
         tab_ck.clear();
+        tab_var.clear();
         if (srctab)
-            for (const Proc& p : s.procs) {
-                const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
-                if (wk < 0 || !invariant(wk) || c0(wk) == 0.0 || !invariant(wk - 1) || !invariant(wk + 1)) continue;
-                tab_of[p.id] = static_cast<int>(tab_ck.size());
-                tab_ck.push_back({wk - 1, wk, wk + 1});
-            }
+            for (int pass = 0; pass < 2; ++pass)  // shared columns first, then per-lane ones
+                for (const Proc& p : s.procs) {
+                    const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
+                    if (wk < 0 || (invariant(wk) && c0(wk) == 0.0)) continue;  // DC (or omega varying incl. 0: below)
+                    bool ok = true;  // omega must be nonzero in every lane
+                    for (int l = 0; l < W && ok; ++l) ok = ct[static_cast<size_t>(wk) * W + l] != 0.0;
+                    if (!ok) continue;
+                    const bool shared = invariant(wk) && invariant(wk - 1) && invariant(wk + 1);
+                    if (shared != (pass == 0)) continue;
+                    tab_of[p.id] = static_cast<int>(tab_ck.size());
+                    tab_ck.push_back({wk - 1, wk, wk + 1});
+                    tab_var.push_back(shared ? 0 : 1);
+                }
         if (presrc)
             for (const Proc& p : s.procs) {
                 const int wk = p.code == kNortonVoltageSource ? p.par + 2 : p.code == kNortonCurrentSource ? p.par + 1 : -1;
@@ -993,8 +1009,8 @@ const KindCode kCode[K_NKINDS] = {
     /*SRCPRE*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
                "const double v@ = m@ * cos(w@ * tn + p@);", "ST({I0}, v@);"},
     // sources read from the launch's value table (emt_src_kernel computes m*cos(w t + p))
-    /*VSRCT*/ {"const double g@ = {C0}; const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + {I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
-    /*ISRCT*/ {"const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + {I1});", "", "ST({I0}, v@);"},
+    /*VSRCT*/ {"const double g@ = {C0}; const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + ({I1} < NSHR_ ? {I1} : NSHR_ + ({I1} - NSHR_) * W_ + gl));", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
+    /*ISRCT*/ {"const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + ({I1} < NSHR_ ? {I1} : NSHR_ + ({I1} - NSHR_) * W_ + gl));", "", "ST({I0}, v@);"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1079,6 +1095,7 @@ struct LitCtx {
     int sw_bit = -1;                       // >= 0: switch task writes its change flag to bit sw_bit of swbits
     bool chg_flag = false;                 // switch "changed" slots collapsed into needS
     bool dok = true;                       // divergence as an AND-ed predicate (cold index scan)
+    bool sw_slim = false;                  // switch hot path only tests for a change; stores go to the cold path
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
@@ -1118,6 +1135,10 @@ std::string task_literal(const Task& t, const LitCtx& c) {
             else
                 o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
+    } else if (t.kind == K_SW && c.sw_bit >= 0 && c.sw_slim) {
+        o << "int now = " << c.cst(t.ck[2]) << " != 0.0 ? 1 : 0; ";
+        for (size_t j = 3; j < t.ck.size(); ++j) o << "if (t >= " << c.cst(t.ck[j]) << ") now ^= 1; ";
+        o << "if ((double)now != LD(" << t.f[0] << ")) swbits |= 1ull << " << c.sw_bit << ";";
     } else if (t.kind == K_SW && c.sw_bit >= 0) {
         // change flag into the warp's bit mask; event logging, the refactor flag
         // and wflag happen once per pass in the (rare) non-zero-mask path
@@ -1370,6 +1391,17 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     };
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
+    bool sw_slim = switch_bits && g.chg_flag && knob("EMTB200_CG_SWSLIM", 1) != 0;
+    {
+        std::set<int> sw_slots;
+        for (const Task& t : g.tasks)
+            if (t.kind == K_SW) { sw_slots.insert(t.reads.begin(), t.reads.end()); sw_slots.insert(t.writes.begin(), t.writes.end()); }
+        for (const Task& t : g.tasks) {
+            if (t.kind == K_SW) continue;
+            for (int x : t.reads) sw_slim = sw_slim && !sw_slots.count(x);
+            for (int x : t.writes) sw_slim = sw_slim && !sw_slots.count(x);
+        }
+    }
     std::vector<std::pair<std::string, std::vector<int>>> sw_tables;
     // One same-kind segment as a loop over a constant-memory record table
     // (warp-uniform records: LDCU + LDS [lane base + uniform offset]).
@@ -1437,6 +1469,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             for (int w = 0; w < G; ++w) {
                 rc << "    case " << w << ": {\n";
                 std::vector<int> sw_ids;  // process id per swbits bit
+                std::vector<int> sw_tasks;  // task per swbits bit
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
                     if (p > 0) rc << mark(prof_base + 2 * static_cast<int>(p) - 2) << "      BAR();\n"
                                   << mark(prof_base + 2 * static_cast<int>(p) - 1);
@@ -1454,10 +1487,12 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         const int id = ordered[oi];
                         const Task& t = g.tasks[static_cast<size_t>(id)];
                         LitCtx c = lctx;
-                        if (t.kind == K_SW && switch_bits && sw_ids.size() < 64) {
+                        if (t.kind == K_SW && switch_bits && sw_ids.size() < 64 && t.region == 0) {
                             c.sw_bit = static_cast<int>(sw_ids.size());
                             c.chg_flag = g.chg_flag;
+                            c.sw_slim = sw_slim;
                             sw_ids.push_back(t.f[3]);
+                            sw_tasks.push_back(id);
                         }
                         rc << "      " << task_literal(t, c) << "\n";
                     }
@@ -1465,6 +1500,24 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 if (!sw_ids.empty()) {
                     const std::string tab = "kSwIds" + std::to_string(sw_tables.size());
                     sw_tables.push_back({tab, sw_ids});
+                    std::string commit;  // slim path: state and conductance stores of the changed switches
+                    if (sw_slim) {
+                        std::ostringstream cm;
+                        // the first pass of a launch writes every switch's state and conductance,
+                        // as the reference does each pass (the arena may hold other initial values)
+                        cm << " { unsigned long long b = it == 0 ? " << (sw_tasks.size() >= 64 ? std::string("~0ull") : "((1ull << " + std::to_string(sw_tasks.size()) + ") - 1ull)")
+                           << " : swbits; while (b) { const int j = __ffsll((long long)b) - 1; b &= b - 1; switch (j) {";
+                        for (size_t j = 0; j < sw_tasks.size(); ++j) {
+                            const Task& t = g.tasks[static_cast<size_t>(sw_tasks[j])];
+                            cm << " case " << j << ": { int now = " << lctx.cst(t.ck[2]) << " != 0.0 ? 1 : 0;";
+                            for (size_t q = 3; q < t.ck.size(); ++q) cm << " if (t >= " << lctx.cst(t.ck[q]) << ") now ^= 1;";
+                            cm << " ST(" << t.f[0] << ", (double)now); ST(" << t.f[2] << ", now != 0 ? " << lctx.cst(t.ck[0]) << " : "
+                               << lctx.cst(t.ck[1]) << "); } break;";
+                        }
+                        cm << " } } }";
+                        commit = cm.str();
+                    }
+                    if (sw_slim) rc << "      if (it == 0 || swbits != 0ull) {" << commit << " }\n";
                     rc << "      if (swbits != 0ull) { wflag = 1;" << (g.chg_flag ? " needS[lane] = 1;" : "")
                        << " if (live && a.events) { unsigned long long b = swbits; while (b) { const int j = __ffsll((long long)b) - 1; "
                           "b &= b - 1; const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
@@ -1577,7 +1630,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const long long Wl = lanes;
     o << "// generated by emtb200 codegen: " << s.nodes << " nodes, " << s.comps << " components, " << s.layers
       << " layers, " << lanes << " lanes, " << G << " warps, " << nt << " tasks, " << segs_total << " segments\n";
-    o << "#define NSRC_ " << std::max<size_t>(1, g.tab_ck.size()) << "\n";
+    {
+        const int ns = g.tab_shared(), nv = static_cast<int>(g.tab_ck.size()) - g.tab_shared();
+        o << "#define NSHR_ " << ns << "\n#define NSRC_ " << std::max<long long>(1, ns + static_cast<long long>(nv) * lanes) << "LL\n";
+        out.nsrc = static_cast<int>(std::max<long long>(0, ns + static_cast<long long>(nv) * lanes));
+    }
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
@@ -1771,21 +1828,25 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "}\n";
 
     if (!g.tab_ck.empty()) {
-        // per-launch table of the lane-invariant AC source values: the same expression,
-        // operands and time base as the inline form (bit-identical), computed once for
-        // all lanes instead of by every lane group's instruction stream
-        o << "extern \"C\" __global__ void emt_src_kernel(double* tab, int step0, int nsteps) {\n"
-          << "  const int i = blockIdx.x * blockDim.x + threadIdx.x;\n"
-          << "  if (i >= nsteps * NSRC_) return;\n"
-          << "  const int it = i / NSRC_, j = i - it * NSRC_;\n"
+        // per-launch table of the AC source values m*cos(w t + p): the same expression,
+        // operands and time base as the inline form (bit-identical), computed once per
+        // (pass, source[, lane]) instead of inside every lane group's instruction stream.
+        // Row = one pass: shared sources, then per-lane sources x W_ lanes.
+        const int ns = g.tab_shared();
+        o << "extern \"C\" __global__ void emt_src_kernel(double* tab, int step0, int nsteps, const double* __restrict__ ctab) {\n"
+          << "  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;\n"
+          << "  if (i >= (long long)nsteps * NSRC_) return;\n"
+          << "  const int it = (int)(i / NSRC_); const int col = (int)(i - (long long)it * NSRC_);\n"
           << "  const double t = (double)(step0 + it + 1) * " << lit(s.dt) << ";\n"
+          << "  int j = col; long long ln = 0;\n"
+          << "  if (col >= " << ns << ") { j = " << ns << " + (col - " << ns << ") / (int)W_; ln = (col - " << ns << ") % W_; }\n"
+          << "  const double* C = ctab + ln; (void)C;\n"
           << "  double v = 0.0;\n  switch (j) {\n";
         for (size_t j = 0; j < g.tab_ck.size(); ++j)
-            o << "    case " << j << ": v = " << lit(g.c0(g.tab_ck[j][0])) << " * cos(" << lit(g.c0(g.tab_ck[j][1])) << " * t + "
-              << lit(g.c0(g.tab_ck[j][2])) << "); break;\n";
+            o << "    case " << j << ": v = " << g.C(g.tab_ck[j][0]) << " * cos(" << g.C(g.tab_ck[j][1]) << " * t + "
+              << g.C(g.tab_ck[j][2]) << "); break;\n";
         o << "  }\n  tab[i] = v;\n}\n";
     }
-    out.nsrc = static_cast<int>(g.tab_ck.size());
     out.source = o.str();
     out.warps = G;
     out.smem_bytes = smem;

@@ -1014,7 +1014,8 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
             a.srctab = e->d_srctab;
             double* tab = e->d_srctab;
             int s0 = e->step, ns = steps;
-            void* tp[] = {&tab, &s0, &ns};
+            const double* ct = e->plan.ctab;
+            void* tp[] = {&tab, &s0, &ns, &ct};
             const CUresult r2 = driver()->LaunchKernel(e->jit.function2, static_cast<unsigned>((need + 255) / 256), 1, 1, 256, 1, 1, 0,
                                                        reinterpret_cast<CUstream>(e->stream), tp, nullptr);
             if (r2 != CUDA_SUCCESS) return set_error(EMT_CUDA_ERROR, "cuLaunchKernel(emt_src_kernel) failed");
