@@ -107,6 +107,11 @@ struct Gen {
     std::map<int, int> pre_of;   // source process id -> j
     std::vector<std::array<int, 3>> pre_ck;  // j -> const slots (m, w, p)
     int pre_base = 0;
+    // pivot reciprocals 1/u_ii in shared memory (rcp_base + row): the backward sweep's
+    // division becomes q0 = x*r, x/u = fma(fma(-u, q0, x), r, q0) (Markstein; correctly
+    // rounded for normal-range operands, tools/micro/divcheck.c)
+    bool rcp = false;
+    int rcp_base = -1;
     // lane-invariant AC sources tabulated per launch (emt_src_kernel): process id -> table column
     bool srctab = false;
     std::map<int, int> tab_of;
@@ -545,7 +550,7 @@ struct Gen {
                     t.terms.push_back({lu_u(k), off(v + c)});
                 }
                 t.writes = {v + i};
-                t.f = {off(v + i), lu_u(ub), i};
+                t.f = {off(v + i), lu_u(ub), i, rcp_base >= 0 ? (rcp_base + i) * unit : -1};
                 t.cost = 40 + 5 * (ue - ub - 1);
                 add(std::move(t), region);
             }
@@ -687,13 +692,29 @@ struct Gen {
             u_base_smem = l_base_smem + static_cast<int>(s.l_col.size());
             used += lu;
         }
+        rcp_base = -1;
+        const size_t rb = static_cast<size_t>(s.dim) * per_slot;
+        if (rcp && lu_smem && s.dim > 0) {
+            if (used + rb > opt.smem_budget && !vc_slots.empty()) {
+                // make room: lane-varying constants are then read from the const table (L1)
+                used -= vc_slots.size() * per_slot;
+                std::fill(vc_index.begin(), vc_index.end(), -1);
+                vc_slots.clear();
+                l_base_smem = vc_base;
+                u_base_smem = l_base_smem + static_cast<int>(s.l_col.size());
+            }
+            if (used + rb <= opt.smem_budget) {
+                rcp_base = u_base_smem + static_cast<int>(s.u_col.size());
+                used += rb;
+            }
+        }
         smem_bytes = used;
         return true;
     }
 
     int smem_slots() const {
         return vc_base + static_cast<int>(vc_slots.size()) +
-               (l_base_smem >= 0 ? static_cast<int>(s.l_col.size() + s.u_col.size()) : 0);
+               (l_base_smem >= 0 ? static_cast<int>(s.l_col.size() + s.u_col.size()) : 0) + (rcp_base >= 0 ? s.dim : 0);
     }
 
     // Refactorization (FactorizeSystem, exec.cpp:175-204; lu_factor, sparse.cpp:79-145)
@@ -747,7 +768,9 @@ struct Gen {
             }
             for (int k = ub; k < ue; ++k) {
                 const int c = s.u_col[static_cast<size_t>(k)];
-                o << "          u" << k << " = w" << c << "; " << Uw(k, "u" + std::to_string(k)) << "\n";
+                o << "          u" << k << " = w" << c << "; " << Uw(k, "u" + std::to_string(k));
+                if (k == ub && rcp_base >= 0) o << " S[" << (rcp_base + i) * ls << "] = 1.0 / u" << k << ";";
+                o << "\n";
             }
             for (int c : cols)
                 if (last_row[static_cast<size_t>(c)] == i)
@@ -1131,7 +1154,11 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         for (const auto& tm : t.terms) o << "x = x - LU(" << tm.first << ") * LD(" << tm.second << "); ";
         if (t.kind == K_BWD)
             if (c.dok)
-                o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= a.div_limit); ";
+                if (t.f.size() > 3 && t.f[3] >= 0)
+                    o << "{ const double r_ = LD(" << t.f[3] << "); const double d_ = LU(" << t.f[1]
+                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } dok = dok & (fabs(x) <= a.div_limit); ";
+                else
+                    o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= a.div_limit); ";
             else
                 o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
@@ -1260,7 +1287,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
-    g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;  // measured 3% slower: moves cos, does not remove it
+    g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;
+    g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;  // measured 3% slower: moves cos, does not remove it
     g.classify();
     std::vector<double> ginv;
     if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
@@ -1725,6 +1753,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << s.l << " + q) * W_];\n";
         o << "  for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * 32] = A[(size_t)("
           << s.u << " + q) * W_];\n";
+        if (g.rcp_base >= 0) {
+            std::ostringstream dg;
+            for (int i = 0; i < s.dim; ++i) dg << (i ? "," : "") << s.u_row_ptr[static_cast<size_t>(i)];
+            o << "  { const int kUd[" << s.dim << "] = {" << dg.str() << "};\n"
+              << "    for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * 32] = 1.0 / A[(size_t)("
+              << s.u << " + kUd[q]) * W_]; }\n";
+        }
     }
     // watch slots not rewritten by region-A tasks (the dirty flag) are checked up front
     std::set<int> written_a;
