@@ -1156,9 +1156,9 @@ std::string task_literal(const Task& t, const LitCtx& c) {
             if (c.dok)
                 if (t.f.size() > 3 && t.f[3] >= 0)
                     o << "{ const double r_ = LD(" << t.f[3] << "); const double d_ = LU(" << t.f[1]
-                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } dok = dok & (fabs(x) <= a.div_limit); ";
+                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } dok = dok & (fabs(x) <= dlim); ";
                 else
-                    o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= a.div_limit); ";
+                    o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= dlim); ";
             else
                 o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
@@ -1643,7 +1643,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 const int mt = tiles[j] / 4, ntl = tiles[j] % 4;
                 blk << "      { const int m = " << mt * 8 << " + (lane >> 2); if (m < " << s.dim << ") { const int o = kVrow[m] + "
                     << ntl * 8 << " + (lane & 3) * 2; sm[o] = d" << j << "a; sm[o + 1] = d" << j << "b; "
-                    << "dok = dok & (fabs(d" << j << "a) <= a.div_limit) & (fabs(d" << j << "b) <= a.div_limit); } }\n";
+                    << "dok = dok & (fabs(d" << j << "a) <= dlim) & (fabs(d" << j << "b) <= dlim); } }\n";
             }
             blk << "    } break;\n";
         }
@@ -1771,6 +1771,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  __syncthreads();\n"
       << "  int it = 0;\n"
       << "  long long prof_t = clock64(); (void)prof_t;\n"
+      << "  const double dlim = a.div_limit; (void)dlim;\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
@@ -2101,7 +2102,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
             c << "const int n = RI(" << tb << "); double x = S[RI(0)]; ";
             for (int j = 0; j < w.maxt; ++j)
                 c << "if (" << j << " < n) x = x - S[RI(" << tb + 1 + 2 * j << ")] * S[RI(" << tb + 2 + 2 * j << ")]; ";
-            if (w.kind == K_BWD) c << "x = x / S[RI(1)]; dok = dok & (fabs(x) <= a.div_limit); ";
+            if (w.kind == K_BWD) c << "x = x / S[RI(1)]; dok = dok & (fabs(x) <= dlim); ";
             c << "S[RI(0)] = x;";
         } else if (w.kind == K_SW) {
             c << "int now = S[KS(2)] != 0.0 ? 1 : 0; ";
@@ -2204,6 +2205,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << "  for (int q = threadIdx.x; q < " << cslots.size() << "; q += " << NTH << ") S[" << const_base << " + q] = __ldg(C + (size_t)kCst[q] * W_);\n"
       << "  if (threadIdx.x == 0) { S[0] = 0.0; needS[0] = 0; }\n"
       << "  __syncthreads();\n"
+      << "  const double dlim = a.div_limit; (void)dlim;\n"
       << "  for (int it = 0; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"

@@ -59,3 +59,19 @@ def test_codegen_nvrtc_compiles_sm100a():
         g = load_golden(name)
         src, summary = engine.codegen(g.schedule, warps=4, compile=True)
         assert "nvrtc=" in summary and "cubin=" in summary
+
+
+def test_codegen_variants_nvrtc_compile():
+    """Every generator variant compiles for sm_100a: task-SIMT (warps < 0) and the
+    shared-G tensor-core solve (warps <= -100) on a PV batch, lane-SIMT on a line case."""
+    import bench
+    from conftest import load_golden
+    g = load_golden("cyclic_controls")
+    src, summary = engine.codegen(g.schedule, warps=-4, compile=True)
+    assert "emt_ts_kernel" in src and "cubin=" in summary
+    b, _ = bench.build_batch(64, workload="c5")
+    src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=-108, compile=True)
+    assert "solve=dmma" in summary and "mma.sync.aligned.m8n8k4" in src
+    b, _ = bench.build_batch(64, workload="c4")
+    src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=8, compile=True)
+    assert "emt_src_kernel" in src and "cubin=" in summary
