@@ -173,6 +173,12 @@ emt_status emt_engine_commit(emt_engine* engine);
  * has landed; errors as emt_engine_sync. Grows the waveform store as needed
  * (SURVEY.md §8(b) emt_run). */
 emt_status emt_engine_run(emt_engine* engine, int32_t steps, int32_t chunk, double* waves);
+/* emt_engine_run without the final wait: returns once every launch and copy is
+ * enqueued (the host buffer must stay alive and untouched until emt_engine_wait,
+ * and the engine must not be reloaded before it). Lets a caller overlap one
+ * batch's last waveform copies with the next batch's compute on another engine. */
+emt_status emt_engine_run_async(emt_engine* engine, int32_t steps, int32_t chunk, double* waves);
+emt_status emt_engine_wait(emt_engine* engine);
 
 /* Line-end history mirror (Bergeron extension, kernel code 20): a device array
  * of `lanes` (= the whole batch width) x `cols` doubles, lane-major, holding

@@ -1270,7 +1270,7 @@ emt_status emt_engine_attach_ring(emt_engine* e, void* device_ptr) {
     return EMT_OK;
 }
 
-emt_status emt_engine_run(emt_engine* e, int32_t steps, int32_t chunk, double* waves) {
+emt_status emt_engine_run_async(emt_engine* e, int32_t steps, int32_t chunk, double* waves) {
     if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
     if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
     if (e->rows + steps > e->capacity) EMT_TRY(emt_engine_reserve_keep(e, e->rows + steps));
@@ -1297,8 +1297,19 @@ emt_status emt_engine_run(emt_engine* e, int32_t steps, int32_t chunk, double* w
         CUDA_TRY(cudaMemcpyAsync(waves + row * static_cast<size_t>(c) * chunk, e->d_waves + row * r0,
                                  row * n * sizeof(double), cudaMemcpyDeviceToHost, e->copy_stream));
     }
+    return EMT_OK;
+}
+
+emt_status emt_engine_wait(emt_engine* e) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
     if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
     return emt_engine_sync(e);
+}
+
+emt_status emt_engine_run(emt_engine* e, int32_t steps, int32_t chunk, double* waves) {
+    EMT_TRY(emt_engine_run_async(e, steps, chunk, waves));
+    return emt_engine_wait(e);
 }
 
 emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,

@@ -114,6 +114,8 @@ def lib():
         L.emt_engine_stage.argtypes = [vp, dp, ctypes.c_int64, dp]
         L.emt_engine_commit.argtypes = [vp]
         L.emt_engine_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
+        L.emt_engine_run_async.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp]
+        L.emt_engine_wait.argtypes = [vp]
         L.emt_engine_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
         L.emt_engine_ring.argtypes = [vp, ctypes.POINTER(vp), ip, ip, ip]
         L.emt_engine_attach_ring.argtypes = [vp, vp]
@@ -136,7 +138,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
-    "emt_engine_profile",
+    "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
 ]
 
 
@@ -338,6 +340,17 @@ class Engine:
 
     def attach_ring(self, device_ptr: int) -> None:
         _check(lib().emt_engine_attach_ring(self._h, ctypes.c_void_p(device_ptr)))
+
+    def run_async(self, steps: int, out: np.ndarray, chunk: int = 0) -> None:
+        """run() without the final wait (call wait() before touching `out` or reloading)."""
+        assert out.dtype == np.float64 and out.flags.c_contiguous and out.size >= steps * self.channels * self.lanes
+        self._async_out = out
+        _check(lib().emt_engine_run_async(self._h, int(steps), int(chunk), _dp(out)))
+        self.rows += steps
+
+    def wait(self) -> None:
+        _check(lib().emt_engine_wait(self._h))
+        self._async_out = None
 
     def sync(self) -> None:
         _check(lib().emt_engine_sync(self._h))

@@ -261,3 +261,23 @@ def test_tensor_solve_ignored_when_g_is_not_shared():
     eng.reserve(600)
     eng.advance(600)
     assert bitwise_equal(eng.waves().values, base.values)
+
+
+def test_run_async_two_engines_alternating():
+    """run_async/wait with two engines taking turns (the serving pipeline) == synchronous runs."""
+    g = load_golden("feeder_w4")
+    want = engine.interpret(g.schedule, g.initial, 500)
+    engs = [engine.Engine(g.schedule, g.initial) for _ in range(2)]
+    outs = [np.zeros((500, engs[0].channels * engs[0].lanes)) for _ in range(2)]
+    for k in range(4):
+        e = engs[k % 2]
+        if k >= 2:
+            e.wait()
+            assert bitwise_equal(outs[k % 2], want.values)
+            outs[k % 2][:] = 0.0
+        e.stage(g.initial)
+        e.commit()
+        e.run_async(500, outs[k % 2], chunk=128)
+    for k, e in enumerate(engs):
+        e.wait()
+        assert bitwise_equal(outs[k], want.values)
