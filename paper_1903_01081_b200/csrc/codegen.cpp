@@ -72,6 +72,7 @@ struct Task {
     std::vector<int> reads, writes;          // arena slots, for dependencies
     int cost = 1;
     int region = 0;  // 0: before FactorizeSystem, 1: after
+    bool fused = false;  // Norton task that also recomputes its own i_prev (finalize fused away)
 };
 
 enum Cls { kNone = 0, kHot, kDerived, kContrib, kSolver, kChg };
@@ -112,6 +113,11 @@ struct Gen {
     // rounded for normal-range operands, tools/micro/divcheck.c)
     bool rcp = false;
     int rcp_base = -1;
+    // finalize fusion: an L / C / RL component whose current only its own next-pass
+    // Norton update reads gets i_prev = g (vb - va) + h recomputed there (the same
+    // operands and order as the finalize), and its finalize runs once per launch
+    bool fusefin = false;
+    std::set<int> fused;  // component (= Norton process) ids
     // lane-invariant AC sources tabulated per launch (emt_src_kernel): process id -> table column
     bool srctab = false;
     std::map<int, int> tab_of;
@@ -293,6 +299,32 @@ struct Gen {
         }
         for (int x : s.channel_slot) iread.insert(x);
         for (int x : s.latch_live) iread.insert(x);
+        fused.clear();
+        if (fusefin) {
+            std::map<int, int> readers;  // slot -> number of reading ports / channels / latches
+            for (const Proc& p : s.procs) {
+                int lo = 0, hi = p.in_count;
+                if (p.code == kNortonResistor || p.code == kNortonVoltageSource || p.code == kNortonCurrentSource ||
+                    p.code == kNortonSwitch)
+                    hi = 0;
+                else if (p.code == kNortonControlledSource)
+                    lo = 3;
+                else if (p.code == kNortonBergeron)
+                    hi = std::min(hi, 2);
+                for (int j = lo; j < hi; ++j) readers[s.port_slot[static_cast<size_t>(p.in_base + j)]] += 1;
+            }
+            for (int x : s.channel_slot) readers[x] += 1;
+            for (int x : s.latch_live) readers[x] += 1;
+            for (const Proc& p : s.procs) {
+                if (p.code != kNortonInductor && p.code != kNortonCapacitor && p.code != kNortonSeriesRL) continue;
+                if (p.id < 0 || p.id >= s.comps || p.in_count < 3) continue;
+                const int* f = s.finalize.data() + 5 * p.id;
+                const int* in = s.port_slot.data() + p.in_base;
+                if (f[0] < 0 || f[0] != in[2] || f[2] != p.out2 || f[3] != in[0] || f[4] != in[1] || f[1] != p.out) continue;
+                if (readers[f[0]] != 1) continue;
+                fused.insert(p.id);
+            }
+        }
         cls.assign(n, kNone);
         derived_const.assign(n, -2);
         contrib_h.assign(n, -1);
@@ -359,6 +391,10 @@ struct Gen {
             case kNortonSeriesRL:
                 t.kind = p.code == kNortonInductor ? K_IND : p.code == kNortonCapacitor ? K_CAP : K_SRL;
                 reads(t, {IN(0), IN(1), IN(2)});
+                if (fused.count(p.id)) {
+                    t.fused = true;
+                    t.reads.push_back(p.out2);
+                }
                 t.writes = {p.out2};
                 t.f = {off(IN(0)), off(IN(1)), off(IN(2)), off(p.out2)};
                 t.ck = {p.par};
@@ -557,6 +593,10 @@ struct Gen {
         }
         for (int c = 0; c < s.comps; ++c) {  // i = g (v_b - v_a) + h
             const int* f = s.finalize.data() + 5 * c;
+            if (fused.count(c)) {  // recomputed by its next-pass Norton update; arena copy once per launch
+                lazy_fin.push_back(c);
+                continue;
+            }
             if (lazy_i && f[0] >= 0 && !iread.count(f[0])) {
                 // nothing reads this current inside a pass: computing it from the
                 // launch's final v, g, h gives the bits the last pass would have
@@ -1119,6 +1159,7 @@ struct LitCtx {
     bool chg_flag = false;                 // switch "changed" slots collapsed into needS
     bool dok = true;                       // divergence as an AND-ed predicate (cold index scan)
     bool sw_slim = false;                  // switch hot path only tests for a change; stores go to the cold path
+    bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
@@ -1142,7 +1183,16 @@ std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
 std::string task_literal(const Task& t, const LitCtx& c) {
     std::ostringstream o;
     o << "{ ";
-    if (kCode[t.kind].loads != nullptr) {
+    if (t.fused && c.fused_pass) {
+        // i_prev = g (vb - va) + h as the finalize computed it last pass (exec.cpp:220-228)
+        const std::string vb = std::to_string(t.f[1]), va = std::to_string(t.f[0]), h = std::to_string(t.f[3]);
+        o << "const double vs = LD(" << vb << ") - LD(" << va << "); const double hp = LD(" << h << "); const double g = "
+          << c.cst(t.ck[0]) << "; const double ip = g * vs + hp; ";
+        if (t.kind == K_IND) o << "const double hn = ip + g * vs; ";
+        else if (t.kind == K_CAP) o << "const double hn = -ip - g * vs; ";
+        else o << "const double d = " << c.cst(t.ck[1]) << "; const double hn = d * ip + g * vs; ";
+        o << "ST(" << h << ", hn);";
+    } else if (kCode[t.kind].loads != nullptr) {
         o << expand_lit(kCode[t.kind].loads, t, c) << " " << expand_lit(kCode[t.kind].compute, t, c) << " "
           << expand_lit(kCode[t.kind].store, t, c);
     } else if (t.kind == K_GATHER || t.kind == K_SUM) {
@@ -1288,7 +1338,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     Gen g(s, ctab, lanes, opt);
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
     g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;
-    g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;  // measured 3% slower: moves cos, does not remove it
+    g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;
+    g.fusefin = knob("EMTB200_CG_FUSEFIN", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 &&
+                knob("EMTB200_CG_WARPMAJOR", 1) != 0;  // measured 3% slower: moves cos, does not remove it
     g.classify();
     std::vector<double> ginv;
     if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
@@ -1309,6 +1361,16 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     if (!g.assign_hot(lu_smem, smem)) {
         fail = {13, "", "arena hot set exceeds the shared-memory budget"};
         return false;
+    }
+    if (g.fusefin && !g.fused.empty() && !lu_smem && !g.dmma) {
+        // measured: with the factors in HBM (C5 exact path) the fused form schedules worse
+        g.fusefin = false;
+        g.classify();
+        g.emit_all(facts);
+        if (!g.assign_hot(lu_smem, smem)) {
+            fail = {13, "", "arena hot set exceeds the shared-memory budget"};
+            return false;
+        }
     }
     g.emit_all(facts);  // pass 2: records with shared-memory offsets
 
@@ -1486,7 +1548,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     auto loopable = [](int kind) {
         return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
     };
-    auto region_code = [&](const Sched& sc) {
+    auto region_code = [&](const Sched& sc, bool fused_pass) {
         std::ostringstream rc;
         if (straight && warp_major) {
             // One contiguous block per warp holding all of its phases, phases
@@ -1515,6 +1577,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         const int id = ordered[oi];
                         const Task& t = g.tasks[static_cast<size_t>(id)];
                         LitCtx c = lctx;
+                        c.fused_pass = fused_pass;
                         if (t.kind == K_SW && switch_bits && sw_ids.size() < 64 && t.region == 0) {
                             c.sw_bit = static_cast<int>(sw_ids.size());
                             c.chg_flag = g.chg_flag;
@@ -1577,9 +1640,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
         return rc.str();
     };
-    const std::string code_a = region_code(sa);
-    const std::string code_b = region_code(sb);
-    const std::string code_c = g.dmma ? region_code(sc3) : std::string();
+    std::string code_a = region_code(sa, false);
+    if (!g.fused.empty()) {  // the launch's first pass reads i_prev from the arena; later passes recompute it
+        const std::string code_af = region_code(sa, true);
+        code_a = "    if (__builtin_expect(it != 0, 1)) {\n" + code_af + "    } else {\n" + code_a + "    }\n";
+    }
+    const std::string code_b = region_code(sb, false);
+    const std::string code_c = g.dmma ? region_code(sc3, false) : std::string();
     const size_t const_bytes = rki.size() * 4 + rkd.size() * 8 + static_cast<size_t>(s.consts) * 8;
     if (const_bytes > 62 * 1024) {
         fail = {13, "", "task tables (" + std::to_string(const_bytes) + " B) exceed constant memory"};
