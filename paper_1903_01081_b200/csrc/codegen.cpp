@@ -1160,6 +1160,8 @@ struct LitCtx {
     bool dok = true;                       // divergence as an AND-ed predicate (cold index scan)
     bool sw_slim = false;                  // switch hot path only tests for a change; stores go to the cold path
     bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
+    std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
+    bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
@@ -1206,12 +1208,17 @@ std::string task_literal(const Task& t, const LitCtx& c) {
             if (c.dok)
                 if (t.f.size() > 3 && t.f[3] >= 0)
                     o << "{ const double r_ = LD(" << t.f[3] << "); const double d_ = LU(" << t.f[1]
-                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } dok = dok & (fabs(x) <= dlim); ";
+                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } "
+                      << (c.dsum ? "dsum = dsum + fabs(x); " : "dok = dok & (fabs(x) <= dlim); ");
                 else
                     o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= dlim); ";
             else
                 o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
+    } else if (t.kind == K_SW && c.sw_bit >= 0 && c.sw_slim && t.ck.size() == 4 && c.lit_init && c.lit_init(t.ck[2]) >= 0) {
+        // one toggle time: changed <=> (init XOR t >= t0) != state, init folded in
+        o << "{ const bool f_ = t >= " << c.cst(t.ck[3]) << "; const bool s_ = LD(" << t.f[0] << ") != 0.0; if ("
+          << (c.lit_init(t.ck[2]) ? "!f_" : "f_") << " != s_) swbits |= 1ull << " << c.sw_bit << "; }";
     } else if (t.kind == K_SW && c.sw_bit >= 0 && c.sw_slim) {
         o << "int now = " << c.cst(t.ck[2]) << " != 0.0 ? 1 : 0; ";
         for (size_t j = 3; j < t.ck.size(); ++j) o << "if (t >= " << c.cst(t.ck[j]) << ") now ^= 1; ";
@@ -1472,6 +1479,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     int segs_total = 0;
     const bool straight = opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", opt.mode == 1 ? 1 : 1) != 0;
     LitCtx lctx;
+    if (knob("EMTB200_CG_SWFOLD", 1)) lctx.lit_init = [&](int k) -> int { return g.invariant(k) ? (g.c0(k) != 0.0 ? 1 : 0) : -1; };
+    lctx.dsum = knob("EMTB200_CG_DSUM", 0) != 0;  // measured 0.6% slower than the AND-ed predicate
     const bool dok_mode = straight && (knob("EMTB200_CG_DOK", 1) != 0 || g.dmma);
     lctx.dok = dok_mode;
     lctx.cst = [&](int k) -> std::string {
@@ -1843,8 +1852,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    const double tn = (double)(step + 2) * " << lit(s.dt) << "; (void)tn;\n"
-      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
-      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
+      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true; double dsum = 0.0;\n"
+      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok; (void)dsum;\n"
       << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
@@ -1886,16 +1895,20 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         std::ostringstream tb;
         for (int i = 0; i < s.nodes; ++i) tb << (i ? "," : "") << g.off(s.v_base + i);
         if (s.nodes == 0) tb << "0";
-        o << "    if (__syncthreads_or(!dok && live)) {\n"
+        // dsum = sum of |x| over a warp's rows: NaN/inf propagate, and a sum above the
+        // limit only triggers the exact per-node scan (which may find nothing)
+        o << "    if (__syncthreads_or((!dok || !(dsum <= dlim)) && live)) {\n"
           << "      const int kVoff[" << std::max(1, s.nodes) << "] = {" << tb.str() << "};\n"
-          << "      if (!dok) serr[lane] = 0;\n"
+          << "      if (warp == 0 && live) serr[lane] = 0x7fffffff;\n"
           << "      __syncthreads();\n"
-          << "      if (warp == 0 && live && serr[lane] != 0x7fffffff) {\n"
+          << "      if (warp == 0 && live) {\n"
           << "        for (int i = 0; i < " << s.nodes << "; ++i) if (!(fabs(LD(kVoff[i])) <= a.div_limit)) { bad = i; break; }\n"
-          << "        a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
-          << g.solve_layer << ";\n"
+          << "        if (bad != 0x7fffffff) { serr[lane] = bad; a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
+          << g.solve_layer << "; }\n"
           << "      }\n"
-          << "      FAILPUB(); return;\n";
+          << "      if (__syncthreads_or(warp == 0 && live && serr[lane] != 0x7fffffff)) { FAILPUB(); return; }\n"
+          << "    }\n"
+          << "    if (false) {\n";
     } else {
         o << "    if (__syncthreads_or(bad != 0x7fffffff && live)) {\n"
           << "      if (bad != 0x7fffffff) atomicMin(&serr[lane], bad);\n"
