@@ -90,7 +90,7 @@ typedef struct emt_exec_stats {
     int32_t factor_count;    /* refactorization passes; == reference lane-0 fcount */
     int32_t measured_steps;
     double measured_seconds; /* device time of the step loop after warm-up (CUDA events) */
-    int32_t kernel_launches; /* step-loop kernel launches issued */
+    int32_t kernel_launches; /* kernels launched (step loop + per-launch source tables) */
     int32_t switch_events;   /* (step, lane, switch) state changes seen */
 } emt_exec_stats;
 

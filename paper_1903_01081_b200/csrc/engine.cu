@@ -1019,6 +1019,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
             const CUresult r2 = driver()->LaunchKernel(e->jit.function2, static_cast<unsigned>((need + 255) / 256), 1, 1, 256, 1, 1, 0,
                                                        reinterpret_cast<CUstream>(e->stream), tp, nullptr);
             if (r2 != CUDA_SUCCESS) return set_error(EMT_CUDA_ERROR, "cuLaunchKernel(emt_src_kernel) failed");
+            e->launches += 1;  // kernel_launches counts every kernel of ours
         }
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;

