@@ -1,6 +1,7 @@
-# Warp-count sweep + ncu source-level capture of the C2 and C3 specialised kernels.
-set -x
-for w in 4 6 8 10 12 16; do BENCH_ARGS="--warps $w" bash tools/knob_sweep.sh "X=$w"; done
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:emt_cg_kernel --launch-skip 3 -c 1 -o gpurun_out/ncu_c2b python bench.py --workload c2 --skip-cpu --skip-e2e --steps 1 --emt-steps 200 > gpurun_out/ncu_c2b.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:emt_cg_kernel --launch-skip 3 -c 1 -o gpurun_out/ncu_c3b python bench.py --skip-cpu --skip-e2e --steps 1 --emt-steps 200 > gpurun_out/ncu_c3b.log 2>&1
-ls -la gpurun_out/
+# Round profile: default bench line (C3), C2/C4/C5 (+ tensor-core C5), launch list, one full ncu capture.
+timeout 600 python bench.py > gpurun_out/bench_rX.json 2> gpurun_out/bench_rX.err
+for w in c2 c4 c5; do timeout 600 python bench.py --workload $w > gpurun_out/bench_rX_$w.json 2> gpurun_out/bench_rX_$w.err; done
+timeout 600 python bench.py --workload c5 --tensor-solve > gpurun_out/bench_rX_c5t.json 2> gpurun_out/bench_rX_c5t.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_rX.csv python bench.py --steps 2 --warmup 3 --skip-cpu > /dev/null 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:emt_cg_kernel --launch-skip 3 -c 1 -o gpurun_out/ncu_rX python bench.py --skip-cpu --skip-e2e --steps 1 --emt-steps 200 > gpurun_out/ncu_rX.log 2>&1
+cat gpurun_out/bench_rX.json
