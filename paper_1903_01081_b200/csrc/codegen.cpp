@@ -839,7 +839,7 @@ struct Sched {
 // earliest-idle warp starves while enough work waits behind the barrier.
 Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& ids,
                       const std::vector<std::vector<int>>& deps, int G, double* makespan) {
-    const long kBarrier = knob("EMTB200_CG_BARRIER", 200);
+    const long kBarrier = knob("EMTB200_CG_BARRIER", knob("EMTB200_CG_COSTV2", 1) ? 100 : 200);
     Sched out;
     const size_t n = ids.size();
     if (n == 0) {
@@ -1381,6 +1381,31 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     g.emit_all(facts);  // pass 2: records with shared-memory offsets
 
+    if (knob("EMTB200_CG_COSTV2", 1)) {
+        // cost model in issued instructions (the pass is issue/fetch bound)
+        for (Task& t : g.tasks) {
+            const int nt_ = static_cast<int>(t.terms.size());
+            int c = 8;
+            switch (t.kind) {
+                case K_IND: case K_CAP: case K_SRL: c = t.fused ? 12 : 10; break;
+                case K_VSRCT: c = 5; break;
+                case K_ISRCT: c = 4; break;
+                case K_VSRC: case K_ISRC: c = t.cost > 20 ? 60 : 4; break;
+                case K_SW: c = 8; break;
+                case K_GATHER: case K_SUM: c = 3 + 2 * nt_; break;
+                case K_FWD: c = 3 + 4 * nt_; break;
+                case K_BWD: c = (t.f.size() > 3 && t.f[3] >= 0 ? 10 : 20) + 4 * nt_; break;
+                case K_FINC: c = 7; break;
+                case K_FINS: c = 8; break;
+                case K_REC: c = 3; break;
+                case K_LATCH: c = 2; break;
+                case K_BERG: c = 25; break;
+                case K_SRCPRE: c = 60; break;
+                default: c = 8; break;
+            }
+            t.cost = c;
+        }
+    }
     // Dependencies from the sequential order (RAW, WAR, WAW), per region.
     const size_t nt = g.tasks.size();
     std::vector<std::vector<int>> deps(nt);
@@ -1452,6 +1477,27 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             load[bp][static_cast<size_t>(bw)] += g.tasks[static_cast<size_t>(id)].cost;
             pmax[bp] = std::max(pmax[bp], load[bp][static_cast<size_t>(bw)]);
         }
+    }
+    if (knob("EMTB200_CG_FWDSTAT", 0)) {  // how many operand reads could come from the reader warp's registers
+        std::map<int, int> warp_of_task;
+        for (const Sched* sc : std::initializer_list<const Sched*>{&sa, &sb, &sc3})
+            for (size_t p = 0; p < sc->phases.size(); ++p)
+                for (int w = 0; w < G; ++w)
+                    for (int id : sc->phases[p][static_cast<size_t>(w)]) warp_of_task[id] = w;
+        std::map<int, int> last_writer;
+        long same = 0, other = 0, none = 0;
+        for (size_t i = 0; i < nt; ++i) {
+            const Task& t = g.tasks[i];
+            if (i > 0 && g.tasks[i - 1].region != t.region) last_writer.clear();
+            for (int r : t.reads) {
+                auto it = last_writer.find(r);
+                if (it == last_writer.end()) ++none;
+                else if (warp_of_task[it->second] == warp_of_task[static_cast<int>(i)]) ++same;
+                else ++other;
+            }
+            for (int w : t.writes) last_writer[w] = static_cast<int>(i);
+        }
+        std::fprintf(stderr, "operand reads: same-warp producer %ld, other-warp %ld, from before the region %ld\n", same, other, none);
     }
     if (knob("EMTB200_CG_DUMP", 0)) {  // schedule dump: per phase, per warp "kind x count (cost)"
         for (const Sched* sc : std::initializer_list<const Sched*>{&sa, &sb, &sc3}) {
