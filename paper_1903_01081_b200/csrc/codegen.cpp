@@ -73,9 +73,10 @@ struct Task {
     int cost = 1;
     int region = 0;  // 0: before FactorizeSystem, 1: after
     bool fused = false;  // Norton task that also recomputes its own i_prev (finalize fused away)
+    bool out_alias = false;  // integrator / lag whose output slot aliases its state slot (out == y == state0)
 };
 
-enum Cls { kNone = 0, kHot, kDerived, kContrib, kSolver, kChg };
+enum Cls { kNone = 0, kHot, kDerived, kContrib, kSolver, kChg, kAlias };
 
 struct Gen {
     const Schedule& s;
@@ -118,6 +119,10 @@ struct Gen {
     // operands and order as the finalize), and its finalize runs once per launch
     bool fusefin = false;
     std::set<int> fused;  // component (= Norton process) ids
+    // control outputs that always equal the block's first state slot (integrator and
+    // first-order lag store y to both): readers use the state slot, the output slot is
+    // written back once per launch (shared memory and one store per pass saved)
+    std::map<int, int> alias_of;  // output slot -> state slot
     // lane-invariant AC sources tabulated per launch (emt_src_kernel): process id -> table column
     bool srctab = false;
     std::map<int, int> tab_of;
@@ -194,9 +199,12 @@ struct Gen {
         return true;
     }
 
-    /// Deferred finalize (exec.cpp:220-228) of the currents no task reads.
+    /// Deferred finalize (exec.cpp:220-228) of the currents no task reads, and the
+    /// aliased control outputs (= their state slot).
     std::string emit_lazy_finalize() const {
         std::ostringstream o;
+        for (const auto& kv : alias_of)
+            o << "      A[(size_t)" << kv.first << " * W_] = " << R(kv.second) << ";\n";
         for (int c : lazy_fin) {
             const int* f = s.finalize.data() + 5 * c;
             std::string gx;
@@ -220,12 +228,14 @@ struct Gen {
     int off(int slot) const {
         if (slot < 0) return 0;  // ground sentinel reads the zero slot
         if (slot >= s.extent) return (pre_base + slot - s.extent) * unit;  // precomputed source value
+        if (cls[static_cast<size_t>(slot)] == kAlias) return off(alias_of.at(slot));
         if (cls[static_cast<size_t>(slot)] == kDerived && derived_const[static_cast<size_t>(slot)] < 0) return 0;
         if (hot_index[static_cast<size_t>(slot)] < 0) return 0;  // pass 1 (offsets not assigned yet)
         return hot_index[static_cast<size_t>(slot)] * unit;
     }
     int dep_slot(int slot) const {
-        if (slot >= 0 && cls[static_cast<size_t>(slot)] == kContrib) return contrib_h[static_cast<size_t>(slot)];
+        if (slot >= 0 && slot < s.extent && cls[static_cast<size_t>(slot)] == kContrib) return contrib_h[static_cast<size_t>(slot)];
+        if (slot >= 0 && slot < s.extent && cls[static_cast<size_t>(slot)] == kAlias) return alias_of.at(slot);
         return slot;
     }
     int lu_l(int k) const { return l_base_smem >= 0 ? (l_base_smem + k) * unit : s.l + k; }
@@ -238,6 +248,7 @@ struct Gen {
     }
     std::string R(int slot) const {
         if (slot < 0) return "(0.0)";
+        if (cls[static_cast<size_t>(slot)] == kAlias) return R(alias_of.at(slot));
         if (cls[static_cast<size_t>(slot)] == kDerived) {
             const int k = derived_const[static_cast<size_t>(slot)];
             return k < 0 ? std::string("(0.0)") : C(k);
@@ -339,6 +350,9 @@ struct Gen {
         mark_range(s.u, static_cast<int>(s.u_col.size()));
         mark_range(s.scratch, s.dim);
         if (s.fcount >= 0) cls[static_cast<size_t>(s.fcount)] = kSolver;
+        for (const auto& kv : alias_of) {
+            cls[static_cast<size_t>(kv.first)] = kAlias;
+        }
         for (const Proc& p : s.procs) {
             // Norton outputs that are constants every pass (exec.cpp:85-150)
             if (p.code < kNortonSwitch && p.out >= 0) {
@@ -497,6 +511,10 @@ struct Gen {
                 t.kind = p.code == kCtlIntegrator ? K_INTEG : p.code == kCtlFirstOrderLag ? K_LAG : K_PI;
                 reads(t, {IN(0), p.state, p.state + 1});
                 t.writes = {p.state, p.state + 1, p.out};
+                if (p.out >= 0 && alias_of.count(p.out)) {
+                    t.writes = {p.state, p.state + 1};
+                    t.out_alias = true;
+                }
                 t.f = {off(p.out), off(IN(0)), off(p.state), off(p.state + 1), NEG(0)};
                 t.ck = {p.par};
                 if (p.code != kCtlIntegrator) t.ck.push_back(p.par + 1);
@@ -1194,6 +1212,9 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         else if (t.kind == K_CAP) o << "const double hn = -ip - g * vs; ";
         else o << "const double d = " << c.cst(t.ck[1]) << "; const double hn = d * ip + g * vs; ";
         o << "ST(" << h << ", hn);";
+    } else if (t.out_alias && (t.kind == K_INTEG || t.kind == K_LAG)) {
+        o << expand_lit(kCode[t.kind].loads, t, c) << " " << expand_lit(kCode[t.kind].compute, t, c) << " "
+          << expand_lit("ST({I2}, y@); ST({I3}, u@);", t, c);
     } else if (kCode[t.kind].loads != nullptr) {
         o << expand_lit(kCode[t.kind].loads, t, c) << " " << expand_lit(kCode[t.kind].compute, t, c) << " "
           << expand_lit(kCode[t.kind].store, t, c);
@@ -1362,6 +1383,37 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     if (facts != 1) {
         fail = {13, "", "schedule must hold exactly one FactorizeSystem process"};
         return false;
+    }
+    if (knob("EMTB200_CG_ALIAS", 1) && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0) {
+        // output == state0 aliasing: only when the block is the slot's sole writer and no
+        // task reads the output before the block runs in a pass (so the initial value of
+        // the output slot is never observed); channels / latches read it at pass end
+        std::map<int, int> cand, writer_count, first_writer;
+        for (size_t i = 0; i < g.tasks.size(); ++i) {
+            for (int w : g.tasks[i].writes) {
+                writer_count[w] += 1;
+                if (!first_writer.count(w)) first_writer[w] = static_cast<int>(i);
+            }
+        }
+        for (const Proc& p : s.procs)
+            if ((p.code == kCtlIntegrator || p.code == kCtlFirstOrderLag) && p.out >= 0 && p.state >= 0)
+                cand[p.out] = p.state;
+        for (size_t i = 0; i < g.tasks.size(); ++i)
+            for (int r : g.tasks[i].reads) {
+                auto it = cand.find(r);
+                if (it != cand.end() && (!first_writer.count(r) || static_cast<int>(i) <= first_writer[r])) cand.erase(it);
+            }
+        std::set<int> forbidden(s.watch.begin(), s.watch.end());
+        forbidden.insert(s.mentry_slot.begin(), s.mentry_slot.end());
+        for (auto it = cand.begin(); it != cand.end();) {
+            if (writer_count[it->first] != 1 || forbidden.count(it->first)) it = cand.erase(it);
+            else ++it;
+        }
+        if (!cand.empty()) {
+            g.alias_of = cand;
+            g.classify();
+            g.emit_all(facts);
+        }
     }
     bool lu_smem = false;
     size_t smem = 0;
