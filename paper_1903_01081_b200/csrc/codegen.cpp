@@ -1879,7 +1879,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     carr_i("__device__ const", "kConSlot", cslot);
     carr_i("__device__ const", "kConHot", chot);
     carr_i("__device__ const", "kConSign", csign);
-    o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
+    // warps reach their phase barriers at different instructions: the non-.aligned
+    // barrier form is the one the PTX ISA allows there (compute-sanitizer synccheck clean)
+    if (knob("EMTB200_CG_ALIGNEDBAR", 0)) o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
+    else o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
     if (knob("EMTB200_CG_FAKECOS", 0)) o << "#define cos(x) (x)\n";  // timing experiment only: wrong numerics
     o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
@@ -2359,7 +2362,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
     garr("kConHot", chot);
     garr("kConSign", csign);
     garr("kChgSlot", g.chg_flag ? g.chg_slots : std::vector<int>());
-    o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n"
+    o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n"
       << "#define RI(n) __ldg(kRec + rb + (n) * 32)\n";
     std::string refac = g.emit_refactor();
     for (size_t pos; (pos = refac.find("needS[lane]")) != std::string::npos;) refac.replace(pos, 11, "needS[0]");

@@ -170,7 +170,10 @@ bool jit_load(const std::string& source, const std::string& entry, int device, J
         log = "cuModuleLoadData failed";
         return false;
     }
-    if (d->ModuleGetFunction(&out.function2, out.module, "emt_src_kernel") != CUDA_SUCCESS) out.function2 = nullptr;
+    out.function2 = nullptr;
+    if (source.find("emt_src_kernel") != std::string::npos &&
+        d->ModuleGetFunction(&out.function2, out.module, "emt_src_kernel") != CUDA_SUCCESS)
+        out.function2 = nullptr;
     if (d->ModuleGetFunction(&out.function, out.module, entry.c_str()) != CUDA_SUCCESS) {
         log = "cuModuleGetFunction failed for " + entry;
         return false;
