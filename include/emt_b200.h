@@ -200,6 +200,24 @@ emt_status emt_engine_attach_ring(emt_engine* engine, void* device_ptr);
  * 2p+1 = the barrier wait after it, numbered region by region. */
 emt_status emt_engine_profile(emt_engine* engine, int64_t* cycles, int32_t n);
 
+/* Device-side exchange for a line-split system over several engines / GPUs:
+ * every engine of the system attaches the SAME mirror (lanes x cols doubles,
+ * lane-major, see emt_engine_ring) and the SAME progress array (total_ctas
+ * uint32), this engine's CTAs being [cta_offset, cta_offset + ceil(lanes/32)).
+ * Each engine then runs its launches persistently: its CTAs write their
+ * line-end histories straight into the shared mirror and wait on every CTA's
+ * progress word (K-1 passes of slack), so no host exchange is needed. With
+ * system_scope != 0 the acquire/release and ring reads are system-scoped, for
+ * peers on other GPUs (memory from emt_ipc_alloc / emt_ipc_open over NVLink).
+ * All engines' launches must be resident together. */
+emt_status emt_engine_attach_lines(emt_engine* engine, void* mirror, void* progress, int32_t cta_offset,
+                                   int32_t total_ctas, int32_t system_scope);
+/* CUDA IPC helpers for the shared mirror / progress arrays: `handle` is 64 bytes. */
+emt_status emt_ipc_alloc(int32_t device, int64_t bytes, void** ptr, void* handle);
+emt_status emt_ipc_open(int32_t device, const void* handle, void** ptr);
+emt_status emt_ipc_close(void* ptr);
+emt_status emt_ipc_free(void* ptr);
+
 /* Host copies of recorded rows [row0, row0+rows) (WaveformSet layout, this
  * engine's lanes only) and their times. */
 emt_status emt_engine_read_waves(emt_engine* engine, int32_t row0, int32_t rows, double* waves,

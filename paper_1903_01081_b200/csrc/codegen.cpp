@@ -1079,8 +1079,8 @@ const KindCode kCode[K_NKINDS] = {
              "const long long pl@ = (long long)({C4}); const long long pr@ = (long long)({C5}) - a.ring_lo;",
              "const double be@ = y2@ * vs@ + hp@; int q1@ = (step + 1 - K@) % {I4}; if (q1@ < 0) q1@ += {I4}; "
              "const int q0@ = q1@ == 0 ? {I4} - 1 : q1@ - 1; "
-             "const double b1@ = __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q1@); "
-             "const double b0@ = __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q0@); "
+             "const double b1@ = a.sys_scope ? __ldcv(a.ring + pl@ * a.ring_cols + pr@ + q1@) : __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q1@); "
+             "const double b0@ = a.sys_scope ? __ldcv(a.ring + pl@ * a.ring_cols + pr@ + q0@) : __ldcg(a.ring + pl@ * a.ring_cols + pr@ + q0@); "
              "const double h@ = -(c1@ * b1@ + c0@ * b0@);",
              "ST({I2}, h@); if (live) { const int w@ = step % {I4}; A[(size_t)({I3} + w@) * W_] = be@; "
              "a.ring[(LB_ + gl) * a.ring_cols + ({I3} - a.ring_lo) + w@] = be@; }"},
@@ -1840,7 +1840,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab;\n"
+      << "  int prog_off; int sys_scope; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -1887,7 +1888,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
-    o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + blockIdx.x, 0x3fffffffu); } while (0)\n";
+    o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + a.prog_off + blockIdx.x, 0x3fffffffu); } while (0)\n";
     o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
       << "#define ST(o, v) (*(double*)(Sb + (o)) = (v))\n"
       << "#define SGN(x, n) ((n) ? -(x) : (x))\n";
@@ -1963,7 +1964,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "        const long long t0 = clock64(); int m;\n"
       << "        for (;;) {\n"
       << "          m = 0x7fffffff;\n"
-      << "          for (int c = 0; c < a.nblocks; ++c) { unsigned int v; asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
+      << "          for (int c = 0; c < a.nblocks; ++c) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
       << "          if (m >= step + 2 - a.min_k) break;\n"
       << "          if (clock64() - t0 > 8000000000LL) { m = -1; break; }\n"
       << "        }\n"
@@ -2021,7 +2022,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o      << "    }\n"
       << "    if (a.progress != nullptr && threadIdx.x == 0) {\n"
       << "      __threadfence();\n"
-      << "      asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\");\n"
+      << "      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\"); }\n"
+      << "      else asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\");\n"
       << "    }\n"
       << "  }\n";
     // save the resident state back to the arena (+ slots derived from it)
@@ -2333,7 +2335,8 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
-      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab; };\n";
+      << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab;\n"
+      << "  int prog_off; int sys_scope; };\n";
     auto garr = [&](const char* name, const std::vector<int>& v) {
         o << "__device__ const int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];

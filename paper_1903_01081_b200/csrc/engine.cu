@@ -59,6 +59,8 @@ struct CgArgs {
     int min_k, nblocks;
     long long* prof;         // phase profiler accumulators (EMTB200_CG_PROF=1), else null
     const double* srctab;    // this launch's AC source values [pass][source] (emt_src_kernel)
+    int prog_off;            // this engine's first CTA in the (possibly shared) progress array
+    int sys_scope;           // 1: peers on other GPUs (system-scope acquire/release, uncached ring reads)
 };
 
 struct DevPlan {
@@ -489,6 +491,9 @@ struct emt_engine {
     double* d_ring = nullptr;   // line-end history mirror (owned unless attached)
     bool ring_owned = true;
     unsigned int* d_progress = nullptr;  // persistent line-coupled mode: per-CTA pass counters
+    bool progress_owned = true;
+    int prog_off = 0, prog_total = 0;    // shared progress array (emt_engine_attach_lines)
+    int sys_scope = 0;
     long long* d_prof = nullptr;         // 32 warps x 64 markers of cycle sums (profiling builds)
     double* d_srctab = nullptr;          // per-launch AC source table (gen.nsrc columns)
     size_t srctab_cap = 0;               // doubles
@@ -510,7 +515,7 @@ struct emt_engine {
         if (jit.module && driver()) driver()->ModuleUnload(jit.module);
         for (void* p : allocations) cudaFree(p);
         if (d_ring && ring_owned) cudaFree(d_ring);
-        if (d_progress) cudaFree(d_progress);
+        if (d_progress && progress_owned) cudaFree(d_progress);
         if (d_prof) cudaFree(d_prof);
         if (d_srctab) cudaFree(d_srctab);
         if (d_waves) cudaFree(d_waves);
@@ -1001,8 +1006,9 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         CgArgs a{e->plan.arena, e->plan.ctab, e->d_waves, e->d_refactored, reinterpret_cast<int*>(e->plan.lane_err),
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
-                 e->persistent_lines ? e->d_progress : nullptr, e->min_k, static_cast<int>((e->W + 31) / 32), e->d_prof,
-                 e->d_srctab};
+                 e->persistent_lines ? e->d_progress : nullptr, e->min_k,
+                 e->prog_total > 0 ? e->prog_total : static_cast<int>((e->W + 31) / 32), e->d_prof, e->d_srctab,
+                 e->prog_off, e->sys_scope};
         if (e->gen.nsrc > 0 && e->jit.function2 != nullptr) {  // the launch's source value table first
             const size_t need = static_cast<size_t>(steps) * e->gen.nsrc;
             if (need > e->srctab_cap) {
@@ -1217,7 +1223,7 @@ emt_status emt_engine_commit(emt_engine* e) {
     CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
     CUDA_TRY(cudaMemsetAsync(e->plan.n_events, 0, sizeof(int), e->stream));
     if (e->d_progress)
-        CUDA_TRY(cudaMemsetAsync(e->d_progress, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32), e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_progress + e->prog_off, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32), e->stream));
     if (e->d_refactored) CUDA_TRY(cudaMemsetAsync(e->d_refactored, 0, static_cast<size_t>(std::max(1, e->capacity)), e->stream));
     e->step = 0;
     e->rows = 0;
@@ -1250,6 +1256,70 @@ emt_status emt_engine_ring(emt_engine* e, void** device_ptr, int32_t* lanes, int
     if (lanes) *lanes = e->plan.ring ? e->width : 0;
     if (cols) *cols = e->plan.ring_cols;
     if (max_chunk) *max_chunk = e->persistent_lines ? e->min_k - 1 : (e->max_chunk == INT_MAX ? 0 : e->max_chunk);
+    return EMT_OK;
+}
+
+emt_status emt_engine_attach_lines(emt_engine* e, void* mirror, void* progress, int32_t cta_offset, int32_t total_ctas,
+                                   int32_t system_scope) {
+    if (e == nullptr || mirror == nullptr || progress == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    if (e->plan.ring == nullptr) return set_error(EMT_NON_POSITIVE_INPUT, "schedule has no line ends");
+    if (e->kernel_mode != EMT_KERNEL_SPECIALISED)
+        return set_error(EMT_NON_POSITIVE_INPUT, "device-side line exchange needs the specialised kernel");
+    const int nctas = (e->W + 31) / 32;
+    if (cta_offset < 0 || total_ctas < cta_offset + nctas) return set_error(EMT_NON_POSITIVE_INPUT, "progress range");
+    CUDA_TRY(cudaSetDevice(e->device));
+    CUDA_TRY(cudaStreamSynchronize(e->stream));
+    // this engine's rows of the current mirror (the initial histories) into the shared one
+    const size_t cols = static_cast<size_t>(e->plan.ring_cols);
+    CUDA_TRY(cudaMemcpy(static_cast<double*>(mirror) + static_cast<size_t>(e->lane_begin) * cols,
+                        e->plan.ring + static_cast<size_t>(e->lane_begin) * cols, static_cast<size_t>(e->W) * cols * sizeof(double),
+                        cudaMemcpyDefault));
+    CUDA_TRY(cudaMemset(static_cast<unsigned int*>(progress) + cta_offset, 0, sizeof(unsigned int) * static_cast<size_t>(nctas)));
+    if (e->ring_owned && e->d_ring) cudaFree(e->d_ring);
+    e->d_ring = static_cast<double*>(mirror);
+    e->ring_owned = false;
+    e->plan.ring = e->d_ring;
+    if (e->d_progress && e->progress_owned) cudaFree(e->d_progress);
+    e->d_progress = static_cast<unsigned int*>(progress);
+    e->progress_owned = false;
+    if (!e->persistent_lines) {
+        e->min_k = e->max_chunk + 1;
+        e->max_chunk = INT_MAX;
+        e->persistent_lines = true;
+    }
+    e->prog_off = cta_offset;
+    e->prog_total = total_ctas;
+    e->sys_scope = system_scope ? 1 : 0;
+    return EMT_OK;
+}
+
+emt_status emt_ipc_alloc(int32_t device, int64_t bytes, void** ptr, void* handle) {
+    if (ptr == nullptr || handle == nullptr || bytes <= 0) return set_error(EMT_INVALID_HANDLE, "null argument");
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaMalloc(ptr, static_cast<size_t>(bytes)));
+    CUDA_TRY(cudaMemset(*ptr, 0, static_cast<size_t>(bytes)));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, *ptr));
+    std::memcpy(handle, &h, sizeof h);
+    return EMT_OK;
+}
+
+emt_status emt_ipc_open(int32_t device, const void* handle, void** ptr) {
+    if (ptr == nullptr || handle == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return EMT_OK;
+}
+
+emt_status emt_ipc_close(void* ptr) {
+    CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return EMT_OK;
+}
+
+emt_status emt_ipc_free(void* ptr) {
+    CUDA_TRY(cudaFree(ptr));
     return EMT_OK;
 }
 

@@ -119,6 +119,11 @@ def lib():
         L.emt_engine_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]
         L.emt_engine_ring.argtypes = [vp, ctypes.POINTER(vp), ip, ip, ip]
         L.emt_engine_attach_ring.argtypes = [vp, vp]
+        L.emt_engine_attach_lines.argtypes = [vp, vp, vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]
+        L.emt_ipc_alloc.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(vp), ctypes.c_char_p]
+        L.emt_ipc_open.argtypes = [ctypes.c_int32, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.emt_ipc_close.argtypes = [vp]
+        L.emt_ipc_free.argtypes = [vp]
         L.emt_engine_kernel.argtypes = [vp]
         L.emt_engine_kernel.restype = ctypes.c_int32
         L.emt_engine_source.argtypes = [vp]
@@ -139,6 +144,7 @@ EXPORTED_SYMBOLS = [
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
+    "emt_engine_attach_lines", "emt_ipc_alloc", "emt_ipc_open", "emt_ipc_close", "emt_ipc_free",
 ]
 
 
@@ -211,6 +217,20 @@ def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per
     c.device, c.lane_begin, c.lane_count, c.lanes_per_block = device, lane_begin, lane_count, lanes_per_block
     c.warps_per_group, c.kernel, c.flags = warps, kernel, flags
     return c
+
+
+def ipc_alloc(device: int, nbytes: int):
+    """(device pointer, 64-byte IPC handle) of a zeroed allocation shareable with other processes."""
+    p = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(64)
+    _check(lib().emt_ipc_alloc(int(device), int(nbytes), ctypes.byref(p), h))
+    return int(p.value), bytes(h.raw)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    _check(lib().emt_ipc_open(int(device), handle, ctypes.byref(p)))
+    return int(p.value)
 
 
 def codegen(schedule: str, const_table: Optional[np.ndarray] = None, width: int = 0, warps: int = 4,
@@ -351,6 +371,12 @@ class Engine:
     def wait(self) -> None:
         _check(lib().emt_engine_wait(self._h))
         self._async_out = None
+
+    def attach_lines(self, mirror_ptr: int, progress_ptr: int, cta_offset: int, total_ctas: int,
+                     system_scope: bool = False) -> None:
+        """Device-side line exchange with other engines sharing `mirror` / `progress` (emt_engine_attach_lines)."""
+        _check(lib().emt_engine_attach_lines(self._h, ctypes.c_void_p(mirror_ptr), ctypes.c_void_p(progress_ptr),
+                                             int(cta_offset), int(total_ctas), 1 if system_scope else 0))
 
     def sync(self) -> None:
         _check(lib().emt_engine_sync(self._h))

@@ -197,3 +197,40 @@ def test_line_split_shards_with_ring_exchange_equal_one_engine(kernel):
         nch = len(e.channel_names)
         for c in range(nch):
             assert bitwise_equal(got[:, c * (hi - lo):(c + 1) * (hi - lo)], want[:, c * 40 + lo:c * 40 + hi])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("system_scope", [False, True])
+def test_line_split_device_exchange_equals_one_engine(system_scope):
+    """Two lane-shard engines sharing one mirror + progress array (the multi-GPU layout,
+    here both on one device) run concurrently with no host exchange == one engine."""
+    import torch
+    from paper_1903_01081_b200 import engine
+    b = c4_case(40)
+    whole = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width)
+    whole.reserve(700)
+    whole.advance(700)
+    want = whole.waves().values
+    shards = []
+    for lo, hi in ((0, 24), (24, 40)):
+        e = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width, lane_begin=lo,
+                          lane_count=hi - lo)
+        shards.append((e, lo, hi))
+    _, lanes, cols, _ = shards[0][0].ring()
+    mirror = torch.zeros((lanes, cols), dtype=torch.float64, device="cuda")
+    progress = torch.zeros(2, dtype=torch.int32, device="cuda")
+    for k, (e, lo, hi) in enumerate(shards):
+        e.attach_lines(mirror.data_ptr(), progress.data_ptr(), k, 2, system_scope)
+        e.reserve(700)
+    torch.cuda.synchronize()
+    for e, _, _ in shards:
+        e.advance(350)  # both launches in flight together, synchronised by the progress words
+    for e, _, _ in shards:
+        e.advance(350)
+    for e, _, _ in shards:
+        e.sync()
+    for e, lo, hi in shards:
+        got = e.waves().values
+        for c in range(len(e.channel_names)):
+            assert bitwise_equal(got[:, c * (hi - lo):(c + 1) * (hi - lo)], want[:, c * 40 + lo:c * 40 + hi])
+        assert e.stats().kernel_launches <= 4
