@@ -264,7 +264,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             dist.barrier()
             t0 = time.perf_counter()
-            eng.load(init_host, ct_host)
+            runner.reload(init_host, ct_host)
             eng.reserve(S)
             adv(S)
             host_w = eng.waves(0, S).values

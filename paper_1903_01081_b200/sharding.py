@@ -92,14 +92,19 @@ def exchange_rings(dist, mirror, lo: int, hi: int) -> None:
 
 
 class LineSplitShard:
-    """One rank's lanes of a line-coupled batch: an Engine over [lo, hi) whose
-    line-end mirror lives in a torch tensor so collectives can fill peer rows.
+    """One rank's lanes of a line-coupled batch: an Engine over [lo, hi).
 
-    advance(n) runs launches of at most `max_chunk` (= K-1) passes and exchanges
-    the mirror after each one (stream-ordered: engine sync -> collective -> next
-    launch). With world == 1 it is a plain engine advance."""
+    exchange="device" (default with several ranks): rank 0 allocates the
+    line-history mirror and a progress word per CTA of the whole system with
+    CUDA IPC; every rank's engine attaches both (emt_engine_attach_lines) and
+    runs its launches persistently — CTAs write their histories straight into
+    the shared mirror over NVLink and wait on the other ranks' progress words,
+    with no host involvement. exchange="host": launches of at most
+    `max_chunk` (= K-1) passes and a torch.distributed all-gather of the
+    mirror rows after each one. With world == 1 it is a plain engine."""
 
-    def __init__(self, dist, batch, lo: int, hi: int, device: int = 0, **engine_kw):
+    def __init__(self, dist, batch, lo: int, hi: int, device: int = 0, exchange: str = "", **engine_kw):
+        import os
         import torch
         from . import engine
         self.dist, self.lo, self.hi = dist, lo, hi
@@ -107,10 +112,44 @@ class LineSplitShard:
                                  device=device, lane_begin=lo, lane_count=hi - lo, **engine_kw)
         ptr, lanes, cols, self.max_chunk = self.eng.ring()
         self.world = dist.get_world_size() if dist is not None and dist.is_initialized() else 1
+        self.exchange = exchange or os.environ.get("EMTB200_LINE_EXCHANGE", "device")
         self.mirror = None
-        if ptr and self.world > 1:  # peers on other ranks: the collective writes into this buffer
-            self.mirror = torch.zeros((lanes, cols), dtype=torch.float64, device=torch.device("cuda", device))
-            self.eng.attach_ring(self.mirror.data_ptr())
+        self._ipc = []
+        if not ptr or self.world == 1:
+            return
+        if self.exchange == "device" and self.eng.kernel == engine.KERNEL_SPECIALISED:
+            rank = dist.get_rank()
+            spans = [shard_bounds(batch.width, self.world, r) for r in range(self.world)]
+            ctas = [(b - a + 31) // 32 for a, b in spans]
+            total = sum(ctas)
+            offset = sum(ctas[:rank])
+            mb, pb = lanes * cols * 8, total * 4
+            hbuf = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                mptr, mh = engine.ipc_alloc(device, mb)
+                pptr, ph = engine.ipc_alloc(device, pb)
+                self._ipc = [("free", mptr), ("free", pptr)]
+                hbuf[:64] = torch.frombuffer(bytearray(mh), dtype=torch.uint8)
+                hbuf[64:] = torch.frombuffer(bytearray(ph), dtype=torch.uint8)
+            if dist.get_backend() == "nccl":
+                hb = hbuf.cuda(device)
+                dist.broadcast(hb, 0)
+                hbuf = hb.cpu()
+            else:
+                dist.broadcast(hbuf, 0)
+            if rank != 0:
+                raw = bytes(hbuf.numpy().tobytes())
+                mptr = engine.ipc_open(device, raw[:64])
+                pptr = engine.ipc_open(device, raw[64:])
+                self._ipc = [("close", mptr), ("close", pptr)]
+            self.eng.attach_lines(mptr, pptr, offset, total, system_scope=os.environ.get("EMTB200_LINE_SCOPE", "sys") == "sys")
+            dist.barrier()  # every rank's rows and progress words initialised before any launch
+            self.max_chunk = 0
+            return
+        # host exchange: peers' rows arrive by all-gather after every launch of K-1 passes
+        self.exchange = "host"
+        self.mirror = torch.zeros((lanes, cols), dtype=torch.float64, device=torch.device("cuda", device))
+        self.eng.attach_ring(self.mirror.data_ptr())
 
     def advance(self, steps: int) -> None:
         import torch
@@ -125,3 +164,10 @@ class LineSplitShard:
             exchange_rings(self.dist, self.mirror, self.lo, self.hi)
             torch.cuda.current_stream().synchronize()
             done += n
+
+    def reload(self, initial, const_table=None) -> None:
+        """New batch on every rank: reset (own progress words), then a barrier so no
+        rank launches against another rank's stale progress."""
+        self.eng.load(initial, const_table)
+        if self.world > 1:
+            self.dist.barrier()
