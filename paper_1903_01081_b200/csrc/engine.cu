@@ -490,6 +490,7 @@ struct emt_engine {
     int max_chunk = INT_MAX;  // passes per launch; < K when line ends couple lanes across CTAs
     double* d_ring = nullptr;   // line-end history mirror (owned unless attached)
     bool ring_owned = true;
+    bool ring_shared = false;  // mirror shared with other engines (attach_lines): write own rows only
     unsigned int* d_progress = nullptr;  // persistent line-coupled mode: per-CTA pass counters
     bool progress_owned = true;
     int prog_off = 0, prog_total = 0;    // shared progress array (emt_engine_attach_lines)
@@ -1213,10 +1214,14 @@ emt_status emt_engine_commit(emt_engine* e) {
     if (e->staged_ctab)
         CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(e->plan.ctab), e->d_stage_ctab, static_cast<size_t>(s.consts) * W * sizeof(double),
                                  cudaMemcpyDeviceToDevice, e->stream));
-    if (e->plan.ring != nullptr)
-        CUDA_TRY(cudaMemcpyAsync(e->plan.ring, e->d_stage_ring,
-                                 static_cast<size_t>(e->width) * e->plan.ring_cols * sizeof(double), cudaMemcpyDeviceToDevice,
-                                 e->stream));
+    if (e->plan.ring != nullptr) {
+        // an attached (shared) mirror holds other engines' rows too: write only this engine's lanes
+        const size_t cols = static_cast<size_t>(e->plan.ring_cols);
+        const size_t r0 = e->ring_shared ? static_cast<size_t>(e->lane_begin) : 0;
+        const size_t nr = e->ring_shared ? W : static_cast<size_t>(e->width);
+        CUDA_TRY(cudaMemcpyAsync(e->plan.ring + r0 * cols, e->d_stage_ring + r0 * cols, nr * cols * sizeof(double),
+                                 cudaMemcpyDefault, e->stream));
+    }
     CUDA_TRY(cudaEventRecord(e->commit_done, e->stream));
     e->initial_fcount = e->staged_fcount;
     e->base_factor_count = e->staged_base_fc;
@@ -1278,6 +1283,7 @@ emt_status emt_engine_attach_lines(emt_engine* e, void* mirror, void* progress, 
     if (e->ring_owned && e->d_ring) cudaFree(e->d_ring);
     e->d_ring = static_cast<double*>(mirror);
     e->ring_owned = false;
+    e->ring_shared = true;
     e->plan.ring = e->d_ring;
     if (e->d_progress && e->progress_owned) cudaFree(e->d_progress);
     e->d_progress = static_cast<unsigned int*>(progress);

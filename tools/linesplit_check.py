@@ -37,8 +37,7 @@ dt = (time.perf_counter() - t0) / 2000
 if rank == 0:
     print(f"linesplit {mode} {os.environ.get('EMTB200_LINE_SCOPE', 'sys')}: {dt * 1e6:.2f} us/pass", flush=True)
 sh.eng.reserve(steps)
-sh.eng.load(b.initial, b.const_table)
-dist.barrier()
+sh.reload(b.initial, b.const_table)
 sh.advance(steps)
 sh.eng.sync()
 got = torch.from_numpy(sh.eng.waves().values.copy())
