@@ -234,3 +234,24 @@ def test_line_split_device_exchange_equals_one_engine(system_scope):
         for c in range(len(e.channel_names)):
             assert bitwise_equal(got[:, c * (hi - lo):(c + 1) * (hi - lo)], want[:, c * 40 + lo:c * 40 + hi])
         assert e.stats().kernel_launches <= 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["device", "host"])
+def test_line_split_two_processes_bitwise(mode):
+    """Two ranks (torchrun, sharing the one GPU) run a C4 shard each — device mode over a
+    CUDA-IPC mirror + progress array, host mode with all-gathers — and reload once;
+    rank 0 compares both runs with a single engine bit for bit (tools/linesplit_check.py)."""
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, BENCH_SHARE_GPU="1")
+    root = os.path.dirname(GOLDEN.rstrip("/")).rsplit("/tests", 1)[0]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), "tools/linesplit_check.py", mode],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    lines = [l for l in out.stdout.splitlines() if l.startswith("linesplit") and "bitwise" in l]
+    assert lines and "bitwise OK" in lines[-1], out.stdout[-2000:] + out.stderr[-2000:]

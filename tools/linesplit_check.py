@@ -25,15 +25,15 @@ W, steps = 64, 700
 b, _ = bench.build_batch(W, workload="c4")
 lo, hi = sharding.shard_bounds(W, world, rank)
 sh = sharding.LineSplitShard(dist, b, lo, hi, device=dev, exchange=mode)
-sh.eng.reserve(steps + 2000)
+sh.eng.reserve(steps + 200)
 sh.advance(steps)
 sh.eng.sync()
 import time
 dist.barrier()
 t0 = time.perf_counter()
-sh.advance(2000)
+sh.advance(200)
 sh.eng.sync()
-dt = (time.perf_counter() - t0) / 2000
+dt = (time.perf_counter() - t0) / 200
 if rank == 0:
     print(f"linesplit {mode} {os.environ.get('EMTB200_LINE_SCOPE', 'sys')}: {dt * 1e6:.2f} us/pass", flush=True)
 sh.eng.reserve(steps)
