@@ -155,11 +155,13 @@ bool jit_load(const std::string& source, const std::string& entry, int device, J
         std::string parent = cache_dir().substr(0, cache_dir().rfind('/'));
         mkdir(parent.c_str(), 0755);
         mkdir((cache_dir()).c_str(), 0755);
-        std::ofstream f(path + ".tmp", std::ios::binary);
+        // per-process temporary + rename: ranks of one job may compile the same kernel at once
+        const std::string tmp = path + "." + std::to_string(static_cast<long>(getpid())) + ".tmp";
+        std::ofstream f(tmp, std::ios::binary);
         if (f) {
             f.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
             f.close();
-            std::rename((path + ".tmp").c_str(), path.c_str());
+            std::rename(tmp.c_str(), path.c_str());
         }
     }
     {
@@ -167,8 +169,23 @@ bool jit_load(const std::string& source, const std::string& entry, int device, J
         mem_cache()[key] = cubin;
     }
     if (d->ModuleLoadData(&out.module, cubin.data()) != CUDA_SUCCESS) {
-        log = "cuModuleLoadData failed";
-        return false;
+        if (!out.cached) {
+            log = "cuModuleLoadData failed";
+            return false;
+        }
+        // unreadable cache entry: compile afresh
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!jit_compile(source, arch, cubin, log)) return false;
+        out.compile_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out.cached = false;
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            mem_cache()[key] = cubin;
+        }
+        if (d->ModuleLoadData(&out.module, cubin.data()) != CUDA_SUCCESS) {
+            log = "cuModuleLoadData failed";
+            return false;
+        }
     }
     out.function2 = nullptr;
     if (source.find("emt_src_kernel") != std::string::npos &&
