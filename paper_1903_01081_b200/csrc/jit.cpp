@@ -15,6 +15,7 @@
 #include <mutex>
 #include <sstream>
 #include <sys/stat.h>
+#include <unistd.h>
 
 namespace emtb200 {
 
