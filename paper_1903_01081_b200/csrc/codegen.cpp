@@ -1589,6 +1589,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
     bool sw_slim = switch_bits && g.chg_flag && knob("EMTB200_CG_SWSLIM", 1) != 0;
+    const bool sw_gate = knob("EMTB200_CG_SWGATE", 1) != 0;
     {
         std::set<int> sw_slots;
         for (const Task& t : g.tasks)
@@ -1667,6 +1668,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 rc << "    case " << w << ": {\n";
                 std::vector<int> sw_ids;  // process id per swbits bit
                 std::vector<int> sw_tasks;  // task per swbits bit
+                std::string sw_lits;        // gated slim switch tests of this warp
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
                     if (p > 0) rc << mark(prof_base + 2 * static_cast<int>(p) - 2) << "      BAR();\n"
                                   << mark(prof_base + 2 * static_cast<int>(p) - 1);
@@ -1691,9 +1693,27 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                             c.sw_slim = sw_slim;
                             sw_ids.push_back(t.f[3]);
                             sw_tasks.push_back(id);
+                            if (sw_slim && sw_gate) {  // hot path gated below: nothing in the pass reads it
+                                sw_lits += "        " + task_literal(t, c) + "\n";
+                                continue;
+                            }
                         }
                         rc << "      " << task_literal(t, c) << "\n";
                     }
+                }
+                if (!sw_lits.empty()) {
+                    // switches only change state when t reaches one of their toggle times: the
+                    // warp evaluates them on a launch's first pass and when some lane's next
+                    // toggle time is due, and otherwise skips them (their hot path is a no-op)
+                    std::ostringstream nx;
+                    for (int id : sw_tasks) {
+                        const Task& t = g.tasks[static_cast<size_t>(id)];
+                        for (size_t q = 3; q < t.ck.size(); ++q)
+                            nx << " { const double T_ = " << lctx.cst(t.ck[q]) << "; if (T_ > t && T_ < swnext) swnext = T_; }";
+                    }
+                    rc << "      if (__any_sync(0xffffffffu, t >= swnext)) {\n" << sw_lits
+                       << "        swnext = __longlong_as_double(0x7ff0000000000000LL);" << nx.str() << "\n      }\n";
+                    sw_lits.clear();
                 }
                 if (!sw_ids.empty()) {
                     const std::string tab = "kSwIds" + std::to_string(sw_tables.size());
@@ -1949,6 +1969,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  __syncthreads();\n"
       << "  int it = 0;\n"
       << "  long long prof_t = clock64(); (void)prof_t;\n"
+      << "  double swnext = -1.0; (void)swnext;  // per lane: next switch toggle time not yet reached\n"
       << "  const double dlim = a.div_limit; (void)dlim;\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
