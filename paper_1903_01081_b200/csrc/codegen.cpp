@@ -1364,6 +1364,14 @@ std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
+    // scenario lanes per CTA: 32 = one per thread; 16 / 8 (experiment, EMTB200_CG_LPC) leave
+    // the other threads of each warp shadowing lane 0 (same loads and stores, same values)
+    // to shrink shared-memory traffic per instruction and spread the batch over more SMs —
+    // bit-exact, but measured slower (C3 2.81 -> 3.42 / 4.92 ms per 1000 passes)
+    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", 32);
+    if (LPC != 8 && LPC != 16) LPC = 32;
+    g.ls = LPC;
+    g.unit = LPC * 8;
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
     g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;
     g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;
@@ -1371,7 +1379,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 knob("EMTB200_CG_WARPMAJOR", 1) != 0;  // measured 3% slower: moves cos, does not remove it
     g.classify();
     std::vector<double> ginv;
-    if (opt.tensor_solve && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
+    if (opt.tensor_solve && LPC == 32 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && g.shared_g() && g.g_inverse(ginv)) {
         g.dmma = true;
         g.opt.lu_in_smem = false;  // the sweeps are gone; L/U stay in HBM for refactor + state
     }
@@ -1583,7 +1591,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     lctx.dok = dok_mode;
     lctx.cst = [&](int k) -> std::string {
         if (g.invariant(k)) return "kC[" + std::to_string(k) + "]";
-        if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * 256) + ")";
+        if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * g.unit) + ")";
         return "__ldg(C + " + std::to_string(static_cast<long long>(k) * lanes) + ")";
     };
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
@@ -1636,7 +1644,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 const int k = t.ck[static_cast<size_t>(c)];
                 const int m = L.cmode[static_cast<size_t>(c)];
                 if (m == 0) rkd.push_back(g.c0(k));
-                else rec[static_cast<size_t>(L.cpos[static_cast<size_t>(c)])] = m == 2 ? g.vc_index[static_cast<size_t>(k)] * 256 : k;
+                else rec[static_cast<size_t>(L.cpos[static_cast<size_t>(c)])] = m == 2 ? g.vc_index[static_cast<size_t>(k)] * g.unit : k;
             }
             rki.insert(rki.end(), rec.begin(), rec.end());
         }
@@ -1772,6 +1780,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         const std::string code_af = region_code(sa, true);
         code_a = "    if (__builtin_expect(it != 0, 1)) {\n" + code_af + "    } else {\n" + code_a + "    }\n";
     }
+    if (knob("EMTB200_CG_EXP_SKIPA", 0)) code_a = "";  // timing experiment only: wrong numerics
+    if (knob("EMTB200_CG_EXP_SAMEA", 0)) {  // timing experiment only: every warp runs warp 0's region-A code
+        const std::string a0 = region_code(sa, true);
+        const size_t b0 = a0.find("    case 0: {"), c1 = a0.find("    case 1: {", b0);
+        const size_t e0 = a0.rfind("} break;", c1);
+        code_a = "    {\n" + a0.substr(b0 + 13, e0 - b0 - 13) + "    }\n";
+    }
     const std::string code_b = region_code(sb, false);
     const std::string code_c = g.dmma ? region_code(sc3, false) : std::string();
     const size_t const_bytes = rki.size() * 4 + rkd.size() * 8 + static_cast<size_t>(s.consts) * 8;
@@ -1786,7 +1801,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         std::ostringstream pp;
         pp << "  if (warp == 0) { const double tn = (double)(a.step0 + 1) * " << lit(s.dt) << ";\n";
         for (size_t j = 0; j < g.pre_ck.size(); ++j)
-            pp << "    S[" << (g.pre_base + static_cast<int>(j)) * 32 << "] = " << g.C(g.pre_ck[j][0]) << " * cos(" << g.C(g.pre_ck[j][1])
+            pp << "    S[" << (g.pre_base + static_cast<int>(j)) * LPC << "] = " << g.C(g.pre_ck[j][0]) << " * cos(" << g.C(g.pre_ck[j][1])
                << " * tn + " << g.C(g.pre_ck[j][2]) << ");\n";
         pp << "  }\n";
         pre_prologue = pp.str();
@@ -1932,30 +1947,31 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * G << ", 1) emt_cg_kernel(const KArgs a) {\n"
       << "  extern __shared__ double sm[];\n"
       << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
-      << "  const int graw = blockIdx.x * 32 + lane; const bool live = graw < W_;\n"
-      << "  const int gl = live ? graw : (int)(W_ - 1);\n"
-      << "  double* __restrict__ S = sm + lane;\n"
+      << "  const int slane = lane < " << LPC << " ? lane : 0;  // shadow threads mirror lane 0\n"
+      << "  const int graw = blockIdx.x * " << LPC << " + slane; const bool live = lane < " << LPC << " && graw < W_;\n"
+      << "  const int gl = graw < W_ ? graw : (int)(W_ - 1);\n"
+      << "  double* __restrict__ S = sm + slane;\n"
       << "  char* __restrict__ Sb = (char*)S;\n"
-      << "  int* serr = (int*)(sm + " << static_cast<long long>(g.smem_slots()) * 32 << ");\n"
-      << "  int* needS = serr + 32; (void)needS;\n"
+      << "  int* serr = (int*)(sm + " << static_cast<long long>(g.smem_slots()) * LPC << ") + slane - lane;\n"
+      << "  int* needS = serr + " << LPC << "; (void)needS;\n"
       << "  double* __restrict__ A = a.arena + gl;\n"
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
       << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
       << pre_prologue
       << dmma_prologue
-      << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * 32] = __ldg(C + (size_t)kVC[q] * W_);\n"
-      << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * 32] = A[(size_t)kHot[q] * W_];\n";
+      << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * " << LPC << "] = __ldg(C + (size_t)kVC[q] * W_);\n"
+      << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * " << LPC << "] = A[(size_t)kHot[q] * W_];\n";
     if (lu_smem) {
-        o << "  for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * 32] = A[(size_t)("
+        o << "  for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * " << LPC << "] = A[(size_t)("
           << s.l << " + q) * W_];\n";
-        o << "  for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * 32] = A[(size_t)("
+        o << "  for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * " << LPC << "] = A[(size_t)("
           << s.u << " + q) * W_];\n";
         if (g.rcp_base >= 0) {
             std::ostringstream dg;
             for (int i = 0; i < s.dim; ++i) dg << (i ? "," : "") << s.u_row_ptr[static_cast<size_t>(i)];
             o << "  { const int kUd[" << s.dim << "] = {" << dg.str() << "};\n"
-              << "    for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * 32] = 1.0 / A[(size_t)("
+              << "    for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = 1.0 / A[(size_t)("
               << s.u << " + kUd[q]) * W_]; }\n";
         }
     }
@@ -2050,16 +2066,16 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
       << "  if (live) {\n"
-      << "    for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * 32];\n";
+      << "    for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * " << LPC << "];\n";
     if (lu_smem) {
         o << "    for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * W_] = S[("
-          << g.l_base_smem << " + q) * 32];\n";
+          << g.l_base_smem << " + q) * " << LPC << "];\n";
         o << "    for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * W_] = S[("
-          << g.u_base_smem << " + q) * 32];\n";
+          << g.u_base_smem << " + q) * " << LPC << "];\n";
     }
     o << "    if (a.nsteps > 0) {\n"
       << "      for (int q = warp; q < " << dslot.size() << "; q += " << G << ") A[(size_t)kDerSlot[q] * W_] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * W_];\n"
-      << "      for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * 32]; "
+      << "      for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * " << LPC << "]; "
       << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
       << "      for (int q = warp; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << G << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n"
       << "      if (warp == " << (G - 1) << ") {\n" << g.emit_lazy_finalize() << "      }\n"
@@ -2089,6 +2105,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     out.source = o.str();
     out.warps = G;
+    out.lpc = LPC;
     out.smem_bytes = smem;
     out.hot_slots = nhot;
     out.lu_smem = lu_smem ? 1 : 0;
@@ -2098,7 +2115,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     long work = 0;
     for (const Task& t : g.tasks) work += t.cost;
     std::ostringstream sum;
-    sum << (straight ? "straight " : "compact ") << "tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
+    sum << (straight ? "straight " : "compact ") << "lpc=" << LPC << " tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
         << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
         << " est_span=" << static_cast<long>(span_a + span_b + span_c) << " est_work=" << work
         << (g.dmma ? " solve=dmma(G^-1 " + std::to_string(s.dim) + "x" + std::to_string(s.dim) + ")" : std::string(opt.tensor_solve ? " solve=lu(shared-G ineligible)" : ""));

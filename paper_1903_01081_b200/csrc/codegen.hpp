@@ -23,6 +23,7 @@ struct CodegenOptions {
     int mode = 0;                   // 0 auto, 1 straight-line tasks, 2 compact per-type loops
     long long lane_begin = 0;       // first batch lane of the engine (line-end peer lanes are batch indices)
     bool tensor_solve = false;      // shared-G batches: V = G^-1 I on the FP64 tensor cores (not bit-exact)
+    int lanes_per_cta = 0;          // scenario lanes per CTA (32, 16 or 8; 0 = EMTB200_CG_LPC or 32)
 };
 
 struct GeneratedKernel {
@@ -35,6 +36,7 @@ struct GeneratedKernel {
     int phases_a = 0, phases_b = 0;
     int tasks = 0;
     int nsrc = 0;           // AC source values tabulated per launch by emt_src_kernel (srctab)
+    int lpc = 32;           // scenario lanes per CTA of the specialised kernel
     std::string summary;
 };
 

@@ -546,6 +546,12 @@ struct emt_engine {
 
 namespace {
 
+/// CTAs of the specialised kernel: gen.lpc scenario lanes each (32, or 16 / 8)
+int cta_count(const emt_engine* e) {
+    const int lpc = e->gen.lpc > 0 ? e->gen.lpc : 32;
+    return (e->W + lpc - 1) / lpc;
+}
+
 #define EMT_TRY(expr)                          \
     do {                                       \
         emt_status _s = (expr);                \
@@ -925,10 +931,10 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
             const char* pe = std::getenv("EMTB200_LINE_PERSISTENT");
-            if (e->plan.ring != nullptr && e->max_chunk != INT_MAX && (e->W + 31) / 32 <= sms &&
+            if (e->plan.ring != nullptr && e->max_chunk != INT_MAX && cta_count(e.get()) <= sms &&
                 !(pe && std::strcmp(pe, "0") == 0)) {
-                CUDA_TRY(cudaMalloc(&e->d_progress, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32)));
-                CUDA_TRY(cudaMemset(e->d_progress, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32)));
+                CUDA_TRY(cudaMalloc(&e->d_progress, sizeof(unsigned int) * static_cast<size_t>(cta_count(e.get()))));
+                CUDA_TRY(cudaMemset(e->d_progress, 0, sizeof(unsigned int) * static_cast<size_t>(cta_count(e.get()))));
                 e->min_k = e->max_chunk + 1;
                 e->max_chunk = INT_MAX;
                 e->persistent_lines = true;
@@ -1008,7 +1014,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
                  e->plan.events, e->plan.n_events, e->plan.max_events, e->step, steps, e->rows, e->plan.div_limit,
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
                  e->persistent_lines ? e->d_progress : nullptr, e->min_k,
-                 e->prog_total > 0 ? e->prog_total : static_cast<int>((e->W + 31) / 32), e->d_prof, e->d_srctab,
+                 e->prog_total > 0 ? e->prog_total : static_cast<int>(cta_count(e)), e->d_prof, e->d_srctab,
                  e->prog_off, e->sys_scope};
         if (e->gen.nsrc > 0 && e->jit.function2 != nullptr) {  // the launch's source value table first
             const size_t need = static_cast<size_t>(steps) * e->gen.nsrc;
@@ -1030,7 +1036,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         }
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
-        const unsigned grid = static_cast<unsigned>(ts ? e->W : (e->W + 31) / 32);
+        const unsigned grid = static_cast<unsigned>(ts ? e->W : cta_count(e));
         const CUresult r = driver()->LaunchKernel(e->jit.function, grid, 1, 1, static_cast<unsigned>(32 * e->gen.warps), 1, 1,
                                           static_cast<unsigned>(e->gen.smem_bytes), reinterpret_cast<CUstream>(e->stream),
                                           params, nullptr);
@@ -1228,7 +1234,7 @@ emt_status emt_engine_commit(emt_engine* e) {
     CUDA_TRY(cudaMemsetAsync(e->plan.lane_err, 0, W * sizeof(LaneError), e->stream));
     CUDA_TRY(cudaMemsetAsync(e->plan.n_events, 0, sizeof(int), e->stream));
     if (e->d_progress)
-        CUDA_TRY(cudaMemsetAsync(e->d_progress + e->prog_off, 0, sizeof(unsigned int) * static_cast<size_t>((e->W + 31) / 32), e->stream));
+        CUDA_TRY(cudaMemsetAsync(e->d_progress + e->prog_off, 0, sizeof(unsigned int) * static_cast<size_t>(cta_count(e)), e->stream));
     if (e->d_refactored) CUDA_TRY(cudaMemsetAsync(e->d_refactored, 0, static_cast<size_t>(std::max(1, e->capacity)), e->stream));
     e->step = 0;
     e->rows = 0;
@@ -1270,7 +1276,7 @@ emt_status emt_engine_attach_lines(emt_engine* e, void* mirror, void* progress, 
     if (e->plan.ring == nullptr) return set_error(EMT_NON_POSITIVE_INPUT, "schedule has no line ends");
     if (e->kernel_mode != EMT_KERNEL_SPECIALISED)
         return set_error(EMT_NON_POSITIVE_INPUT, "device-side line exchange needs the specialised kernel");
-    const int nctas = (e->W + 31) / 32;
+    const int nctas = cta_count(e);
     if (cta_offset < 0 || total_ctas < cta_offset + nctas) return set_error(EMT_NON_POSITIVE_INPUT, "progress range");
     CUDA_TRY(cudaSetDevice(e->device));
     CUDA_TRY(cudaStreamSynchronize(e->stream));
