@@ -1090,8 +1090,8 @@ const KindCode kCode[K_NKINDS] = {
     /*SRCPRE*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
                "const double v@ = m@ * cos(w@ * tn + p@);", "ST({I0}, v@);"},
     // sources read from the launch's value table (emt_src_kernel computes m*cos(w t + p))
-    /*VSRCT*/ {"const double g@ = {C0}; const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + ({I1} < NSHR_ ? {I1} : NSHR_ + ({I1} - NSHR_) * W_ + gl));", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
-    /*ISRCT*/ {"const double v@ = __ldg(a.srctab + (size_t)it * NSRC_ + ({I1} < NSHR_ ? {I1} : NSHR_ + ({I1} - NSHR_) * W_ + gl));", "", "ST({I0}, v@);"},
+    /*VSRCT*/ {"const double g@ = {C0}; const double v@ = SRCV_({I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
+    /*ISRCT*/ {"const double v@ = SRCV_({I1});", "", "ST({I0}, v@);"},
 };
 
 // Per-segment record layout. Constant field modes: 0 = lane-invariant value in
@@ -1182,11 +1182,11 @@ struct LitCtx {
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
 };
 
-std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
+std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c, const std::string& sfx = "_") {
     std::string out;
     for (const char* p = tpl; p && *p; ++p) {
         if (*p == '@') {
-            out += "_";
+            out += sfx;
         } else if (*p == '{' && (p[1] == 'I' || p[1] == 'C')) {
             const char kind = p[1];
             const char* e = std::strchr(p, '}');
@@ -1198,6 +1198,41 @@ std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c) {
         }
     }
     return out;
+}
+
+/// Loads / compute / store of one task as separate statement strings with
+/// variables suffixed `sfx`, so a batch of independent tasks can issue all of
+/// its shared-memory loads before any compute (the compiler does not hoist
+/// loads over the stores of earlier tasks on its own). False for kinds
+/// without a split form.
+bool task_literal_parts(const Task& t, const LitCtx& c, const std::string& sfx, std::string& ld, std::string& cp,
+                        std::string& st) {
+    if (t.fused && c.fused_pass) {
+        const std::string vb = std::to_string(t.f[1]), va = std::to_string(t.f[0]), h = std::to_string(t.f[3]);
+        ld = "const double vb" + sfx + " = LD(" + vb + "); const double va" + sfx + " = LD(" + va + "); const double hp" + sfx +
+             " = LD(" + h + "); const double g" + sfx + " = " + c.cst(t.ck[0]) + ";";
+        if (t.kind == K_SRL) ld += " const double d" + sfx + " = " + c.cst(t.ck[1]) + ";";
+        cp = "const double vs" + sfx + " = vb" + sfx + " - va" + sfx + "; const double ip" + sfx + " = g" + sfx + " * vs" + sfx +
+             " + hp" + sfx + "; ";
+        if (t.kind == K_IND) cp += "const double hn" + sfx + " = ip" + sfx + " + g" + sfx + " * vs" + sfx + ";";
+        else if (t.kind == K_CAP) cp += "const double hn" + sfx + " = -ip" + sfx + " - g" + sfx + " * vs" + sfx + ";";
+        else cp += "const double hn" + sfx + " = d" + sfx + " * ip" + sfx + " + g" + sfx + " * vs" + sfx + ";";
+        st = "ST(" + h + ", hn" + sfx + ");";
+        return true;
+    }
+    if (t.out_alias) return false;
+    switch (t.kind) {
+        case K_IND: case K_CAP: case K_SRL: case K_VSRCT: case K_ISRCT: case K_CSRC: case K_FINC: case K_FINS:
+        case K_GAIN: case K_LIM: case K_CONST: case K_DELAY: case K_LATCH:
+            break;
+        default:
+            return false;
+    }
+    if (kCode[t.kind].loads == nullptr) return false;
+    ld = expand_lit(kCode[t.kind].loads, t, c, sfx);
+    cp = expand_lit(kCode[t.kind].compute, t, c, sfx);
+    st = expand_lit(kCode[t.kind].store, t, c, sfx);
+    return true;
 }
 
 std::string task_literal(const Task& t, const LitCtx& c) {
@@ -1596,6 +1631,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     };
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
+    // runs of up to batch_max independent tasks emitted loads-first (all loads, then the
+    // arithmetic, then the stores): measured within noise (C3 2.640 -> 2.630 ms), so off
+    const int batch_max = knob("EMTB200_CG_BATCH", 0);
     bool sw_slim = switch_bits && g.chg_flag && knob("EMTB200_CG_SWSLIM", 1) != 0;
     const bool sw_gate = knob("EMTB200_CG_SWGATE", 1) != 0;
     {
@@ -1695,6 +1733,36 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         const Task& t = g.tasks[static_cast<size_t>(id)];
                         LitCtx c = lctx;
                         c.fused_pass = fused_pass;
+                        if (batch_max > 1) {
+                            // gather a run of independent splittable tasks: loads, then computes, then stores
+                            std::vector<std::string> L_, C_, S_;
+                            std::set<int> members;
+                            size_t oj = oi;
+                            while (oj < ordered.size() && static_cast<int>(L_.size()) < batch_max) {
+                                const int idj = ordered[oj];
+                                const Task& tj = g.tasks[static_cast<size_t>(idj)];
+                                if (tj.kind == K_SW) break;
+                                bool dep = false;
+                                for (int d : deps[static_cast<size_t>(idj)]) dep = dep || members.count(d);
+                                if (dep) break;
+                                std::string l1, c1, s1;
+                                if (!task_literal_parts(tj, c, "_" + std::to_string(L_.size()), l1, c1, s1)) break;
+                                L_.push_back(l1);
+                                C_.push_back(c1);
+                                S_.push_back(s1);
+                                members.insert(idj);
+                                ++oj;
+                            }
+                            if (L_.size() >= 2) {
+                                rc << "      {\n";
+                                for (const auto& x : L_) rc << "        " << x << "\n";
+                                for (const auto& x : C_) rc << "        " << x << "\n";
+                                for (const auto& x : S_) rc << "        " << x << "\n";
+                                rc << "      }\n";
+                                oi = oj - 1;
+                                continue;
+                            }
+                        }
                         if (t.kind == K_SW && switch_bits && sw_ids.size() < 64 && t.region == 0) {
                             c.sw_bit = static_cast<int>(sw_ids.size());
                             c.chg_flag = g.chg_flag;
@@ -1861,6 +1929,18 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         dmma_block = blk.str();
         smem += ginv_bytes + 32 * sizeof(int);
     }
+    // AC source values one pass ahead: at the top of a pass the CTA starts async copies
+    // (cp.async) of the next pass's table row (its own columns) into the other half of
+    // a double-buffered shared row, waited for at the end of the pass, so region A
+    // reads shared memory instead of waiting on an L2 load. Measured slower (C3 2.64 ->
+    // 2.75 ms, C4 3.92 -> 4.34 ms per 1000 passes; register-held variant likewise), so off.
+    const int pf_ns = g.tab_shared(), pf_nv = static_cast<int>(g.tab_ck.size()) - pf_ns;
+    const int pf_row = pf_ns + pf_nv * LPC;
+    const size_t pf_off = (smem + 7) / 8;  // doubles
+    const size_t pf_bytes = 2 * static_cast<size_t>(pf_row) * sizeof(double);
+    const bool srcpf = !g.tab_ck.empty() && knob("EMTB200_CG_SRCPF", 0) != 0 &&
+                       pf_off * 8 + pf_bytes <= opt.smem_budget;
+    if (srcpf) smem = pf_off * 8 + pf_bytes;
     // ---- source
     std::ostringstream o;
     const int nhot = static_cast<int>(g.hot_slots.size());
@@ -1871,6 +1951,16 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         const int ns = g.tab_shared(), nv = static_cast<int>(g.tab_ck.size()) - g.tab_shared();
         o << "#define NSHR_ " << ns << "\n#define NSRC_ " << std::max<long long>(1, ns + static_cast<long long>(nv) * lanes) << "LL\n";
         out.nsrc = static_cast<int>(std::max<long long>(0, ns + static_cast<long long>(nv) * lanes));
+        if (srcpf) {
+            o << "#define NSRCL_ " << pf_row << "\n"
+              << "#define SRCV_(j) ((j) < NSHR_ ? s_pf[(it & 1) * NSRCL_ + (j)] : s_pf[(it & 1) * NSRCL_ + NSHR_ + ((j) - NSHR_) * "
+              << LPC << " + slane])\n"
+              // global table column of element q of this CTA's row
+              << "#define PFCOL_(q) ((q) < NSHR_ ? (long long)(q) : NSHR_ + (long long)(((q) - NSHR_) / " << LPC << ") * W_ + "
+              << "min((long long)blockIdx.x * " << LPC << " + ((q) - NSHR_) % " << LPC << ", W_ - 1))\n";
+        } else {
+            o << "#define SRCV_(j) __ldg(a.srctab + (size_t)it * NSRC_ + ((j) < NSHR_ ? (j) : NSHR_ + ((j) - NSHR_) * W_ + gl))\n";
+        }
     }
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
@@ -1980,6 +2070,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (const Task& t : g.tasks)
         if (t.region == 0)
             for (int w : t.writes) written_a.insert(w);
+    if (srcpf)
+        o << "  double* __restrict__ s_pf = sm + " << pf_off << ";\n"
+          << "  if (a.nsteps > 0) for (int q = threadIdx.x; q < NSRCL_; q += " << 32 * G << ") s_pf[q] = __ldg(a.srctab + PFCOL_(q));\n";
     o << "  __shared__ int s_cmin;\n"
       << "  if (threadIdx.x == 0) s_cmin = -0x3fffffff;\n"
       << "  __syncthreads();\n"
@@ -2015,6 +2108,12 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
     o << "}\n";
+    if (srcpf) {  // next pass's row: an async global->shared copy (no registers held across the pass)
+        o << "    if (it + 1 < a.nsteps) for (int q = threadIdx.x; q < NSRCL_; q += " << 32 * G << ") {\n"
+          << "      const unsigned int d = (unsigned int)__cvta_generic_to_shared(s_pf + ((it + 1) & 1) * NSRCL_ + q);\n"
+          << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(d), \"l\"(a.srctab + (size_t)(it + 1) * NSRC_ + PFCOL_(q)) : \"memory\");\n"
+          << "    }\n";
+    }
     o << code_a;
     o << "    if (__syncthreads_or(wflag)) {\n"
       << "      if (warp == 0) {\n"
@@ -2028,6 +2127,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      }\n"
       << "    }\n";
     o << code_b << dmma_block << code_c;
+    if (srcpf)  // the pass-end barrier below orders the copies before the next pass's reads
+        o << "    asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
     if (dok_mode) {
         // divergence (exec.cpp:229-237): rows only AND a NaN-safe predicate; the
         // failing node index (the lowest) is found in the cold path
