@@ -1180,6 +1180,7 @@ struct LitCtx {
     bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
     std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
+    bool zterm = false;                    // drop zero-slot terms from sums
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c, const std::string& sfx = "_") {
@@ -1254,8 +1255,12 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         o << expand_lit(kCode[t.kind].loads, t, c) << " " << expand_lit(kCode[t.kind].compute, t, c) << " "
           << expand_lit(kCode[t.kind].store, t, c);
     } else if (t.kind == K_GATHER || t.kind == K_SUM) {
+        // terms read from the zero slot (resistor h, ground) are dropped: acc starts at +0.0
+        // and an IEEE sum is -0 only when both addends are -0, so acc is never -0 and
+        // acc + (+-0) == acc bit for bit
         o << "double acc = 0.0; ";
-        for (const auto& tm : t.terms) o << "acc = acc + " << (tm.second ? "-" : "") << "LD(" << tm.first << "); ";
+        for (const auto& tm : t.terms)
+            if (tm.first != 0 || !c.zterm) o << "acc = acc + " << (tm.second ? "-" : "") << "LD(" << tm.first << "); ";
         o << "ST(" << t.f[0] << ", acc);";
     } else if (t.kind == K_FWD || t.kind == K_BWD) {
         o << "double x = LD(" << t.f[0] << "); ";
@@ -1629,6 +1634,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * g.unit) + ")";
         return "__ldg(C + " + std::to_string(static_cast<long long>(k) * lanes) + ")";
     };
+    // zero slot (S[0] = +0.0, never written): sums skip it and other reads become the
+    // literal, removing a shared load from each ground-side branch voltage
+    const int zmode = knob("EMTB200_CG_ZTERM", 1);  // 1: sums skip it, 2: also literal reads
+    const bool zterm = straight && zmode != 0;
+    lctx.zterm = zterm;
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
     // runs of up to batch_max independent tasks emitted loads-first (all loads, then the
@@ -2205,6 +2215,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         o << "  }\n  tab[i] = v;\n}\n";
     }
     out.source = o.str();
+    if (zterm && zmode == 2)
+        for (size_t q = out.source.find("LD(0)"); q != std::string::npos; q = out.source.find("LD(0)", q + 5))
+            out.source.replace(q, 5, "(0.0)");
     out.warps = G;
     out.lpc = LPC;
     out.smem_bytes = smem;
