@@ -1401,6 +1401,32 @@ std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
 
 }  // namespace
 
+// Straight-line launch prologue/epilogue copies: per warp, items q = warp (mod G) in
+// groups whose loads issue back to back (a loop over an index table serialises a table
+// load and the dependent arena load per slot: ~35 us per launch on C3).
+static std::string warp_copies(const std::vector<std::pair<std::string, std::string>>& items, int G,
+                               const std::string& ind, int group = 16) {
+    if (items.empty()) return std::string();
+    std::ostringstream o;
+    o << ind << "switch (warp) {\n";
+    for (int w = 0; w < G; ++w) {
+        std::vector<size_t> mine;
+        for (size_t q = static_cast<size_t>(w); q < items.size(); q += static_cast<size_t>(G)) mine.push_back(q);
+        if (mine.empty()) continue;
+        o << ind << "case " << w << ": {\n";
+        for (size_t g0 = 0; g0 < mine.size(); g0 += static_cast<size_t>(group)) {
+            const size_t g1 = std::min(mine.size(), g0 + static_cast<size_t>(group));
+            o << ind << "  { ";
+            for (size_t j = g0; j < g1; ++j) o << "const double t" << j - g0 << " = " << items[mine[j]].second << "; ";
+            for (size_t j = g0; j < g1; ++j) o << items[mine[j]].first << " = t" << j - g0 << "; ";
+            o << "}\n";
+        }
+        o << ind << "} break;\n";
+    }
+    o << ind << "}\n";
+    return o.str();
+}
+
 bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                      GeneratedKernel& out, Failure& fail) {
     Gen g(s, ctab, lanes, opt);
@@ -2060,18 +2086,48 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
       << pre_prologue
       << dmma_prologue
-      << "  for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * " << LPC << "] = __ldg(C + (size_t)kVC[q] * W_);\n"
-      << "  for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * " << LPC << "] = A[(size_t)kHot[q] * W_];\n";
-    if (lu_smem) {
-        o << "  for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * " << LPC << "] = A[(size_t)("
+;
+    const bool slcopy = knob("EMTB200_CG_SLCOPY", 1) != 0;
+    if (slcopy) {
+        std::vector<std::pair<std::string, std::string>> it;
+        for (size_t q = 0; q < g.vc_slots.size(); ++q)
+            it.push_back({"S[" + std::to_string((g.vc_base + static_cast<long long>(q)) * LPC) + "]",
+                          "__ldg(C + (size_t)" + std::to_string(g.vc_slots[q]) + " * W_)"});
+        for (int q = 0; q + 1 < nhot; ++q)
+            it.push_back({"S[" + std::to_string(static_cast<long long>(q + 1) * LPC) + "]",
+                          "A[(size_t)" + std::to_string(g.hot_slots[static_cast<size_t>(q) + 1]) + " * W_]"});
+        o << warp_copies(it, G, "  ");
+    } else {
+        o << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * " << LPC << "] = __ldg(C + (size_t)kVC[q] * W_);\n"
+          << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * " << LPC << "] = A[(size_t)kHot[q] * W_];\n";
+    }
+    if (lu_smem && slcopy) {
+        std::vector<std::pair<std::string, std::string>> it;
+        for (size_t q = 0; q < s.l_col.size(); ++q)
+            it.push_back({"S[" + std::to_string((g.l_base_smem + static_cast<long long>(q)) * LPC) + "]",
+                          "A[(size_t)" + std::to_string(s.l + static_cast<long long>(q)) + " * W_]"});
+        for (size_t q = 0; q < s.u_col.size(); ++q)
+            it.push_back({"S[" + std::to_string((g.u_base_smem + static_cast<long long>(q)) * LPC) + "]",
+                          "A[(size_t)" + std::to_string(s.u + static_cast<long long>(q)) + " * W_]"});
+        o << warp_copies(it, G, "  ");
+    } else if (lu_smem) {
+        o << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * " << LPC << "] = A[(size_t)("
           << s.l << " + q) * W_];\n";
-        o << "  for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * " << LPC << "] = A[(size_t)("
+        o << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") S[(" << g.u_base_smem << " + q) * " << LPC << "] = A[(size_t)("
           << s.u << " + q) * W_];\n";
-        if (g.rcp_base >= 0) {
+    }
+    if (lu_smem) {
+        if (g.rcp_base >= 0 && slcopy) {
+            std::vector<std::pair<std::string, std::string>> it;
+            for (int i = 0; i < s.dim; ++i)
+                it.push_back({"S[" + std::to_string(static_cast<long long>(g.rcp_base + i) * LPC) + "]",
+                              "1.0 / A[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_]"});
+            o << warp_copies(it, G, "  ");
+        } else if (g.rcp_base >= 0) {
             std::ostringstream dg;
             for (int i = 0; i < s.dim; ++i) dg << (i ? "," : "") << s.u_row_ptr[static_cast<size_t>(i)];
             o << "  { const int kUd[" << s.dim << "] = {" << dg.str() << "};\n"
-              << "    for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = 1.0 / A[(size_t)("
+              << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = 1.0 / A[(size_t)("
               << s.u << " + kUd[q]) * W_]; }\n";
         }
     }
@@ -2177,19 +2233,59 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
       << "  if (live) {\n"
-      << "    for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * " << LPC << "];\n";
+;
+    if (slcopy) {
+        std::vector<std::pair<std::string, std::string>> it;
+        for (int q = 0; q + 1 < nhot; ++q)
+            it.push_back({"A[(size_t)" + std::to_string(g.hot_slots[static_cast<size_t>(q) + 1]) + " * W_]",
+                          "S[" + std::to_string(static_cast<long long>(q + 1) * LPC) + "]"});
+        o << warp_copies(it, G, "    ");
+    } else {
+        o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * " << LPC << "];\n";
+    }
     if (lu_smem) {
-        o << "    for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * W_] = S[("
+        o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * W_] = S[("
           << g.l_base_smem << " + q) * " << LPC << "];\n";
-        o << "    for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * W_] = S[("
+        o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * W_] = S[("
           << g.u_base_smem << " + q) * " << LPC << "];\n";
     }
-    o << "    if (a.nsteps > 0) {\n"
-      << "      for (int q = warp; q < " << dslot.size() << "; q += " << G << ") A[(size_t)kDerSlot[q] * W_] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * W_];\n"
-      << "      for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * " << LPC << "]; "
-      << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
-      << "      for (int q = warp; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << G << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n"
-      << "      if (warp == " << (G - 1) << ") {\n" << g.emit_lazy_finalize() << "      }\n"
+    o << "    if (a.nsteps > 0) {\n";
+    if (slcopy) {
+        std::vector<std::pair<std::string, std::string>> it;
+        for (size_t q = 0; q < dslot.size(); ++q)
+            it.push_back({"A[(size_t)" + std::to_string(dslot[q]) + " * W_]",
+                          dconst[q] < 0 ? std::string("0.0") : "C[(size_t)" + std::to_string(dconst[q]) + " * W_]"});
+        for (size_t q = 0; q < cslot.size(); ++q) {
+            const std::string h = chot[q] < 0 ? std::string("0.0") : "S[" + std::to_string(static_cast<long long>(chot[q]) * LPC) + "]";
+            it.push_back({"A[(size_t)" + std::to_string(cslot[q]) + " * W_]", csign[q] > 0 ? h : "-" + h});
+        }
+        if (g.chg_flag)
+            for (int x : g.chg_slots) it.push_back({"A[(size_t)" + std::to_string(x) + " * W_]", "0.0"});
+        o << warp_copies(it, G, "      ");
+    } else {
+        o << "      _Pragma(\"unroll 8\") for (int q = warp; q < " << dslot.size() << "; q += " << G << ") A[(size_t)kDerSlot[q] * W_] = kDerConst[q] < 0 ? 0.0 : C[(size_t)kDerConst[q] * W_];\n"
+          << "      _Pragma(\"unroll 8\") for (int q = warp; q < " << cslot.size() << "; q += " << G << ") { const double h = kConHot[q] < 0 ? 0.0 : S[kConHot[q] * " << LPC << "]; "
+          << "A[(size_t)kConSlot[q] * W_] = kConSign[q] > 0 ? h : -h; }\n"
+          << "      _Pragma(\"unroll 8\") for (int q = warp; q < " << (g.chg_flag ? g.chg_slots.size() : 0) << "; q += " << G << ") A[(size_t)kChgSlot[q] * W_] = 0.0;\n";
+    }
+    if (slcopy) {  // one independent statement per line: spread over the warps
+        std::vector<std::string> ln;
+        std::istringstream fin(g.emit_lazy_finalize());
+        for (std::string l; std::getline(fin, l);) ln.push_back(l);
+        if (!ln.empty()) {
+            o << "      switch (warp) {\n";
+            for (int w = 0; w < G; ++w) {
+                if (static_cast<size_t>(w) >= ln.size()) break;
+                o << "      case " << w << ": {\n";
+                for (size_t q = static_cast<size_t>(w); q < ln.size(); q += static_cast<size_t>(G)) o << ln[q] << "\n";
+                o << "      } break;\n";
+            }
+            o << "      }\n";
+        }
+    } else {
+        o << "      if (warp == " << (G - 1) << ") {\n" << g.emit_lazy_finalize() << "      }\n";
+    }
+    o
       << "    }\n"
       << "  }\n"
       << "}\n";

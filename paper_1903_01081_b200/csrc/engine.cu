@@ -1215,11 +1215,21 @@ emt_status emt_engine_commit(emt_engine* e) {
     const size_t W = static_cast<size_t>(e->W);
     CUDA_TRY(cudaSetDevice(e->device));
     CUDA_TRY(cudaStreamWaitEvent(e->stream, e->stage_done, 0));
-    CUDA_TRY(cudaMemcpyAsync(e->plan.arena, e->d_stage_arena, static_cast<size_t>(s.extent) * W * sizeof(double),
-                             cudaMemcpyDeviceToDevice, e->stream));
-    if (e->staged_ctab)
-        CUDA_TRY(cudaMemcpyAsync(const_cast<double*>(e->plan.ctab), e->d_stage_ctab, static_cast<size_t>(s.consts) * W * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, e->stream));
+    // the staged buffers become the live ones (no device copy): launches enqueued from
+    // here on read them, and the next stage writes the old ones only after commit_done,
+    // i.e. after every launch that used them
+    auto swap_owned = [e](double*& live, double*& staged) {
+        for (void*& a : e->allocations)
+            if (a == live) a = staged;
+        std::swap(live, staged);
+    };
+    swap_owned(e->plan.arena, e->d_stage_arena);
+    if (e->staged_ctab) {
+        double* ct = const_cast<double*>(e->plan.ctab);
+        swap_owned(ct, e->d_stage_ctab);
+        e->plan.ctab = ct;
+    }
+    (void)s;
     if (e->plan.ring != nullptr) {
         // an attached (shared) mirror holds other engines' rows too: write only this engine's lanes
         const size_t cols = static_cast<size_t>(e->plan.ring_cols);
