@@ -1181,6 +1181,8 @@ struct LitCtx {
     std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
     bool zterm = false;                    // drop zero-slot terms from sums
+    int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
+    std::string* deferred = nullptr;       // hoisted line end: its global stores go here (phase end)
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c, const std::string& sfx = "_") {
@@ -1239,6 +1241,23 @@ bool task_literal_parts(const Task& t, const LitCtx& c, const std::string& sfx, 
 std::string task_literal(const Task& t, const LitCtx& c) {
     std::ostringstream o;
     o << "{ ";
+    if (c.hoist >= 0 && (t.kind == K_VSRCT || t.kind == K_ISRCT)) {
+        const std::string v = "gv" + std::to_string(c.hoist);
+        if (t.kind == K_VSRCT) o << "const double g_ = " << c.cst(t.ck[0]) << "; ST(" << t.f[0] << ", g_ * " << v << "); }";
+        else o << "ST(" << t.f[0] << ", " << v << "); }";
+        return o.str();
+    }
+    if (c.hoist >= 0 && t.kind == K_BERG && c.deferred != nullptr) {
+        // ring values gb1/gb0 loaded at the phase start; be stored to HBM at the phase end
+        const std::string id = std::to_string(c.hoist);
+        o << "const double vs_ = LD(" << t.f[1] << ") - LD(" << t.f[0] << "); const double hp_ = LD(" << t.f[2] << "); gbe" << id
+          << " = " << c.cst(t.ck[0]) << " * vs_ + hp_; ST(" << t.f[2] << ", -(" << c.cst(t.ck[1]) << " * gb1" << id << " + "
+          << c.cst(t.ck[2]) << " * gb0" << id << ")); }";
+        *c.deferred += "      if (live) { const int w_ = step % " + std::to_string(t.f[4]) + "; A[(size_t)(" + std::to_string(t.f[3]) +
+                       " + w_) * W_] = gbe" + id + "; a.ring[(LB_ + gl) * a.ring_cols + (" + std::to_string(t.f[3]) +
+                       " - a.ring_lo) + w_] = gbe" + id + "; }\n";
+        return o.str();
+    }
     if (t.fused && c.fused_pass) {
         // i_prev = g (vb - va) + h as the finalize computed it last pass (exec.cpp:220-228)
         const std::string vb = std::to_string(t.f[1]), va = std::to_string(t.f[0]), h = std::to_string(t.f[3]);
@@ -1670,6 +1689,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // runs of up to batch_max independent tasks emitted loads-first (all loads, then the
     // arithmetic, then the stores): measured within noise (C3 2.640 -> 2.630 ms), so off
     const int batch_max = knob("EMTB200_CG_BATCH", 0);
+    // measured neutral (C4 -0.5%, C2 +1..7%): ptxas already issues these loads early
+    const bool glhoist = knob("EMTB200_CG_GLHOIST", 0) != 0;
     bool sw_slim = switch_bits && g.chg_flag && knob("EMTB200_CG_SWSLIM", 1) != 0;
     const bool sw_gate = knob("EMTB200_CG_SWGATE", 1) != 0;
     {
@@ -1759,6 +1780,29 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                     std::vector<int> seg_of(ordered.size(), -1);
                     for (size_t si = 0; si < segs.size(); ++si)
                         for (int q = 0; q < segs[si].count; ++q) seg_of[static_cast<size_t>(segs[si].first + q)] = static_cast<int>(si);
+                    // global loads (source table, peer line histories) issued at the phase
+                    // start so their L2 latency overlaps the phase's shared-memory work; a line
+                    // end's HBM stores move to the phase end (nothing in the pass reads them)
+                    std::string post;
+                    std::set<int> hoisted;
+                    if (glhoist && loop_min == 0 && batch_max <= 1)
+                        for (int id : ordered) {
+                            const Task& t = g.tasks[static_cast<size_t>(id)];
+                            if (t.kind == K_VSRCT || t.kind == K_ISRCT) {
+                                rc << "      const double gv" << id << " = SRCV_(" << t.f[1] << ");\n";
+                                hoisted.insert(id);
+                            } else if (t.kind == K_BERG) {
+                                const std::string L = std::to_string(t.f[4]);
+                                const std::string at = "a.ring + pl_ * a.ring_cols + pr_ + ";
+                                rc << "      double gb1" << id << ", gb0" << id << ", gbe" << id << "; { const int K_ = (int)(" << lctx.cst(t.ck[3])
+                                   << "); const long long pl_ = (long long)(" << lctx.cst(t.ck[4]) << "); const long long pr_ = (long long)("
+                                   << lctx.cst(t.ck[5]) << ") - a.ring_lo; int q1_ = (step + 1 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
+                                   << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; gb1" << id << " = a.sys_scope ? __ldcv(" << at
+                                   << "q1_) : __ldcg(" << at << "q1_); gb0" << id << " = a.sys_scope ? __ldcv(" << at << "q0_) : __ldcg(" << at
+                                   << "q0_); }\n";
+                                hoisted.insert(id);
+                            }
+                        }
                     for (size_t oi = 0; oi < ordered.size(); ++oi) {
                         const Segment& sg = segs[static_cast<size_t>(seg_of[oi])];
                         if (loop_min > 0 && sg.count >= loop_min && sg.indep && loopable(sg.kind)) {
@@ -1769,6 +1813,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         const Task& t = g.tasks[static_cast<size_t>(id)];
                         LitCtx c = lctx;
                         c.fused_pass = fused_pass;
+                        if (hoisted.count(id)) {
+                            c.hoist = id;
+                            c.deferred = &post;
+                        }
                         if (batch_max > 1) {
                             // gather a run of independent splittable tasks: loads, then computes, then stores
                             std::vector<std::string> L_, C_, S_;
@@ -1812,6 +1860,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         }
                         rc << "      " << task_literal(t, c) << "\n";
                     }
+                    rc << post;
                 }
                 if (!sw_lits.empty()) {
                     // switches only change state when t reaches one of their toggle times: the
@@ -2156,16 +2205,18 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
       << "      __syncthreads();\n"
-      << "      if (threadIdx.x == 0) {\n"
+      // warp 0 polls the progress words in parallel (one acquire round trip, not nblocks)
+      << "      if (warp == 0) {\n"
       << "        const long long t0 = clock64(); int m;\n"
       << "        for (;;) {\n"
       << "          m = 0x7fffffff;\n"
-      << "          for (int c = 0; c < a.nblocks; ++c) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
+      << "          for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
+      << "          m = __reduce_min_sync(0xffffffffu, m);\n"
       << "          if (m >= step + 2 - a.min_k) break;\n"
-      << "          if (clock64() - t0 > 8000000000LL) { m = -1; break; }\n"
+      << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
       << "        }\n"
       << "        __threadfence();\n"
-      << "        s_cmin = m;\n"
+      << "        if (lane == 0) s_cmin = m;\n"
       << "      }\n"
       << "      __syncthreads();\n"
       << "      if (s_cmin < 0) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
