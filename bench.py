@@ -88,6 +88,25 @@ def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3")
     return sch.n1_batch(s, st, ids, scen), sch.parse_info(s)
 
 
+def fp64_gemm_peak(dev) -> float:
+    """Measured FP64 GEMM rate (TFLOP/s) of this GPU: torch.matmul (cuBLAS DGEMM), 8192^3, best of 10."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    c = a @ b
+    best = float("inf")
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    del a, b, c
+    return 2.0 * n ** 3 / best / 1e12
+
+
 def algorithmic_bytes_per_scenario_step(info, batch, shared_g: bool = False) -> float:
     """SURVEY.md §8(d): B = 8 [2 (n + m + S_blk + 2 N_sw + N_latch) + F_lane + C_var + K];
     F_lane = l_nnz + u_nnz for per-lane factors, else 0 plus the shared factor 8 (l+u) / W."""
@@ -391,6 +410,17 @@ def run_ours(args):
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "clocks": clk,
         }
+        if args.tensor_solve and "solve=dmma" in eng.summary:
+            # the batched V = G^-1 I product on the FP64 tensor cores, 2 n^2 flops
+            # per scenario-step, against this GPU's FP64 GEMM rate measured here (cuBLAS DGEMM
+            # 8192^3, best of 10) since MEASURED_PEAKS.json holds no FP64 figure
+            n = info.nodes
+            dflops = 2.0 * n * n * lanes_local * S / avg_launch_s / 1e12
+            dpeak = fp64_gemm_peak(cdev)
+            out["roofline_dmma"] = {"bound": "tensor", "achieved": dflops, "peak": dpeak, "unit": "TFLOP/s",
+                                    "frac": dflops / dpeak, "flops_per_scenario_step": 2.0 * n * n,
+                                    "peak_source": "torch.matmul float64 8192^3 on this GPU, best of 10",
+                                    "note": "the solve is one part of the pass: the kernel as a whole is in 'roofline'"}
         if cpu is not None:
             out["cpu_baseline"] = cpu
         print(json.dumps(out), flush=True)
