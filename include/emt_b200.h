@@ -252,6 +252,20 @@ const char* emt_engine_summary(const emt_engine* engine);
 emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,
                        int32_t compile, const char* arch, const char** source, const char** summary);
 
+/* ---- waveform text (WaveformSet::to_text, proj/src/waveform.cpp:22-42) ---- */
+
+/* Formats `rows` waveform rows as the reference's text form: a header line
+ * "time <name>..." (names "<name>#<lane>" when width > 1), then per row the
+ * time and channels*width values (channel-major, then lane), each as %.17g
+ * (format_g17, proj/src/common.cpp:85-89), space-separated, '\n'-terminated.
+ * Byte-identical to the reference; `threads` host threads format row blocks.
+ * *out is malloc'd (NUL-terminated, *out_len bytes without the NUL); release
+ * it with emt_free. */
+emt_status emt_waves_to_text(const char* const* channel_names, int32_t channels, int32_t width,
+                             const double* time, const double* values, int64_t rows, int32_t threads,
+                             char** out, int64_t* out_len);
+void emt_free(void* ptr);
+
 /* Library build string (arch, flags). */
 const char* emt_version(void);
 

@@ -169,3 +169,20 @@ def apply_overrides(document: str, row) -> str:
     _check(L.emtref_apply_overrides(document.encode(), json.dumps(row).encode(), ctypes.byref(out), err,
                                     len(err)), err)
     return _take_str(out)
+
+
+def waves_text(channels, width: int, time: np.ndarray, values: np.ndarray) -> str:
+    """WaveformSet::to_text (proj/src/waveform.cpp:22-42) of host rows."""
+    L = lib()
+    L.emtref_waves_text.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p, ctypes.c_int]
+    t = np.ascontiguousarray(time, dtype=np.float64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    names = (ctypes.c_char_p * max(1, len(channels)))(*[c.encode() for c in channels])
+    err = ctypes.create_string_buffer(4096)
+    out = ctypes.c_void_p()
+    dp = ctypes.POINTER(ctypes.c_double)
+    _check(L.emtref_waves_text(names, len(channels), int(width), t.ctypes.data_as(dp), v.ctypes.data_as(dp),
+                               int(t.size), ctypes.byref(out), err, len(err)), err)
+    return _take_str(out)

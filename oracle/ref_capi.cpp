@@ -197,4 +197,20 @@ int emtref_apply_overrides(const char* document, const char* row_json, char** ou
     });
 }
 
+/// WaveformSet::to_text of host rows (values: rows x (channels*width), row-major).
+int emtref_waves_text(const char* const* names, int channels, int width, const double* time,
+                      const double* values, int rows, char** out, char* err, int err_len) {
+    return guarded(err, err_len, [&] {
+        WaveformSet w;
+        for (int c = 0; c < channels; ++c) w.channels.emplace_back(names[c]);
+        w.width = width;
+        w.time.assign(time, time + rows);
+        const int cols = channels * width;
+        w.values.resize(rows, cols);
+        for (int r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) w.values(r, c) = values[static_cast<size_t>(r) * cols + c];
+        *out = dup(w.to_text());
+    });
+}
+
 }  // extern "C"

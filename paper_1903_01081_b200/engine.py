@@ -132,6 +132,10 @@ def lib():
         L.emt_engine_summary.restype = ctypes.c_char_p
         L.emt_codegen.argtypes = [ctypes.c_char_p, dp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                   ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_char_p)]
+        L.emt_waves_to_text.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int32, ctypes.c_int32, dp, dp,
+                                        ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int64)]
+        L.emt_free.argtypes = [vp]
+        L.emt_free.restype = None
         _lib = L
     return _lib
 
@@ -145,6 +149,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
     "emt_engine_attach_lines", "emt_ipc_alloc", "emt_ipc_open", "emt_ipc_close", "emt_ipc_free",
+    "emt_waves_to_text", "emt_free",
 ]
 
 
@@ -200,15 +205,27 @@ class WaveformSet:
         cols = [c * self.width + lane for c in range(len(self.channels))]
         return WaveformSet(list(self.channels), 1, self.time.copy(), self.values[:, cols].copy())
 
-    def to_text(self) -> str:
-        """WaveformSet::to_text (proj/src/waveform.cpp:22-42): %.17g rows."""
-        head = ["time"]
-        for name in self.channels:
-            head += [name] if self.width == 1 else [f"{name}#{l}" for l in range(self.width)]
-        lines = [" ".join(head)]
-        for r in range(len(self.time)):
-            lines.append(" ".join(["%.17g" % self.time[r]] + ["%.17g" % x for x in self.values[r]]))
-        return "\n".join(lines) + "\n"
+    def to_text(self, threads: int = 0) -> str:
+        """WaveformSet::to_text (proj/src/waveform.cpp:22-42): %.17g rows, formatted
+        natively by emt_waves_to_text on `threads` host threads (0: all cores)."""
+        return waves_to_text(self.channels, self.width, self.time, self.values, threads).decode()
+
+
+def waves_to_text(channels: List[str], width: int, time: np.ndarray, values: np.ndarray, threads: int = 0) -> bytes:
+    """The reference's waveform text (WaveformSet::to_text) of host rows, as bytes."""
+    L = lib()
+    t = np.ascontiguousarray(time, dtype=np.float64)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if v.size != t.size * len(channels) * width:
+        raise ValueError("values must hold rows x channels x width doubles")
+    names = (ctypes.c_char_p * max(1, len(channels)))(*[c.encode() for c in channels])
+    out, n = ctypes.c_void_p(), ctypes.c_int64()
+    _check(L.emt_waves_to_text(names, len(channels), int(width), _dp(t), _dp(v), t.size,
+                               int(threads) if threads > 0 else (os.cpu_count() or 1), ctypes.byref(out), ctypes.byref(n)))
+    try:
+        return ctypes.string_at(out.value, n.value)
+    finally:
+        L.emt_free(out)
 
 
 def _config(device: int = 0, lane_begin: int = 0, lane_count: int = 0, lanes_per_block: int = 0,
