@@ -2215,7 +2215,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "          if (m >= step + 2 - a.min_k) break;\n"
       << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
       << "        }\n"
-      << "        __threadfence();\n"
+      << "        if (a.sys_scope) __threadfence_system();  // gpu scope: the acquire loads + bar.sync suffice\n"
       << "        if (lane == 0) s_cmin = m;\n"
       << "      }\n"
       << "      __syncthreads();\n"
@@ -2243,6 +2243,44 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "        FAILPUB(); return;\n"
       << "      }\n"
       << "    }\n";
+    // progress release: right after the barrier that follows region A when every line
+    // end writes its history there (peers only read histories), else at the pass end.
+    // st.release after bar.sync orders the whole CTA's earlier stores (PTX memory
+    // model: the barrier puts them before thread 0's release in causality order).
+    bool berg_a_only = true;
+    for (const Task& t : g.tasks)
+        if (t.kind == K_BERG && t.region != 0) berg_a_only = false;
+    const bool early_rel = berg_a_only && knob("EMTB200_CG_EARLYREL", 0) != 0;  // measured: C4 3.35 -> 4.60 us (the release stalls warp 0 mid-pass)
+    // delayed publication (EMTB200_CG_DELAYREL, min_k >= 3): the pass end releases the
+    // previous pass, whose stores have long completed, so the release does not hold
+    // warp 0; the last pass is published after the loop. Deadlock-free for K >= 3: a
+    // CTA at pass p needs its peers at p+2-K, and they need it at p+4-2K <= p-2.
+    const bool delay_rel = knob("EMTB200_CG_DELAYREL", 0) != 0;
+    auto rel_stmt = [](const std::string& val) {
+        return std::string("      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(") +
+               val + ")) : \"memory\"); }\n" +
+               "      else asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(" +
+               val + ")) : \"memory\");\n";
+    };
+    // the release waits for the CTA's outstanding stores: issue it from the warp with
+    // the least region-A work so that wait does not delay the next pass's critical path
+    int rel_warp = 0;
+    {
+        long long best = -1;
+        for (int w = 0; w < G; ++w) {
+            long long c = 0;
+            for (const auto& ph : sa.phases)
+                for (int id : ph[static_cast<size_t>(w)]) c += g.tasks[static_cast<size_t>(id)].cost;
+            if (best < 0 || c < best) { best = c; rel_warp = w; }
+        }
+        if (knob("EMTB200_CG_RELWARP", 1) == 0) rel_warp = 0;
+    }
+    const std::string release =
+        std::string("    if (a.progress != nullptr && threadIdx.x == ") + std::to_string(32 * rel_warp) + ") {\n" +
+        (delay_rel ? std::string("      if (a.min_k >= 3) { if (it > 0) {\n") + rel_stmt("step") + "      } } else {\n" + rel_stmt("step + 1") + "      }\n"
+                   : rel_stmt("step + 1")) +
+        "    }\n";
+    if (early_rel) o << release;
     o << code_b << dmma_block << code_c;
     if (srcpf)  // the pass-end barrier below orders the copies before the next pass's reads
         o << "    asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
@@ -2274,13 +2312,12 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << g.solve_layer << "; }\n"
           << "      FAILPUB(); return;\n";
     }
-    o      << "    }\n"
-      << "    if (a.progress != nullptr && threadIdx.x == 0) {\n"
-      << "      __threadfence();\n"
-      << "      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\"); }\n"
-      << "      else asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(step + 1)) : \"memory\");\n"
-      << "    }\n"
-      << "  }\n";
+    o      << "    }\n";
+    if (!early_rel) o << release;
+    o << "  }\n";
+    if (delay_rel)
+        o << "  if (a.progress != nullptr && threadIdx.x == 0 && a.min_k >= 3 && a.nsteps > 0) {\n"
+          << "    const int step = a.step0 + a.nsteps - 1;\n" << rel_stmt("step + 1") << "  }\n";
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
       << "  if (live) {\n"
