@@ -6,6 +6,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 from conftest import ROOT
 from paper_1903_01081_b200 import build, engine
 
@@ -75,3 +77,18 @@ def test_codegen_variants_nvrtc_compile():
     b, _ = bench.build_batch(64, workload="c4")
     src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=8, compile=True)
     assert "emt_src_kernel" in src and "cubin=" in summary
+
+
+@pytest.mark.parametrize("knobs", [
+    {"EMTB200_CG_SRCPF": "1"}, {"EMTB200_CG_GLHOIST": "1"}, {"EMTB200_CG_BATCH": "8"},
+    {"EMTB200_CG_DELAYREL": "1"}, {"EMTB200_CG_EARLYREL": "1"}, {"EMTB200_CG_SLCOPY": "0", "EMTB200_CG_ZTERM": "2"},
+])
+def test_codegen_knob_variants_compile(knobs, monkeypatch):
+    """The measured-and-kept-off generator options still produce compilable kernels
+    (the line-coupled C4 case exercises every one of them)."""
+    import bench
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    b, _ = bench.build_batch(64, workload="c4")
+    src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=8, compile=True)
+    assert "cubin=" in summary
