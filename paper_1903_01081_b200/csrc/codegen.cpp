@@ -1759,6 +1759,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     auto loopable = [](int kind) {
         return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
     };
+    std::vector<std::string> wprefix, wsuffix;  // per-warp code around a region's block (empty: none)
     auto region_code = [&](const Sched& sc, bool fused_pass) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -1769,6 +1770,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             rc << "    switch (warp) {\n";
             for (int w = 0; w < G; ++w) {
                 rc << "    case " << w << ": {\n";
+                if (!wprefix.empty()) rc << wprefix[static_cast<size_t>(w)];
                 std::vector<int> sw_ids;  // process id per swbits bit
                 std::vector<int> sw_tasks;  // task per swbits bit
                 std::string sw_lits;        // gated slim switch tests of this warp
@@ -1902,6 +1904,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                           "b &= b - 1; const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
                           "a.events[3*e+1] = gl; a.events[3*e+2] = " << tab << "[j]; } } } }\n";
                 }
+                if (!wsuffix.empty()) rc << wsuffix[static_cast<size_t>(w)];
                 rc << mark(prof_base + 2 * static_cast<int>(sc.phases.size()) - 2) << "    } break;\n";
             }
             rc << "    }\n";
@@ -1940,7 +1943,40 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         const size_t e0 = a0.rfind("} break;", c1);
         code_a = "    {\n" + a0.substr(b0 + 13, e0 - b0 - 13) + "    }\n";
     }
+    bool has_lines = false;
+    for (const Task& t : g.tasks) has_lines = has_lines || t.kind == K_BERG;
+    // measured slower (C4 3.37 -> 3.77 us: the acquire fence stalls that warp ~1000
+    // cycles at the end of the pass), so off
+    if (has_lines && straight && warp_major && knob("EMTB200_CG_BGPOLL", 0) != 0) {
+        // line coupling: the warp with the least region-B work reads every CTA's progress
+        // word once per pass (relaxed loads issued at the region start, consumed at its
+        // end, then an acquire fence) and raises s_cmin, so the blocking poll at the top
+        // of a pass rarely runs
+        int lw = 0;
+        long long best = -1;
+        for (int w = 0; w < G; ++w) {
+            long long c = 0;
+            for (const auto& ph : sb.phases)
+                for (int id : ph[static_cast<size_t>(w)]) c += g.tasks[static_cast<size_t>(id)].cost;
+            if (best < 0 || c < best) { best = c; lw = w; }
+        }
+        wprefix.assign(static_cast<size_t>(G), std::string());
+        wsuffix.assign(static_cast<size_t>(G), std::string());
+        wprefix[static_cast<size_t>(lw)] =
+            "      unsigned int pm_ = 0xffffffffu;\n"
+            "      if (a.progress != nullptr) for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; "
+            "if (a.sys_scope) asm volatile(\"ld.relaxed.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); "
+            "else asm volatile(\"ld.relaxed.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); pm_ = min(pm_, v); }\n";
+        wsuffix[static_cast<size_t>(lw)] =
+            "      if (a.progress != nullptr) {\n"
+            "        pm_ = __reduce_min_sync(0xffffffffu, pm_);\n"
+            "        if (a.sys_scope) asm volatile(\"fence.acq_rel.sys;\" ::: \"memory\"); else asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n"
+            "        if (lane == 0 && (int)pm_ > s_cmin && pm_ < 0x3fffffffu) s_cmin = (int)pm_;\n"
+            "      }\n";
+    }
     const std::string code_b = region_code(sb, false);
+    wprefix.clear();
+    wsuffix.clear();
     const std::string code_c = g.dmma ? region_code(sc3, false) : std::string();
     const size_t const_bytes = rki.size() * 4 + rkd.size() * 8 + static_cast<size_t>(s.consts) * 8;
     if (const_bytes > 62 * 1024) {
