@@ -1544,7 +1544,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                 case K_FINS: c = 8; break;
                 case K_REC: c = 3; break;
                 case K_LATCH: c = 2; break;
-                case K_BERG: c = 25; break;
+                case K_BERG: c = knob("EMTB200_CG_BERGCOST", 150); break;  // + two L2 loads of peer histories (25..1000 swept: 150 best, C4 -2%)
                 case K_SRCPRE: c = 60; break;
                 default: c = 8; break;
             }
@@ -1760,6 +1760,40 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
     };
     std::vector<std::string> wprefix, wsuffix;  // per-warp code around a region's block (empty: none)
+    // Line coupling, split poll: one warp (the one with the least region-A work) waits
+    // for the peers' progress and hands the result to the warps holding line ends with
+    // a named barrier (barrier.arrive / barrier.sync 1); every other warp starts its
+    // region-A work at once instead of all warps waiting at two CTA barriers.
+    bool split_poll = false;
+    int poll_warp = 0;
+    std::vector<char> berg_warp(static_cast<size_t>(G), 0);
+    int n_berg_sync = 0;
+    {
+        bool any = false, a_only = true;
+        for (const Task& t : g.tasks)
+            if (t.kind == K_BERG) { any = true; a_only = a_only && t.region == 0; }
+        // measured slower (C4 3.26 -> 3.61 us): the line-end warps are region A's critical
+        // path and their ring loads then start only after the poll warp's release
+        if (any && a_only && straight && warp_major && knob("EMTB200_CG_SPLITPOLL", 0) != 0) {
+            // the lightest warp publishes progress at the pass end (and starts the next
+            // pass late while its release drains): poll from the second lightest
+            std::vector<std::pair<long long, int>> load;
+            for (int w = 0; w < G; ++w) {
+                long long c = 0;
+                for (const auto& ph : sa.phases)
+                    for (int id : ph[static_cast<size_t>(w)]) {
+                        c += g.tasks[static_cast<size_t>(id)].cost;
+                        if (g.tasks[static_cast<size_t>(id)].kind == K_BERG) berg_warp[static_cast<size_t>(w)] = 1;
+                    }
+                load.push_back({c, w});
+            }
+            std::stable_sort(load.begin(), load.end());
+            poll_warp = load.size() > 1 ? load[1].second : load[0].second;
+            for (int w = 0; w < G; ++w) n_berg_sync += (w != poll_warp && berg_warp[static_cast<size_t>(w)]) ? 1 : 0;
+            split_poll = true;
+        }
+    }
+    bool in_region_a = false;
     auto region_code = [&](const Sched& sc, bool fused_pass) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -1782,6 +1816,23 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                     std::vector<int> seg_of(ordered.size(), -1);
                     for (size_t si = 0; si < segs.size(); ++si)
                         for (int q = 0; q < segs[si].count; ++q) seg_of[static_cast<size_t>(segs[si].first + q)] = static_cast<int>(si);
+                    const bool berg_sync = split_poll && in_region_a && w != poll_warp && berg_warp[static_cast<size_t>(w)] &&
+                                           n_berg_sync > 0;
+                    if (berg_sync && loop_min == 0) {
+                        // line ends last in the warp's block (nothing in region A reads their output)
+                        std::set<int> bset;
+                        for (int id : ordered)
+                            if (g.tasks[static_cast<size_t>(id)].kind == K_BERG) bset.insert(id);
+                        bool indep = true;
+                        for (int id : ordered)
+                            for (int d : deps[static_cast<size_t>(id)]) indep = indep && !bset.count(d);
+                        if (indep) {
+                            std::stable_partition(ordered.begin(), ordered.end(),
+                                                  [&](int id) { return !bset.count(id); });
+                            for (size_t q = 0; q < ordered.size(); ++q) seg_of[q] = -1;
+                        }
+                    }
+                    bool berg_synced = false;
                     // global loads (source table, peer line histories) issued at the phase
                     // start so their L2 latency overlaps the phase's shared-memory work; a line
                     // end's HBM stores move to the phase end (nothing in the pass reads them)
@@ -1793,7 +1844,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                             if (t.kind == K_VSRCT || t.kind == K_ISRCT) {
                                 rc << "      const double gv" << id << " = SRCV_(" << t.f[1] << ");\n";
                                 hoisted.insert(id);
-                            } else if (t.kind == K_BERG) {
+                            } else if (t.kind == K_BERG && !berg_sync) {
                                 const std::string L = std::to_string(t.f[4]);
                                 const std::string at = "a.ring + pl_ * a.ring_cols + pr_ + ";
                                 rc << "      double gb1" << id << ", gb0" << id << ", gbe" << id << "; { const int K_ = (int)(" << lctx.cst(t.ck[3])
@@ -1806,13 +1857,20 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                             }
                         }
                     for (size_t oi = 0; oi < ordered.size(); ++oi) {
-                        const Segment& sg = segs[static_cast<size_t>(seg_of[oi])];
-                        if (loop_min > 0 && sg.count >= loop_min && sg.indep && loopable(sg.kind)) {
-                            if (static_cast<int>(oi) == sg.first) rc << emit_compact(sg, ordered);  // tasks in order
-                            continue;
+                        if (loop_min > 0) {
+                            const Segment& sg = segs[static_cast<size_t>(seg_of[oi])];
+                            if (sg.count >= loop_min && sg.indep && loopable(sg.kind)) {
+                                if (static_cast<int>(oi) == sg.first) rc << emit_compact(sg, ordered);  // tasks in order
+                                continue;
+                            }
                         }
                         const int id = ordered[oi];
                         const Task& t = g.tasks[static_cast<size_t>(id)];
+                        if (berg_sync && !berg_synced && t.kind == K_BERG) {
+                            rc << "      if (a.progress != nullptr) asm volatile(\"barrier.sync 1, " << 32 * (n_berg_sync + 1)
+                               << ";\" ::: \"memory\");  // the poll warp's progress result\n";
+                            berg_synced = true;
+                        }
                         LitCtx c = lctx;
                         c.fused_pass = fused_pass;
                         if (hoisted.count(id)) {
@@ -1931,11 +1989,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
         return rc.str();
     };
+    in_region_a = true;
     std::string code_a = region_code(sa, false);
     if (!g.fused.empty()) {  // the launch's first pass reads i_prev from the arena; later passes recompute it
         const std::string code_af = region_code(sa, true);
         code_a = "    if (__builtin_expect(it != 0, 1)) {\n" + code_af + "    } else {\n" + code_a + "    }\n";
     }
+    in_region_a = false;
     if (knob("EMTB200_CG_EXP_SKIPA", 0)) code_a = "";  // timing experiment only: wrong numerics
     if (knob("EMTB200_CG_EXP_SAMEA", 0)) {  // timing experiment only: every warp runs warp 0's region-A code
         const std::string a0 = region_code(sa, true);
@@ -2231,13 +2291,36 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  long long prof_t = clock64(); (void)prof_t;\n"
       << "  double swnext = -1.0; (void)swnext;  // per lane: next switch toggle time not yet reached\n"
       << "  const double dlim = a.div_limit; (void)dlim;\n"
+      << "  int pcmin = -0x3fffffff; int pfail = 0; (void)pcmin;  // split poll: the poll warp's view of peer progress\n"
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    const double tn = (double)(step + 2) * " << lit(s.dt) << "; (void)tn;\n"
       << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true; double dsum = 0.0;\n"
       << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok; (void)dsum;\n"
-      << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
+      ;
+    if (split_poll) {
+        o << "    if (a.progress != nullptr && warp == " << poll_warp << ") {\n"
+          << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs: this warp\n"
+          << "      // waits until every CTA has completed pass step+1-K, then releases the line-end warps\n"
+          << "      if (pcmin < step + 2 - a.min_k) {\n"
+          << "        const long long t0 = clock64(); int m;\n"
+          << "        for (;;) {\n"
+          << "          m = 0x7fffffff;\n"
+          << "          for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
+          << "          m = __reduce_min_sync(0xffffffffu, m);\n"
+          << "          if (m >= step + 2 - a.min_k) break;\n"
+          << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
+          << "        }\n"
+          << "        if (a.sys_scope) __threadfence_system();\n"
+          << "        pcmin = m;\n"
+          << "        if (m < 0) pfail = 1;\n"
+          << "      }\n";
+        if (n_berg_sync > 0)
+            o << "      asm volatile(\"barrier.arrive 1, " << 32 * (n_berg_sync + 1) << ";\" ::: \"memory\");\n";
+        o << "    }\n";
+    } else {
+        o << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
       << "      __syncthreads();\n"
@@ -2257,7 +2340,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "      __syncthreads();\n"
       << "      if (s_cmin < 0) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
       << "    }\n"
-      << "    if (warp == 0) { ";
+;
+    }
+    o       << "    if (warp == 0) { ";
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
     o << "}\n";
@@ -2268,7 +2353,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "    }\n";
     }
     o << code_a;
-    o << "    if (__syncthreads_or(wflag)) {\n"
+    o << "    if (__syncthreads_or(wflag | pfail)) {\n"
+      << "      if (__syncthreads_or(pfail)) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
       << "      if (warp == 0) {\n"
       << (knob("EMTB200_CG_NOINLINE", 0) ? "        srow = emt_refactor(S, A, C, live, lane, needS);\n" : g.emit_refactor())
       << "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
