@@ -1182,6 +1182,8 @@ struct LitCtx {
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
     bool zterm = false;                    // drop zero-slot terms from sums
     int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
+    int task_id = -1;                      // the task's index (per-task registers)
+    bool berg_pf = false;                  // line ends: peer histories loaded one pass ahead into registers
     std::string* deferred = nullptr;       // hoisted line end: its global stores go here (phase end)
 };
 
@@ -1256,6 +1258,29 @@ std::string task_literal(const Task& t, const LitCtx& c) {
         *c.deferred += "      if (live) { const int w_ = step % " + std::to_string(t.f[4]) + "; A[(size_t)(" + std::to_string(t.f[3]) +
                        " + w_) * W_] = gbe" + id + "; a.ring[(LB_ + gl) * a.ring_cols + (" + std::to_string(t.f[3]) +
                        " - a.ring_lo) + w_] = gbe" + id + "; }\n";
+        return o.str();
+    }
+    if (c.berg_pf && t.kind == K_BERG && c.task_id >= 0) {
+        // peer histories for this pass were loaded during the previous one (when the
+        // poll keeps one more pass of slack, min_k >= 3); this pass loads the next's
+        const std::string id = std::to_string(c.task_id), L = std::to_string(t.f[4]);
+        const std::string at = "a.ring + pl_ * a.ring_cols + pr_ + ";
+        auto ld = [&](const std::string& q) {
+            return "(a.sys_scope ? __ldcv(" + at + q + ") : __ldcg(" + at + q + "))";
+        };
+        o << "const double vs_ = LD(" << t.f[1] << ") - LD(" << t.f[0] << "); const double hp_ = LD(" << t.f[2]
+          << "); const int K_ = (int)(" << c.cst(t.ck[3]) << "); const long long pl_ = (long long)(" << c.cst(t.ck[4])
+          << "); const long long pr_ = (long long)(" << c.cst(t.ck[5]) << ") - a.ring_lo; "
+          << "double b1_ = pb1_" << id << ", b0_ = pb0_" << id << "; "
+          << "if (!pfok || it == 0) { int q1_ = (step + 1 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
+          << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; b1_ = " << ld("q1_") << "; b0_ = " << ld("q0_") << "; } "
+          << "if (pfok && it + 1 < a.nsteps) { int q1_ = (step + 2 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
+          << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; pb1_" << id << " = " << ld("q1_") << "; pb0_" << id
+          << " = " << ld("q0_") << "; } "
+          << "const double be_ = " << c.cst(t.ck[0]) << " * vs_ + hp_; ST(" << t.f[2] << ", -(" << c.cst(t.ck[1])
+          << " * b1_ + " << c.cst(t.ck[2]) << " * b0_)); "
+          << "if (live) { const int w_ = step % " << L << "; A[(size_t)(" << t.f[3] << " + w_) * W_] = be_; a.ring[(LB_ + gl) * a.ring_cols + ("
+          << t.f[3] << " - a.ring_lo) + w_] = be_; } }";
         return o.str();
     }
     if (t.fused && c.fused_pass) {
@@ -1794,6 +1819,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
     }
     bool in_region_a = false;
+    bool berg_pf = false;
+    {
+        bool any = false;
+        for (const Task& t : g.tasks) any = any || t.kind == K_BERG;
+        // measured slower (C4 3.21 -> 3.30 us), so off
+        berg_pf = any && !split_poll && straight && warp_major && knob("EMTB200_CG_BERGPF", 0) != 0;
+    }
     auto region_code = [&](const Sched& sc, bool fused_pass) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -1873,6 +1905,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         }
                         LitCtx c = lctx;
                         c.fused_pass = fused_pass;
+                        c.task_id = id;
+                        c.berg_pf = berg_pf;
                         if (hoisted.count(id)) {
                             c.hoist = id;
                             c.deferred = &post;
@@ -1989,6 +2023,47 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
         return rc.str();
     };
+    // Line coupling, early poll (EMTB200_CG_APOLL): the second-lightest region-A warp
+    // (the lightest publishes progress at the pass end) issues relaxed loads of every
+    // CTA's progress word at the start of its region-A block; at the start of region B
+    // (after the CTA barrier, so no thread still reads s_cmin for this pass) it takes
+    // the minimum, fences (acquire) and raises s_cmin, so the blocking poll at the top
+    // of a pass rarely runs.
+    std::vector<std::string> apoll_b;  // region-B prefixes (set after region A is emitted)
+    {
+        bool any = false;
+        for (const Task& t : g.tasks) any = any || t.kind == K_BERG;
+        // measured slower (C4 3.27 -> 3.55 us: the acquire fence holds the warp ~1000
+        // cycles at the start of region B), so off
+        if (any && straight && warp_major && !split_poll && knob("EMTB200_CG_APOLL", 0) != 0) {
+            std::vector<std::pair<long long, int>> load;
+            for (int w = 0; w < G; ++w) {
+                long long c = 0;
+                for (const auto& ph : sa.phases)
+                    for (int id : ph[static_cast<size_t>(w)]) c += g.tasks[static_cast<size_t>(id)].cost;
+                load.push_back({c, w});
+            }
+            std::stable_sort(load.begin(), load.end());
+            const int pw = load.size() > 1 ? load[1].second : load[0].second;
+            wprefix.assign(static_cast<size_t>(G), std::string());
+            wprefix[static_cast<size_t>(pw)] =
+                "      if (a.progress != nullptr) { pm_ = 0xffffffffu; for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; "
+                "if (a.sys_scope) asm volatile(\"ld.relaxed.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); "
+                "else asm volatile(\"ld.relaxed.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); pm_ = min(pm_, v); } }\n";
+            apoll_b.assign(static_cast<size_t>(G), std::string());
+            apoll_b[static_cast<size_t>(pw)] =
+                "      if (a.progress != nullptr) {\n"
+                "        pm_ = __reduce_min_sync(0xffffffffu, pm_);\n"
+                "        if (a.sys_scope) asm volatile(\"fence.acq_rel.sys;\" ::: \"memory\"); else asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n"
+                "        if (lane == 0 && (int)pm_ > s_cmin && pm_ < 0x3fffffffu) s_cmin = (int)pm_;\n"
+                "      }\n";
+        }
+    }
+    std::string berg_decls;
+    if (berg_pf)
+        for (size_t i = 0; i < g.tasks.size(); ++i)
+            if (g.tasks[i].kind == K_BERG)
+                berg_decls += "  double pb1_" + std::to_string(i) + " = 0.0, pb0_" + std::to_string(i) + " = 0.0;\n";
     in_region_a = true;
     std::string code_a = region_code(sa, false);
     if (!g.fused.empty()) {  // the launch's first pass reads i_prev from the arena; later passes recompute it
@@ -1996,6 +2071,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         code_a = "    if (__builtin_expect(it != 0, 1)) {\n" + code_af + "    } else {\n" + code_a + "    }\n";
     }
     in_region_a = false;
+    wprefix.clear();
     if (knob("EMTB200_CG_EXP_SKIPA", 0)) code_a = "";  // timing experiment only: wrong numerics
     if (knob("EMTB200_CG_EXP_SAMEA", 0)) {  // timing experiment only: every warp runs warp 0's region-A code
         const std::string a0 = region_code(sa, true);
@@ -2033,6 +2109,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             "        if (a.sys_scope) asm volatile(\"fence.acq_rel.sys;\" ::: \"memory\"); else asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n"
             "        if (lane == 0 && (int)pm_ > s_cmin && pm_ < 0x3fffffffu) s_cmin = (int)pm_;\n"
             "      }\n";
+    }
+    if (!apoll_b.empty()) {
+        if (wprefix.empty()) wprefix.assign(static_cast<size_t>(G), std::string());
+        for (int w = 0; w < G; ++w) wprefix[static_cast<size_t>(w)] = apoll_b[static_cast<size_t>(w)] + wprefix[static_cast<size_t>(w)];
     }
     const std::string code_b = region_code(sb, false);
     wprefix.clear();
@@ -2292,6 +2372,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  double swnext = -1.0; (void)swnext;  // per lane: next switch toggle time not yet reached\n"
       << "  const double dlim = a.div_limit; (void)dlim;\n"
       << "  int pcmin = -0x3fffffff; int pfail = 0; (void)pcmin;  // split poll: the poll warp's view of peer progress\n"
+      // one-pass-ahead peer histories (deadlock-free only with >= 2 passes of slack)
+      << "  const int pfok = " << (berg_pf ? "a.min_k >= 3 ? 1 : 0" : "0") << "; (void)pfok;\n"
+      << "  unsigned int pm_ = 0xffffffffu; (void)pm_;\n"
+      << berg_decls
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
@@ -2320,7 +2404,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             o << "      asm volatile(\"barrier.arrive 1, " << 32 * (n_berg_sync + 1) << ";\" ::: \"memory\");\n";
         o << "    }\n";
     } else {
-        o << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
+        o << (knob("EMTB200_CG_EXP_NOPOLL", 0) ? "    if (false) {\n"  // timing experiment only: unsynchronised line coupling
+                                               : "    if (a.progress != nullptr && s_cmin < step + 2 + pfok - a.min_k) {\n")
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
       << "      __syncthreads();\n"
@@ -2331,7 +2416,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "          m = 0x7fffffff;\n"
       << "          for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
       << "          m = __reduce_min_sync(0xffffffffu, m);\n"
-      << "          if (m >= step + 2 - a.min_k) break;\n"
+      << "          if (m >= step + 2 + pfok - a.min_k) break;\n"
       << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
       << "        }\n"
       << "        if (a.sys_scope) __threadfence_system();  // gpu scope: the acquire loads + bar.sync suffice\n"
