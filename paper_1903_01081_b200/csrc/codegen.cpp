@@ -114,6 +114,12 @@ struct Gen {
     // rounded for normal-range operands, tools/micro/divcheck.c)
     bool rcp = false;
     int rcp_base = -1;
+    // shared factors: when G is the same constant matrix in every lane and nothing
+    // changes it (no switches), every lane's refactorisation produces the same L, U
+    // and pivot reciprocals; one copy per CTA (SH, broadcast reads) replaces the
+    // per-lane [slot][lane] copies, which frees room for the reciprocals
+    bool lu_shared = false;
+    long long sh_base = -1;  // double offset of SH from the dynamic shared-memory base
     // finalize fusion: an L / C / RL component whose current only its own next-pass
     // Norton update reads gets i_prev = g (vb - va) + h recomputed there (the same
     // operands and order as the finalize), and its finalize runs once per launch
@@ -238,8 +244,31 @@ struct Gen {
         if (slot >= 0 && slot < s.extent && cls[static_cast<size_t>(slot)] == kAlias) return alias_of.at(slot);
         return slot;
     }
-    int lu_l(int k) const { return l_base_smem >= 0 ? (l_base_smem + k) * unit : s.l + k; }
-    int lu_u(int k) const { return u_base_smem >= 0 ? (u_base_smem + k) * unit : s.u + k; }
+    // L/U operand codes: >= 0 a shared-memory byte offset (or arena slot); < 0 the
+    // shared-factor entry SH[-(code + 1)]
+    int lu_l(int k) const {
+        if (lu_shared) return -(1 + k);
+        return l_base_smem >= 0 ? (l_base_smem + k) * unit : s.l + k;
+    }
+    int lu_u(int k) const {
+        if (lu_shared) return -(1 + static_cast<int>(s.l_col.size()) + k);
+        return u_base_smem >= 0 ? (u_base_smem + k) * unit : s.u + k;
+    }
+    int sh_rcp(int i) const { return static_cast<int>(s.l_col.size() + s.u_col.size()) + i; }
+    /// G is a lane-invariant constant and nothing refactorises it differently per lane
+    bool factor_shared() const {
+        if (s.nodes <= 0 || s.dim <= 0) return false;
+        for (const Proc& p : s.procs)
+            if (p.code == kNortonSwitch) return false;
+        for (int x : s.watch)
+            if (x != s.dirty) return false;
+        for (int x : s.mentry_slot) {
+            if (x < 0 || cls[static_cast<size_t>(x)] != kDerived) return false;
+            const int k = derived_const[static_cast<size_t>(x)];
+            if (k >= 0 && !invariant(k)) return false;
+        }
+        return true;
+    }
 
     // ---- expressions for the straight-line refactorization
     std::string C(int k) const {
@@ -257,10 +286,12 @@ struct Gen {
     }
     std::string Wr(int slot) const { return "S[" + std::to_string(hot_index[static_cast<size_t>(slot)] * ls) + "]"; }
     std::string Lw(int k, const std::string& v) const {
+        if (lu_shared) return "SH[" + std::to_string(k) + "] = " + v + ";";
         if (l_base_smem >= 0) return "S[" + std::to_string((l_base_smem + k) * ls) + "] = " + v + ";";
         return "if (live) A[" + std::to_string(static_cast<long long>(s.l + k) * W) + "] = " + v + ";";
     }
     std::string Uw(int k, const std::string& v) const {
+        if (lu_shared) return "SH[" + std::to_string(s.l_col.size() + static_cast<size_t>(k)) + "] = " + v + ";";
         if (u_base_smem >= 0) return "S[" + std::to_string((u_base_smem + k) * ls) + "] = " + v + ";";
         return "if (live) A[" + std::to_string(static_cast<long long>(s.u + k) * W) + "] = " + v + ";";
     }
@@ -604,7 +635,7 @@ struct Gen {
                     t.terms.push_back({lu_u(k), off(v + c)});
                 }
                 t.writes = {v + i};
-                t.f = {off(v + i), lu_u(ub), i, rcp_base >= 0 ? (rcp_base + i) * unit : -1};
+                t.f = {off(v + i), lu_u(ub), i, lu_shared ? -(2 + i) : rcp_base >= 0 ? (rcp_base + i) * unit : -1};
                 t.cost = 40 + 5 * (ue - ub - 1);
                 add(std::move(t), region);
             }
@@ -724,7 +755,8 @@ struct Gen {
             hot_slots.push_back(x);
         }
         const size_t per_slot = static_cast<size_t>(ls) * sizeof(double);
-        const size_t fixed = 2 * static_cast<size_t>(ls) * sizeof(int);  // serr + refactor flags
+        const size_t fixed = 2 * static_cast<size_t>(ls) * sizeof(int) +  // serr + refactor flags
+                             (lu_shared ? (s.l_col.size() + s.u_col.size() + static_cast<size_t>(s.dim)) * sizeof(double) : 0);
         pre_base = static_cast<int>(hot_slots.size());
         size_t used = (hot_slots.size() + pre_ck.size()) * per_slot + fixed;
         if (used > opt.smem_budget) return false;
@@ -744,7 +776,7 @@ struct Gen {
         }
         const int next = vc_base + static_cast<int>(vc_slots.size());
         const size_t lu = (s.l_col.size() + s.u_col.size()) * per_slot;
-        lu_smem = opt.lu_in_smem && used + lu <= opt.smem_budget;
+        lu_smem = !lu_shared && opt.lu_in_smem && used + lu <= opt.smem_budget;
         if (lu_smem) {
             l_base_smem = next;
             u_base_smem = l_base_smem + static_cast<int>(s.l_col.size());
@@ -828,6 +860,7 @@ struct Gen {
                 const int c = s.u_col[static_cast<size_t>(k)];
                 o << "          u" << k << " = w" << c << "; " << Uw(k, "u" + std::to_string(k));
                 if (k == ub && rcp_base >= 0) o << " S[" << (rcp_base + i) * ls << "] = 1.0 / u" << k << ";";
+                if (k == ub && lu_shared) o << " SH[" << sh_rcp(i) << "] = 1.0 / u" << k << ";";
                 o << "\n";
             }
             for (int c : cols)
@@ -1183,6 +1216,7 @@ struct LitCtx {
     bool zterm = false;                    // drop zero-slot terms from sums
     int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
     int task_id = -1;                      // the task's index (per-task registers)
+    int sh_rcp0 = 0;                       // SH index of the first pivot reciprocal (shared factors)
     bool berg_pf = false;                  // line ends: peer histories loaded one pass ahead into registers
     std::string* deferred = nullptr;       // hoisted line end: its global stores go here (phase end)
 };
@@ -1307,18 +1341,20 @@ std::string task_literal(const Task& t, const LitCtx& c) {
             if (tm.first != 0 || !c.zterm) o << "acc = acc + " << (tm.second ? "-" : "") << "LD(" << tm.first << "); ";
         o << "ST(" << t.f[0] << ", acc);";
     } else if (t.kind == K_FWD || t.kind == K_BWD) {
+        auto lu = [](int x) { return x < 0 ? "SH[" + std::to_string(-x - 1) + "]" : "LU(" + std::to_string(x) + ")"; };
         o << "double x = LD(" << t.f[0] << "); ";
-        for (const auto& tm : t.terms) o << "x = x - LU(" << tm.first << ") * LD(" << tm.second << "); ";
+        for (const auto& tm : t.terms) o << "x = x - " << lu(tm.first) << " * LD(" << tm.second << "); ";
         if (t.kind == K_BWD)
             if (c.dok)
-                if (t.f.size() > 3 && t.f[3] >= 0)
-                    o << "{ const double r_ = LD(" << t.f[3] << "); const double d_ = LU(" << t.f[1]
-                      << "); const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } "
+                if (t.f.size() > 3 && (t.f[3] >= 0 || t.f[3] <= -2))
+                    o << "{ const double r_ = " << (t.f[3] >= 0 ? "LD(" + std::to_string(t.f[3]) + ")" : "SH[" + std::to_string(c.sh_rcp0 - t.f[3] - 2) + "]")
+                      << "; const double d_ = " << lu(t.f[1])
+                      << "; const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } "
                       << (c.dsum ? "dsum = dsum + fabs(x); " : "dok = dok & (fabs(x) <= dlim); ");
                 else
-                    o << "x = x / LU(" << t.f[1] << "); dok = dok & (fabs(x) <= dlim); ";
+                    o << "x = x / " << lu(t.f[1]) << "; dok = dok & (fabs(x) <= dlim); ";
             else
-                o << "x = x / LU(" << t.f[1] << "); if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
+                o << "x = x / " << lu(t.f[1]) << "; if (!(fabs(x) <= a.div_limit) && " << t.f[2] << " < bad) bad = " << t.f[2] << "; ";
         o << "ST(" << t.f[0] << ", x);";
     } else if (t.kind == K_SW && c.sw_bit >= 0 && c.sw_slim && t.ck.size() == 4 && c.lit_init && c.lit_init(t.ck[2]) >= 0) {
         // one toggle time: changed <=> (init XOR t >= t0) != state, init folded in
@@ -1494,6 +1530,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         g.opt.lu_in_smem = false;  // the sweeps are gone; L/U stay in HBM for refactor + state
     }
     const int MT = (s.dim + 7) / 8, KT = (s.dim + 3) / 4;  // DMMA m8n8k4 tiles of G^-1
+    if (!g.dmma && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && knob("EMTB200_CG_LOOPMIN", 0) == 0 &&
+        knob("EMTB200_CG_SHLU", 1) != 0)
+        g.lu_shared = g.factor_shared();
     const size_t ginv_bytes = g.dmma ? static_cast<size_t>(MT) * 8 * KT * 4 * sizeof(double) : 0;
     g.opt.smem_budget = opt.smem_budget > ginv_bytes ? opt.smem_budget - ginv_bytes : 0;
     int facts = 0;
@@ -1539,7 +1578,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         fail = {13, "", "arena hot set exceeds the shared-memory budget"};
         return false;
     }
-    if (g.fusefin && !g.fused.empty() && !lu_smem && !g.dmma) {
+    if (g.fusefin && !g.fused.empty() && !lu_smem && !g.dmma && !g.lu_shared) {
         // measured: with the factors in HBM (C5 exact path) the fused form schedules worse
         g.fusefin = false;
         g.classify();
@@ -1699,6 +1738,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     lctx.dsum = knob("EMTB200_CG_DSUM", 0) != 0;  // measured 0.6% slower than the AND-ed predicate
     const bool dok_mode = straight && (knob("EMTB200_CG_DOK", 1) != 0 || g.dmma);
     lctx.dok = dok_mode;
+    lctx.sh_rcp0 = g.sh_rcp(0);
     lctx.cst = [&](int k) -> std::string {
         if (g.invariant(k)) return "kC[" + std::to_string(k) + "]";
         if (g.vc_index[static_cast<size_t>(k)] >= 0) return "LD(" + std::to_string(g.vc_index[static_cast<size_t>(k)] * g.unit) + ")";
@@ -2309,6 +2349,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
       << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+      << (g.lu_shared ? "  double* __restrict__ SH = sm + " + std::to_string(static_cast<long long>(g.smem_slots()) * LPC + LPC) +
+                            ";  // shared factors: L, U, pivot reciprocals (one copy per CTA)\n"
+                      : std::string())
       << pre_prologue
       << dmma_prologue
 ;
@@ -2355,6 +2398,21 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
               << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = 1.0 / A[(size_t)("
               << s.u << " + kUd[q]) * W_]; }\n";
         }
+    }
+    if (g.lu_shared) {
+        // the factors of the CTA's first lane (every lane holds the same); reciprocals
+        // from the same arena values
+        const std::string base = "(size_t)blockIdx.x * " + std::to_string(LPC);
+        std::vector<std::pair<std::string, std::string>> it;
+        const size_t nl = s.l_col.size(), nu = s.u_col.size();
+        for (size_t q = 0; q < nl; ++q)
+            it.push_back({"SH[" + std::to_string(q) + "]", "a.arena[(size_t)" + std::to_string(s.l + static_cast<long long>(q)) + " * W_ + " + base + "]"});
+        for (size_t q = 0; q < nu; ++q)
+            it.push_back({"SH[" + std::to_string(nl + q) + "]", "a.arena[(size_t)" + std::to_string(s.u + static_cast<long long>(q)) + " * W_ + " + base + "]"});
+        for (int i = 0; i < s.dim; ++i)
+            it.push_back({"SH[" + std::to_string(g.sh_rcp(i)) + "]",
+                          "1.0 / a.arena[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_ + " + base + "]"});
+        o << warp_copies(it, G, "  ");
     }
     // watch slots not rewritten by region-A tasks (the dirty flag) are checked up front
     std::set<int> written_a;
@@ -2544,6 +2602,14 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.u_col.size() << "; q += " << G << ") A[(size_t)(" << s.u << " + q) * W_] = S[("
           << g.u_base_smem << " + q) * " << LPC << "];\n";
     }
+    if (g.lu_shared) {
+        std::vector<std::pair<std::string, std::string>> it;
+        const size_t nl = s.l_col.size(), nu = s.u_col.size();
+        for (size_t q = 0; q < nl; ++q) it.push_back({"A[(size_t)" + std::to_string(s.l + static_cast<long long>(q)) + " * W_]", "SH[" + std::to_string(q) + "]"});
+        for (size_t q = 0; q < nu; ++q)
+            it.push_back({"A[(size_t)" + std::to_string(s.u + static_cast<long long>(q)) + " * W_]", "SH[" + std::to_string(nl + q) + "]"});
+        o << warp_copies(it, G, "    ");
+    }
     o << "    if (a.nsteps > 0) {\n";
     if (slcopy) {
         std::vector<std::pair<std::string, std::string>> it;
@@ -2620,7 +2686,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     long work = 0;
     for (const Task& t : g.tasks) work += t.cost;
     std::ostringstream sum;
-    sum << (straight ? "straight " : "compact ") << "lpc=" << LPC << " tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << " smem=" << smem
+    sum << (straight ? "straight " : "compact ") << "lpc=" << LPC << " tasks=" << nt << " segments=" << segs_total << " hot=" << nhot << " lu_smem=" << lu_smem << (g.lu_shared ? " lu=shared" : "") << " smem=" << smem
         << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
         << " est_span=" << static_cast<long>(span_a + span_b + span_c) << " est_work=" << work
         << (g.dmma ? " solve=dmma(G^-1 " + std::to_string(s.dim) + "x" + std::to_string(s.dim) + ")" : std::string(opt.tensor_solve ? " solve=lu(shared-G ineligible)" : ""));
