@@ -1514,8 +1514,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // the other threads of each warp shadowing lane 0 (same loads and stores, same values)
     // to shrink shared-memory traffic per instruction and spread the batch over more SMs —
     // bit-exact, but measured slower (C3 2.81 -> 3.42 / 4.92 ms per 1000 passes)
-    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", 32);
-    if (LPC != 8 && LPC != 16) LPC = 32;
+    // a single scenario (C2) runs as one lane that every thread shadows: each shared-memory
+    // access is a broadcast (C2 2.52 -> 2.17 us per step)
+    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", lanes == 1 ? 1 : 32);
+    if (LPC != 1 && LPC != 2 && LPC != 4 && LPC != 8 && LPC != 16) LPC = 32;
     g.ls = LPC;
     g.unit = LPC * 8;
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
