@@ -160,8 +160,10 @@ emt_status emt_engine_load(emt_engine* engine, const double* initial, int64_t in
 /* emt_engine_load in two halves, for pipelining batches: `stage` starts the
  * H2D of the next batch into device staging buffers on a separate stream
  * (returns at once for pinned buffers; it may overlap a running batch), and
- * `commit` makes the staged batch current (device-to-device, ordered after
- * everything already issued on the engine's stream) and rewinds to pass 0. */
+ * `commit` makes the staged batch current (the staging and live buffers swap
+ * roles, no copy; launches issued after it read the new batch, and the next
+ * `stage` writes the old buffers only after every launch issued before the
+ * commit has finished) and rewinds to pass 0. */
 emt_status emt_engine_stage(emt_engine* engine, const double* initial, int64_t initial_len,
                             const double* const_table);
 emt_status emt_engine_commit(emt_engine* engine);
