@@ -1660,7 +1660,40 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     const int G = std::max(1, std::min(opt.warps, 32));
     double span_a = 0, span_b = 0;
-    const Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
+    Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
+    if (sa.phases.size() == 1 && knob("EMTB200_CG_AFFINITY", 1) != 0) {
+        // region A is one phase of independent tasks: regroup them so that tasks reading
+        // the same node voltages share a warp (the compiler then loads each voltage once
+        // per warp) — order by the lowest node slot read, cut into G chunks of equal cost
+        std::vector<int> all;
+        for (const auto& wl : sa.phases[0]) all.insert(all.end(), wl.begin(), wl.end());
+        // (not with line ends: their peer-history loads want the scheduler's spread,
+        // measured C4 3.22 -> 3.41 us when regrouped; C3 2.70 -> 2.63 ms, C2 2.18 -> 2.12 us)
+        bool indep = true;
+        for (int id : all) indep = indep && g.tasks[static_cast<size_t>(id)].kind != K_BERG;
+        std::set<int> in_a(all.begin(), all.end());
+        for (int id : all)
+            for (int d : deps[static_cast<size_t>(id)]) indep = indep && !in_a.count(d);
+        if (indep && !all.empty()) {
+            auto key = [&](int id) {
+                int k = 1 << 30;
+                for (int r : g.tasks[static_cast<size_t>(id)].reads)
+                    if (r >= s.v_base && r < s.v_base + s.nodes) k = std::min(k, r - s.v_base);
+                return k;
+            };
+            std::stable_sort(all.begin(), all.end(), [&](int a, int b) { return key(a) < key(b); });
+            long long total = 0;
+            for (int id : all) total += g.tasks[static_cast<size_t>(id)].cost;
+            std::vector<std::vector<int>> parts(static_cast<size_t>(G));
+            long long acc = 0;
+            for (int id : all) {
+                const int w = static_cast<int>(std::min<long long>(G - 1, acc * G / std::max<long long>(1, total)));
+                parts[static_cast<size_t>(w)].push_back(id);
+                acc += g.tasks[static_cast<size_t>(id)].cost;
+            }
+            sa.phases[0] = parts;
+        }
+    }
     Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
     double span_c = 0;
     Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
