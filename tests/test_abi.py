@@ -81,7 +81,7 @@ def test_codegen_variants_nvrtc_compile():
 
 @pytest.mark.parametrize("knobs", [
     {"EMTB200_CG_SRCPF": "1"}, {"EMTB200_CG_GLHOIST": "1"}, {"EMTB200_CG_BATCH": "8"},
-    {"EMTB200_CG_DELAYREL": "1"}, {"EMTB200_CG_EARLYREL": "1"}, {"EMTB200_CG_BGPOLL": "1"}, {"EMTB200_CG_SPLITPOLL": "1"}, {"EMTB200_CG_BERGPF": "1"}, {"EMTB200_CG_APOLL": "1"}, {"EMTB200_CG_SLCOPY": "0", "EMTB200_CG_ZTERM": "2"},
+    {"EMTB200_CG_DELAYREL": "1"}, {"EMTB200_CG_EARLYREL": "1"}, {"EMTB200_CG_BGPOLL": "1"}, {"EMTB200_CG_SPLITPOLL": "1"}, {"EMTB200_CG_BERGPF": "1"}, {"EMTB200_CG_APOLL": "1"}, {"EMTB200_CG_AFFINITY": "2"}, {"EMTB200_CG_SLCOPY": "0", "EMTB200_CG_ZTERM": "2"},
 ])
 def test_codegen_knob_variants_compile(knobs, monkeypatch):
     """The measured-and-kept-off generator options still produce compilable kernels
