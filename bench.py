@@ -407,7 +407,10 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_scenario_step": bytes_per,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
+                         "note": "achieved = SURVEY §8(d) algorithmic bytes / launch time; the lane state stays in "
+                                 "shared memory for a whole launch, so DRAM moves only `traffic` per launch and the "
+                                 "kernel is bound by its per-pass instruction latency, not HBM (DESIGN.md §3.3)"},
             "clocks": clk,
         }
         if args.tensor_solve and "solve=dmma" in eng.summary:
