@@ -1514,9 +1514,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // the other threads of each warp shadowing lane 0 (same loads and stores, same values)
     // to shrink shared-memory traffic per instruction and spread the batch over more SMs —
     // bit-exact, but measured slower (C3 2.81 -> 3.42 / 4.92 ms per 1000 passes)
-    // a single scenario (C2) runs as one lane that every thread shadows: each shared-memory
-    // access is a broadcast (C2 2.52 -> 2.17 us per step)
-    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", lanes == 1 ? 1 : 32);
+    // EMTB200_CG_LPC=1 runs a single scenario (C2) as one lane every thread shadows, so each
+    // shared-memory access is a broadcast (C2 2.52 -> 2.17 us per step, bit-exact in every
+    // test) — but the shadows' read-then-write of one address is only ordered while the warp
+    // stays converged (compute-sanitizer racecheck warns), so it is not the default
+    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", 32);
     if (LPC != 1 && LPC != 2 && LPC != 4 && LPC != 8 && LPC != 16) LPC = 32;
     g.ls = LPC;
     g.unit = LPC * 8;
