@@ -1677,11 +1677,18 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         for (int id : all)
             for (int d : deps[static_cast<size_t>(id)]) indep = indep && !in_a.count(d);
         if (indep && !all.empty()) {
+            // sort key 0 lowest node read, 1 highest, 2 (lowest, highest): all within 0.3% on C3
+            const int kmode = knob("EMTB200_CG_AFFKEY", 0);
             auto key = [&](int id) {
-                int k = 1 << 30;
+                long long lo = 1 << 30, hi = -1;
                 for (int r : g.tasks[static_cast<size_t>(id)].reads)
-                    if (r >= s.v_base && r < s.v_base + s.nodes) k = std::min(k, r - s.v_base);
-                return k;
+                    if (r >= s.v_base && r < s.v_base + s.nodes) {
+                        lo = std::min<long long>(lo, r - s.v_base);
+                        hi = std::max<long long>(hi, r - s.v_base);
+                    }
+                if (kmode == 1) return hi < 0 ? (1LL << 30) : hi;
+                if (kmode == 2) return lo * 4096 + (hi < 0 ? 4095 : hi);
+                return lo;
             };
             std::stable_sort(all.begin(), all.end(), [&](int a, int b) { return key(a) < key(b); });
             long long total = 0;
