@@ -1485,7 +1485,7 @@ std::vector<std::vector<int>> task_deps(const std::vector<Task>& tasks) {
 // groups whose loads issue back to back (a loop over an index table serialises a table
 // load and the dependent arena load per slot: ~35 us per launch on C3).
 static std::string warp_copies(const std::vector<std::pair<std::string, std::string>>& items, int G,
-                               const std::string& ind, int group = 16) {
+                               const std::string& ind, int group = 16, bool solo = false) {
     if (items.empty()) return std::string();
     std::ostringstream o;
     o << ind << "switch (warp) {\n";
@@ -1494,6 +1494,8 @@ static std::string warp_copies(const std::vector<std::pair<std::string, std::str
         for (size_t q = static_cast<size_t>(w); q < items.size(); q += static_cast<size_t>(G)) mine.push_back(q);
         if (mine.empty()) continue;
         o << ind << "case " << w << ": {\n";
+        if (solo) o << ind << "  if (lane == 0)\n";  // one-lane mode: the shadows stay off shared memory
+        if (solo) o << ind << "  {\n";
         for (size_t g0 = 0; g0 < mine.size(); g0 += static_cast<size_t>(group)) {
             const size_t g1 = std::min(mine.size(), g0 + static_cast<size_t>(group));
             o << ind << "  { ";
@@ -1501,6 +1503,7 @@ static std::string warp_copies(const std::vector<std::pair<std::string, std::str
             for (size_t j = g0; j < g1; ++j) o << items[mine[j]].first << " = t" << j - g0 << "; ";
             o << "}\n";
         }
+        if (solo) o << ind << "  }\n";
         o << ind << "} break;\n";
     }
     o << ind << "}\n";
@@ -1514,14 +1517,17 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // the other threads of each warp shadowing lane 0 (same loads and stores, same values)
     // to shrink shared-memory traffic per instruction and spread the batch over more SMs —
     // bit-exact, but measured slower (C3 2.81 -> 3.42 / 4.92 ms per 1000 passes)
-    // EMTB200_CG_LPC=1 runs a single scenario (C2) as one lane every thread shadows, so each
-    // shared-memory access is a broadcast (C2 2.52 -> 2.17 us per step, bit-exact in every
-    // test) — but the shadows' read-then-write of one address is only ordered while the warp
-    // stays converged (compute-sanitizer racecheck warns), so it is not the default
-    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", 32);
+    // a single scenario (C2) runs with one lane per CTA in "solo" form (below): only thread 0
+    // of each warp executes the step, so every shared-memory access moves one word
+    int LPC = opt.lanes_per_cta > 0 ? opt.lanes_per_cta : knob("EMTB200_CG_LPC", lanes == 1 ? 1 : 32);
     if (LPC != 1 && LPC != 2 && LPC != 4 && LPC != 8 && LPC != 16) LPC = 32;
     g.ls = LPC;
     g.unit = LPC * 8;
+    // one lane per CTA: only thread 0 of each warp touches shared memory (the other
+    // threads only take part in the barriers), so there is no shared address two threads
+    // read and write; every access is a single-thread one (C2)
+    const bool solo = LPC == 1 && knob("EMTB200_CG_SOLO", 1) != 0 && knob("EMTB200_CG_SLCOPY", 1) != 0 &&
+                      knob("EMTB200_CG_WARPMAJOR", 1) != 0 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && opt.mode != 2;
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
     g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;
     g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;
@@ -1969,12 +1975,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             for (int w = 0; w < G; ++w) {
                 rc << "    case " << w << ": {\n";
                 if (!wprefix.empty()) rc << wprefix[static_cast<size_t>(w)];
+                if (solo) rc << "      if (lane == 0) {\n";
                 std::vector<int> sw_ids;  // process id per swbits bit
                 std::vector<int> sw_tasks;  // task per swbits bit
                 std::string sw_lits;        // gated slim switch tests of this warp
                 for (size_t p = 0; p < sc.phases.size(); ++p) {
-                    if (p > 0) rc << mark(prof_base + 2 * static_cast<int>(p) - 2) << "      BAR();\n"
-                                  << mark(prof_base + 2 * static_cast<int>(p) - 1);
+                    if (p > 0) rc << mark(prof_base + 2 * static_cast<int>(p) - 2) << (solo ? "      }\n" : "") << "      BAR();\n"
+                                  << (solo ? "      if (lane == 0) {\n" : "") << mark(prof_base + 2 * static_cast<int>(p) - 1);
                     std::vector<int> ordered;
                     const auto segs = segments_of(sc.phases[p][static_cast<size_t>(w)], deps, g.tasks, ordered);
                     std::vector<int> seg_of(ordered.size(), -1);
@@ -2098,7 +2105,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         for (size_t q = 3; q < t.ck.size(); ++q)
                             nx << " { const double T_ = " << lctx.cst(t.ck[q]) << "; if (T_ > t && T_ < swnext) swnext = T_; }";
                     }
-                    rc << "      if (__any_sync(0xffffffffu, t >= swnext)) {\n" << sw_lits
+                    rc << (solo ? "      if (t >= swnext) {\n" : "      if (__any_sync(0xffffffffu, t >= swnext)) {\n") << sw_lits
                        << "        swnext = __longlong_as_double(0x7ff0000000000000LL);" << nx.str() << "\n      }\n";
                     sw_lits.clear();
                 }
@@ -2128,6 +2135,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                           "b &= b - 1; const int e = atomicAdd(a.n_events, 1); if (e < a.max_events) { a.events[3*e] = step; "
                           "a.events[3*e+1] = gl; a.events[3*e+2] = " << tab << "[j]; } } } }\n";
                 }
+                if (solo) rc << "      }\n";
                 if (!wsuffix.empty()) rc << wsuffix[static_cast<size_t>(w)];
                 rc << mark(prof_base + 2 * static_cast<int>(sc.phases.size()) - 2) << "    } break;\n";
             }
@@ -2440,7 +2448,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  double* __restrict__ A = a.arena + gl;\n"
       << "  const double* __restrict__ C = a.ctab + gl;\n"
       << "  (void)C;\n"
-      << "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+      << (solo ? "  if (warp == 0 && lane == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n"
+               : "  if (warp == 0) { S[0] = 0.0; serr[lane] = 0x7fffffff; needS[lane] = 0; }\n")
       << (g.lu_shared ? "  double* __restrict__ SH = sm + " + std::to_string(static_cast<long long>(g.smem_slots()) * LPC + LPC) +
                             ";  // shared factors: L, U, pivot reciprocals (one copy per CTA)\n"
                       : std::string())
@@ -2456,7 +2465,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         for (int q = 0; q + 1 < nhot; ++q)
             it.push_back({"S[" + std::to_string(static_cast<long long>(q + 1) * LPC) + "]",
                           "A[(size_t)" + std::to_string(g.hot_slots[static_cast<size_t>(q) + 1]) + " * W_]"});
-        o << warp_copies(it, G, "  ");
+        o << warp_copies(it, G, "  ", 16, solo);
     } else {
         o << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << g.vc_slots.size() << "; q += " << G << ") S[(" << g.vc_base << " + q) * " << LPC << "] = __ldg(C + (size_t)kVC[q] * W_);\n"
           << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") S[(q + 1) * " << LPC << "] = A[(size_t)kHot[q] * W_];\n";
@@ -2469,7 +2478,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         for (size_t q = 0; q < s.u_col.size(); ++q)
             it.push_back({"S[" + std::to_string((g.u_base_smem + static_cast<long long>(q)) * LPC) + "]",
                           "A[(size_t)" + std::to_string(s.u + static_cast<long long>(q)) + " * W_]"});
-        o << warp_copies(it, G, "  ");
+        o << warp_copies(it, G, "  ", 16, solo);
     } else if (lu_smem) {
         o << "  _Pragma(\"unroll 8\") for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") S[(" << g.l_base_smem << " + q) * " << LPC << "] = A[(size_t)("
           << s.l << " + q) * W_];\n";
@@ -2482,7 +2491,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             for (int i = 0; i < s.dim; ++i)
                 it.push_back({"S[" + std::to_string(static_cast<long long>(g.rcp_base + i) * LPC) + "]",
                               "1.0 / A[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_]"});
-            o << warp_copies(it, G, "  ");
+            o << warp_copies(it, G, "  ", 16, solo);
         } else if (g.rcp_base >= 0) {
             std::ostringstream dg;
             for (int i = 0; i < s.dim; ++i) dg << (i ? "," : "") << s.u_row_ptr[static_cast<size_t>(i)];
@@ -2504,7 +2513,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         for (int i = 0; i < s.dim; ++i)
             it.push_back({"SH[" + std::to_string(g.sh_rcp(i)) + "]",
                           "1.0 / a.arena[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_ + " + base + "]"});
-        o << warp_copies(it, G, "  ");
+        o << warp_copies(it, G, "  ", 16, solo);
     }
     // watch slots not rewritten by region-A tasks (the dirty flag) are checked up front
     std::set<int> written_a;
@@ -2577,7 +2586,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "    }\n"
 ;
     }
-    o       << "    if (warp == 0) { ";
+    o       << (solo ? "    if (warp == 0 && lane == 0) { " : "    if (warp == 0) { ");
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
     o << "}\n";
@@ -2590,7 +2599,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << code_a;
     o << "    if (__syncthreads_or(wflag | pfail)) {\n"
       << "      if (__syncthreads_or(pfail)) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
-      << "      if (warp == 0) {\n"
+      << (solo ? "      if (warp == 0 && lane == 0) {\n" : "      if (warp == 0) {\n")
       << (knob("EMTB200_CG_NOINLINE", 0) ? "        srow = emt_refactor(S, A, C, live, lane, needS);\n" : g.emit_refactor())
       << "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
       << "      }\n"
