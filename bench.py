@@ -2,23 +2,26 @@
 """Benchmark: IEEE-39 N-1 contingency sweep (BASELINE.json metric, config C3).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3|c5|c2|c4] [--scaling strong|weak]
 
-Workload: 1000 scenarios per GPU (46 breakers x 22 fault times 0.10-0.31 s,
-outage-major; sharding.n1_sweep — at N=1 exactly the BASELINE C3 sweep) of the
-synthetic IEEE 39-bus EMT case (n = 85 nodes, m = 149 components,
-dt = 50 us), in contiguous lane shards, one process per GPU under torchrun;
-weak scaling, no inter-GPU traffic but the final reductions / result gather. One bench "step" = one launch of
-the persistent step-loop kernel advancing every scenario by `--emt-steps`
-(default 1000) EMT passes, i.e. 50 ms of simulated time; the default K + W
-covers 1.15 s of simulated time.
+Workload: the BASELINE C3 sweep — 1000 scenarios (46 breakers x 22 fault times
+0.10-0.31 s, outage-major; sharding.n1_sweep) of the synthetic IEEE 39-bus EMT
+case (n = 85 nodes, m = 149 components, dt = 50 us) — in contiguous lane
+shards, one process per GPU under torchrun (strong scaling: 1000 scenarios in
+total; `--scaling weak` runs 1000 per GPU). No inter-GPU traffic but the final
+reductions / result gather. One bench "step" = one launch of the persistent
+step-loop kernel advancing every scenario by `--emt-steps` (default 1000) EMT
+passes, i.e. 50 ms of simulated time; the default K + W covers 1.15 s.
 
-value = total scenario-steps / max-over-ranks device time of the K timed
-launches (CUDA events on the engine's stream, L2 flushed between launches).
-e2e   = the same metric through the C ABI with HOST buffers: engine create
-(H2D of arena + constants + tables), advance, waveform D2H, per step.
-The reference arm (--impl reference) runs the reference library
-(oracle/_ref/libemtref.so, emtgrid::interpret) over lane shards on all host
-cores, as BASELINE.md §2 prescribes.
+value  = total scenario-steps / max-over-ranks device time of the K timed
+         launches (CUDA events on the engine's stream, L2 flushed between launches).
+e2e    = the same metric through the C ABI with HOST buffers (batch H2D from
+         pinned memory, S passes, waveform rows D2H), per step.
+parity = every sample of the device run (warm-up + timed passes, all lanes)
+         against the reference itself (oracle/_ref/libemtref.so, emtgrid::interpret
+         on lane shards; the C oracle for C4), which also gives cpu_baseline.
+The reference arm (--impl reference) runs the reference library over the same
+lanes and pass window on all host cores, as BASELINE.md §2 prescribes.
 """
 from __future__ import annotations
 
@@ -198,6 +201,9 @@ def run_ours(args):
     from paper_1903_01081_b200 import engine
 
     rank, world, local = dist_env()
+    if "DEVELOPER" in engine.lib().emt_version().decode() and not args.allow_dev_build:
+        raise SystemExit("bench.py: libemtb200.so is a developer build (EMTB200_* knobs live); rebuild with "
+                         "paper_1903_01081_b200/build.py --force or pass --allow-dev-build")
     if world > 1:
         # BENCH_DIST_BACKEND=gloo + BENCH_SHARE_GPU=1 lets the multi-rank control flow be
         # exercised with several ranks on one GPU (NCCL refuses duplicate devices)
@@ -214,9 +220,12 @@ def run_ours(args):
 
     from paper_1903_01081_b200 import sharding
     wl_name, _, _ = WORKLOADS[args.workload]
-    # weak scaling: `--scenarios` per GPU, contiguous shards; C4 is ONE system of
-    # `--scenarios` line-coupled copies split over the GPUs (strong scaling)
-    W = args.scenarios if args.workload == "c4" else args.scenarios * world
+    # strong scaling (default, BASELINE C3 "1000 scenarios sharded over 1/2/4/8"): the
+    # `--scenarios` lanes are split into contiguous shards, one per GPU; weak scaling
+    # (`--scaling weak`): `--scenarios` per GPU. C4 is ONE system of `--scenarios`
+    # line-coupled copies split over the GPUs (always strong).
+    weak = args.scaling == "weak" and args.workload != "c4"
+    W = args.scenarios * world if weak else args.scenarios
     lo, hi = sharding.shard_bounds(W, world, rank)
     batch, info = build_batch(W, lo, hi, args.workload)
     S = args.emt_steps
@@ -264,6 +273,8 @@ def run_ours(args):
     launches_timed = st.kernel_launches - launches0
     last = eng.waves(total_steps - S, S).values
     fc_local, steps_local = st.factor_count, eng.refactor_steps()
+    # every pass of the run (warm-up + timed) for the parity check against the reference
+    all_waves = eng.waves(0, total_steps).values if (world == 1 and not args.skip_cpu) else None
 
     # ---- e2e through the public API with HOST buffers, rank-local shard. The engine
     # (schedule parse + code generation + JIT, the analogue of compile_task, which the
@@ -368,7 +379,8 @@ def run_ours(args):
         if os.path.exists(tp):  # ncu --set full capture of the same kernel (tools/ncu_summary.py), per EMT step
             per_step = json.load(open(tp)).get("dram_bytes_per_emt_step")
             traffic = per_step * S * lanes_local / json.load(open(tp)).get("lanes", lanes_local) if per_step else None
-        cpu = cpu_baseline(args) if (world == 1 and not args.skip_cpu) else None
+        cpu, par = cpu_baseline(args, batch, all_waves, total_steps) if all_waves is not None else (None, None)
+        del all_waves
         h2d = batch.const_table.nbytes + batch.initial.nbytes  # per bench step (S passes)
         d2h = S * len(info.channels) * (hi - lo) * 8
         metric, unit, hib, val, e2e_val = (METRIC[args.workload], "scenario-steps/s", True, value, W * S / e2e_max)
@@ -384,14 +396,15 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": max_ms / args.steps,
             "higher_is_better": hib,
-            "scaling": "strong" if args.workload == "c4" else "weak",
+            "scaling": "weak" if weak else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": wl_name, "scenarios": W, "scenarios_per_gpu": args.scenarios,
+            "config": {"workload": wl_name, "scenarios": W, "scenarios_per_gpu": hi - lo,
                        "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
                        "components": info.comps, "case": WORKLOADS[args.workload][1],
-                       "parallelism": f"scenario lanes sharded over {world} GPU(s), no per-step traffic",
+                       "parallelism": f"{W} scenario lanes in contiguous shards over {world} GPU(s), no per-step "
+                                      "traffic" if args.workload != "c4" else f"{W} line-coupled copies split over {world} GPU(s)",
                        "l2": "flushed (256 MiB write) between timed launches"},
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "matches_device_run": e2e_digest_ok,
@@ -426,6 +439,8 @@ def run_ours(args):
                                     "note": "the solve is one part of the pass: the kernel as a whole is in 'roofline'"}
         if cpu is not None:
             out["cpu_baseline"] = cpu
+        if par is not None:
+            out["parity"] = par
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -433,82 +448,71 @@ def run_ours(args):
 
 # ----------------------------------------------------------------- reference (CPU) arm
 
-def _ref_worker(args_tuple):
-    text, init, steps, warmup = args_tuple
-    from oracle import ref
-    r = ref.execute(text, init, warmup + steps, warmup=warmup)
-    return r.measured_seconds  # step loop after warm-up (ExecStats, proj/src/exec.cpp:375-381)
-
-
-def _shard(batch, lo, hi):
-    from paper_1903_01081_b200 import schedule as sch
-    ct = batch.const_table[:, lo:hi]
-    ext = batch.initial.size // batch.width
-    init = batch.initial.reshape(ext, batch.width)[:, lo:hi].reshape(-1)
-    return sch.widen_text(batch.schedule, ct), np.ascontiguousarray(init)
-
-
-def reference_measure(scenarios: int, emt_steps: int, warmup_emt: int, procs: int, workload: str = "c3"):
-    """emtgrid::interpret (the reference, unmodified) on contiguous lane shards, one
-    process per host core; returns (lanes, max step-loop seconds)."""
-    import multiprocessing as mp
-    batch, info = build_batch(scenarios, workload=workload)
-    W = batch.width
-    procs = max(1, min(procs, W))
-    bounds = [(p * W // procs, (p + 1) * W // procs) for p in range(procs)]
-    jobs = []
-    for lo, hi in bounds:
-        text, init = _shard(batch, lo, hi)
-        jobs.append((text, init, emt_steps, warmup_emt))
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs) as pool:
-        res = pool.map(_ref_worker, jobs)
-    return W, max(res), procs
-
-
-def oracle_measure(scenarios: int, emt_steps: int, workload: str):
-    """C4 has no reference path (the reference has no line model): time the C
-    restatement (oracle/emt_oracle.c, the parity checker) on the whole coupled
-    system, one thread — the lanes are one system, so they cannot be sharded."""
-    from oracle import oracle
-    batch, info = build_batch(scenarios, workload=workload)
+def oracle_run(batch, steps: int, got=None):
+    """C4 has no reference path (the reference has no line model): the C restatement
+    (oracle/emt_oracle.c, the parity checker) on the whole coupled system, one thread —
+    the copies are one system, so they cannot be sharded. Returns (seconds, parity)."""
+    from oracle import oracle, parity
     sched = oracle.Schedule(batch.text())
     sched.interpret(batch.initial, 20)  # warm-up
     t0 = time.perf_counter()
-    sched.interpret(batch.initial, emt_steps)
-    return batch.width, time.perf_counter() - t0
+    r = sched.interpret(batch.initial, steps)
+    secs = time.perf_counter() - t0
+    rep = parity.merge([parity.compare(got, r.waves)]) if got is not None else None
+    return secs, rep
 
 
-def cpu_baseline(args):
+def cpu_baseline(args, batch, got, total_steps):
+    """The reference on the box's host cores over the SAME lanes and passes the device
+    just ran (warm-up + timed launches), timed over the timed passes, and every sample
+    of the device run checked against it (oracle/parity.py). Returns (cpu_baseline, parity)."""
+    from oracle import parity
+    S = args.emt_steps
+    W = batch.width
     if args.workload == "c4":
-        steps = 2000
-        W, secs = oracle_measure(args.scenarios, steps, "c4")
-        return {"value": 1e6 * secs / steps, "unit": "us/step", "cores": 1, "kind": "port",
-                "sample": f"{W}-copy line-coupled system x {steps} EMT steps, oracle/emt_oracle.c interpret "
-                          "(the reference has no line model), single thread"}
-    steps = args.cpu_emt_steps if args.workload != "c2" else 20000
-    W, secs, procs = reference_measure(args.scenarios, steps, 20, os.cpu_count() or 1, args.workload)
+        secs, rep = oracle_run(batch, total_steps, got)
+        rep.update({"against": "oracle/emt_oracle.c interpret (the reference has no line model)",
+                    "lanes": W, "passes": total_steps})
+        return ({"value": 1e6 * secs / total_steps, "unit": "us/step", "cores": 1, "kind": "port",
+                 "sample": f"{W}-copy line-coupled system x {total_steps} EMT steps, oracle/emt_oracle.c "
+                           "interpret (the reference has no line model), single thread"}, rep)
+    res = parity.reference_sweep(batch, total_steps, got=got, warmup=S * args.warmup)
+    rep = res["parity"]
+    rep.update({"against": "reference emtgrid::interpret (oracle/_ref/libemtref.so) on lane shards",
+                "lanes": W, "passes": total_steps})
+    timed = S * args.steps
     if args.workload == "c2":
-        return {"value": 1e6 * secs / steps, "unit": "us/step", "cores": 1, "kind": "reference",
-                "sample": f"1 scenario x {steps} EMT steps (after 20 warm-up), emtgrid::interpret "
-                          "(oracle/_ref/libemtref.so), single thread"}
-    return {"value": W * steps / secs, "unit": "scenario-steps/s", "cores": procs, "kind": "reference",
-            "sample": f"{W} scenarios x {steps} EMT steps (after 20 warm-up), emtgrid::interpret on "
-                      f"{procs} contiguous lane shards, one process per core (oracle/_ref/libemtref.so)"}
+        cpu = {"value": 1e6 * res["seconds"] / timed, "unit": "us/step", "cores": 1, "kind": "reference",
+               "sample": f"1 scenario x {total_steps} EMT steps ({S * args.warmup} warm-up), emtgrid::interpret "
+                         "(oracle/_ref/libemtref.so), single thread"}
+    else:
+        cpu = {"value": W * timed / res["seconds"], "unit": "scenario-steps/s", "cores": res["procs"],
+               "kind": "reference",
+               "sample": f"{W} scenarios x {total_steps} EMT steps (the device run's passes; {S * args.warmup} "
+                         f"warm-up outside the clock), emtgrid::interpret on {res['procs']} contiguous lane "
+                         "shards, one process per core (oracle/_ref/libemtref.so)"}
+    return cpu, rep
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation on the same workload,
+    lanes and pass window as our arm (S passes per bench step, W warm-up + K timed steps)."""
     rank, world, local = dist_env()
     if rank != 0:
         return
-    S = args.cpu_emt_steps_per_step
+    from oracle import parity
+    S = args.cpu_emt_steps_per_step or args.emt_steps
+    weak = args.scaling == "weak" and args.workload != "c4"
+    W0 = args.scenarios * world if weak else args.scenarios
+    batch, info = build_batch(W0, workload=args.workload)
     kind = "reference"
     if args.workload == "c4":
         kind, procs = "port", 1
-        W, secs = oracle_measure(args.scenarios, S * args.steps, "c4")
+        secs, _ = oracle_run(batch, S * args.steps)
+        W = batch.width
     else:
-        W, secs, procs = reference_measure(args.scenarios * world, S * args.steps, S * args.warmup,
-                                           os.cpu_count() or 1, args.workload)
+        res = parity.reference_sweep(batch, S * (args.warmup + args.steps), warmup=S * args.warmup)
+        W, secs, procs = batch.width, res["seconds"], res["procs"]
     metric, unit, hib, value = METRIC[args.workload], "scenario-steps/s", True, W * S * args.steps / secs
     if args.workload in ("c2", "c4"):
         metric, unit, hib, value = METRIC[args.workload], "us/step", False, 1e6 * secs / (S * args.steps)
@@ -517,16 +521,17 @@ def run_reference(args):
         "metric": metric,
         "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": hib,
-        "scaling": "strong" if args.workload == "c4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": args.scenarios,
-                   "emt_steps_per_bench_step": S,
+        "config": {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": W // world,
+                   "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
+                   "components": info.comps, "case": WORKLOADS[args.workload][1],
                    "parallelism": f"{procs} host processes over contiguous lane shards"},
         "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": kind,
                          "sample": f"{W} {'copies' if kind == 'port' else 'scenarios'} x {S} EMT steps per bench "
-                                   f"step ({args.warmup} warm-up + {args.steps} timed), "
+                                   f"step ({args.warmup} warm-up + {args.steps} timed, the passes our arm times), "
                                    + ("oracle/emt_oracle.c (no reference line model), one thread" if kind == "port"
-                                      else "emtgrid::interpret")},
+                                      else "emtgrid::interpret (oracle/_ref/libemtref.so)")},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -540,18 +545,22 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3",
                     help="c3 = IEEE-39 N-1 sweep (headline), c5 = feeder PV shared-G sweep, c2 = single scenario")
-    ap.add_argument("--scenarios", type=int, default=None, help="scenarios per GPU (weak scaling)")
+    ap.add_argument("--scenarios", type=int, default=None,
+                    help="scenarios in total (strong scaling) or per GPU (--scaling weak)")
     ap.add_argument("--emt-steps", type=int, default=1000, help="EMT passes per bench step (one launch)")
-    ap.add_argument("--cpu-emt-steps", type=int, default=8000, help="EMT passes in the cpu_baseline sample")
-    ap.add_argument("--cpu-emt-steps-per-step", type=int, default=200,
-                    help="EMT passes per bench step in the reference arm")
+    ap.add_argument("--cpu-emt-steps-per-step", type=int, default=0,
+                    help="EMT passes per bench step in the reference arm (0 = --emt-steps, the same window)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: --scenarios lanes in total, sharded over the GPUs (BASELINE C3); "
+                         "weak: --scenarios lanes per GPU")
     ap.add_argument("--e2e-chunk", type=int, default=1000, help="passes per launch in the e2e streaming run")
     ap.add_argument("--kernel", choices=["auto", "specialised", "generic"], default="auto")
     ap.add_argument("--warps", type=int, default=0, help="specialised kernel: warps per 32-lane group (0 = auto)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--tensor-solve", action="store_true",
                     help="shared-G batches (C5): V = G^-1 I on the FP64 tensor cores (amplitude-relative parity)")
-    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true", help="no cpu_baseline / parity leg")
+    ap.add_argument("--allow-dev-build", action="store_true", help="run on a developer build (knobs live)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

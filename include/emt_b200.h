@@ -268,6 +268,14 @@ emt_status emt_waves_to_text(const char* const* channel_names, int32_t channels,
                              char** out, int64_t* out_len);
 void emt_free(void* ptr);
 
+/* ---- source waveform function ---- */
+
+/* y[i] = cos(x[i]) as the device evaluates it for AC sources (kern::source_value,
+ * proj/include/emtgrid/kernels.hpp:68-70): glibc's cos, operation for operation
+ * (csrc/libmcos.cuh), so bit-identical to the reference's std::cos. Host buffers;
+ * for verification of a box's libm against the device. */
+emt_status emt_source_cos(int32_t device, const double* x, double* y, int64_t n);
+
 /* Library build string (arch, flags). */
 const char* emt_version(void);
 

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libemtb200.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_schedule.cpp", "codegen.cpp", "jit.cpp", "waveform_text.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("host_schedule.hpp", "codegen.hpp", "jit.hpp")] + [
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("host_schedule.hpp", "codegen.hpp", "jit.hpp", "libmcos.cuh")] + [
     os.path.join(ROOT, "include", "emt_b200.h")]
 CUDA = "/usr/local/cuda"
 
@@ -43,10 +43,12 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
+    """dev=True: a developer build whose generator reads EMTB200_CG_* A/B knobs from the
+    environment (the product build ignores the environment; bench.py refuses a dev build)."""
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SOURCES]
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-DEMTB200_DEV_KNOBS"] if dev else []), "-o", LIB, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
@@ -55,5 +57,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    build(force="--force" in sys.argv or "--dev" in sys.argv, verbose=True, dev="--dev" in sys.argv)
     print(LIB)

@@ -32,9 +32,44 @@ namespace emtb200 {
 
 namespace {
 
+// glibc's cos, operation for operation (libmcos.cuh), pasted into every generated source
+#define EMT_LIBMCOS_TEXT(...) const char* const kLibmCosSrc = #__VA_ARGS__;
+#include "libmcos.cuh"
+#undef EMT_LIBMCOS_TEXT
+
+std::string libm_cos_prelude() {
+    return std::string("__device__ __forceinline__ int emt_lo32(double d) { return __double2loint(d); }\n"
+                       // pivot reciprocal for the guarded Markstein division: NaN outside [2^-960, 2^960]
+                       "#define EMT_RCP(u) ((fabs(u) >= 0x1p-960 && fabs(u) <= 0x1p960) ? 1.0 / (u) : "
+                       "__longlong_as_double(0x7ff8000000000000LL))\n"
+                       "#define EMT_HD __device__ __forceinline__\n#define EMT_TABLE __device__ const\n") +
+           kLibmCosSrc + "\n";
+}
+
+// Generator tuning knobs. The product library ignores the environment: knob()
+// returns the measured-best default. A developer build (build.py --dev, which
+// defines EMTB200_DEV_KNOBS) reads EMTB200_CG_* overrides for A/B experiments,
+// and the engine summary then lists every override in effect.
+#ifdef EMTB200_DEV_KNOBS
+std::string g_knobs_used;
 int knob(const char* name, int dflt) {
     const char* v = std::getenv(name);
-    return v && *v ? std::atoi(v) : dflt;
+    if (!(v && *v)) return dflt;
+    const int x = std::atoi(v);
+    if (x != dflt && g_knobs_used.find(name) == std::string::npos)
+        g_knobs_used += std::string(g_knobs_used.empty() ? "" : ",") + name + "=" + v;
+    return x;
+}
+#else
+int knob(const char*, int dflt) { return dflt; }
+#endif
+
+std::string dev_knob_note() {
+#ifdef EMTB200_DEV_KNOBS
+    return " devbuild" + (g_knobs_used.empty() ? std::string() : " knobs=" + g_knobs_used);
+#else
+    return std::string();
+#endif
 }
 
 std::string lit(double v) {
@@ -111,7 +146,10 @@ struct Gen {
     int pre_base = 0;
     // pivot reciprocals 1/u_ii in shared memory (rcp_base + row): the backward sweep's
     // division becomes q0 = x*r, x/u = fma(fma(-u, q0, x), r, q0) (Markstein; correctly
-    // rounded for normal-range operands, tools/micro/divcheck.c)
+    // rounded for normal-range operands, tools/micro/divcheck.c). Range guard: the
+    // reciprocal is stored as NaN when |u| leaves [2^-960, 2^960] (EMT_RCP), and a row
+    // whose q0 is NaN, zero, subnormal-bound or huge takes IEEE x / u instead, so the
+    // result is x / u bit for bit everywhere (tests/golden/subnormal_decay).
     bool rcp = false;
     int rcp_base = -1;
     // shared factors: when G is the same constant matrix in every lane and nothing
@@ -859,8 +897,8 @@ struct Gen {
             for (int k = ub; k < ue; ++k) {
                 const int c = s.u_col[static_cast<size_t>(k)];
                 o << "          u" << k << " = w" << c << "; " << Uw(k, "u" + std::to_string(k));
-                if (k == ub && rcp_base >= 0) o << " S[" << (rcp_base + i) * ls << "] = 1.0 / u" << k << ";";
-                if (k == ub && lu_shared) o << " SH[" << sh_rcp(i) << "] = 1.0 / u" << k << ";";
+                if (k == ub && rcp_base >= 0) o << " S[" << (rcp_base + i) * ls << "] = EMT_RCP(u" << k << ");";
+                if (k == ub && lu_shared) o << " SH[" << sh_rcp(i) << "] = EMT_RCP(u" << k << ");";
                 o << "\n";
             }
             for (int c : cols)
@@ -1076,9 +1114,9 @@ const KindCode kCode[K_NKINDS] = {
     /*SRL*/ {"const double vs@ = LD({I1}) - LD({I0}); const double ip@ = LD({I2}); const double g@ = {C0}; const double d@ = {C1};",
              "const double h@ = d@ * ip@ + g@ * vs@;", "ST({I3}, h@);"},
     /*VSRC*/ {"const double g@ = {C0}; const double m@ = {C1}; const double w@ = {C2}; const double p@ = {C3};",
-              "const double h@ = g@ * (w@ == 0.0 ? m@ : m@ * cos(w@ * t + p@));", "ST({I0}, h@);"},
+              "const double h@ = g@ * (w@ == 0.0 ? m@ : m@ * emt_libm_cos(w@ * t + p@));", "ST({I0}, h@);"},
     /*ISRC*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
-              "const double h@ = w@ == 0.0 ? m@ : m@ * cos(w@ * t + p@);", "ST({I0}, h@);"},
+              "const double h@ = w@ == 0.0 ? m@ : m@ * emt_libm_cos(w@ * t + p@);", "ST({I0}, h@);"},
     /*CSRC*/ {"const double k@ = {C0}; const double x@ = LD({I1});", "const double h@ = k@ * x@;", "ST({I0}, h@);"},
     /*SW*/ {nullptr, nullptr, nullptr},
     /*GATHER*/ {nullptr, nullptr, nullptr},
@@ -1121,7 +1159,7 @@ const KindCode kCode[K_NKINDS] = {
     /*VSRCP*/ {"const double g@ = {C0}; const double v@ = LD({I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
     /*ISRCP*/ {"const double v@ = LD({I1});", "", "ST({I0}, v@);"},
     /*SRCPRE*/ {"const double m@ = {C0}; const double w@ = {C1}; const double p@ = {C2};",
-               "const double v@ = m@ * cos(w@ * tn + p@);", "ST({I0}, v@);"},
+               "const double v@ = w@ == 0.0 ? m@ : m@ * emt_libm_cos(w@ * tn + p@);", "ST({I0}, v@);"},
     // sources read from the launch's value table (emt_src_kernel computes m*cos(w t + p))
     /*VSRCT*/ {"const double g@ = {C0}; const double v@ = SRCV_({I1});", "const double h@ = g@ * v@;", "ST({I0}, h@);"},
     /*ISRCT*/ {"const double v@ = SRCV_({I1});", "", "ST({I0}, v@);"},
@@ -1349,7 +1387,8 @@ std::string task_literal(const Task& t, const LitCtx& c) {
                 if (t.f.size() > 3 && (t.f[3] >= 0 || t.f[3] <= -2))
                     o << "{ const double r_ = " << (t.f[3] >= 0 ? "LD(" + std::to_string(t.f[3]) + ")" : "SH[" + std::to_string(c.sh_rcp0 - t.f[3] - 2) + "]")
                       << "; const double d_ = " << lu(t.f[1])
-                      << "; const double q_ = x * r_; x = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); } "
+                      << "; const double q_ = x * r_; double m_ = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); "
+                         "if (__builtin_expect(!(fabs(q_) >= 0x1p-960 && fabs(q_) <= 0x1p960), 0)) m_ = x / d_; x = m_; } "
                       << (c.dsum ? "dsum = dsum + fabs(x); " : "dok = dok & (fabs(x) <= dlim); ");
                 else
                     o << "x = x / " << lu(t.f[1]) << "; dok = dok & (fabs(x) <= dlim); ";
@@ -2212,13 +2251,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     in_region_a = false;
     wprefix.clear();
-    if (knob("EMTB200_CG_EXP_SKIPA", 0)) code_a = "";  // timing experiment only: wrong numerics
-    if (knob("EMTB200_CG_EXP_SAMEA", 0)) {  // timing experiment only: every warp runs warp 0's region-A code
-        const std::string a0 = region_code(sa, true);
-        const size_t b0 = a0.find("    case 0: {"), c1 = a0.find("    case 1: {", b0);
-        const size_t e0 = a0.rfind("} break;", c1);
-        code_a = "    {\n" + a0.substr(b0 + 13, e0 - b0 - 13) + "    }\n";
-    }
     bool has_lines = false;
     for (const Task& t : g.tasks) has_lines = has_lines || t.kind == K_BERG;
     // measured slower (C4 3.37 -> 3.77 us: the acquire fence stalls that warp ~1000
@@ -2270,8 +2302,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         std::ostringstream pp;
         pp << "  if (warp == 0) { const double tn = (double)(a.step0 + 1) * " << lit(s.dt) << ";\n";
         for (size_t j = 0; j < g.pre_ck.size(); ++j)
-            pp << "    S[" << (g.pre_base + static_cast<int>(j)) * LPC << "] = " << g.C(g.pre_ck[j][0]) << " * cos(" << g.C(g.pre_ck[j][1])
-               << " * tn + " << g.C(g.pre_ck[j][2]) << ");\n";
+            pp << "    { const double m_ = " << g.C(g.pre_ck[j][0]) << ", w_ = " << g.C(g.pre_ck[j][1]) << ", p_ = "
+               << g.C(g.pre_ck[j][2]) << "; S[" << (g.pre_base + static_cast<int>(j)) * LPC
+               << "] = w_ == 0.0 ? m_ : m_ * emt_libm_cos(w_ * tn + p_); }\n";
         pp << "  }\n";
         pre_prologue = pp.str();
     }
@@ -2364,6 +2397,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
     }
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
+    o << libm_cos_prelude();
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
       << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab;\n"
@@ -2410,7 +2444,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // barrier form is the one the PTX ISA allows there (compute-sanitizer synccheck clean)
     if (knob("EMTB200_CG_ALIGNEDBAR", 0)) o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
     else o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
-    if (knob("EMTB200_CG_FAKECOS", 0)) o << "#define cos(x) (x)\n";  // timing experiment only: wrong numerics
     o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
@@ -2490,14 +2523,14 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             std::vector<std::pair<std::string, std::string>> it;
             for (int i = 0; i < s.dim; ++i)
                 it.push_back({"S[" + std::to_string(static_cast<long long>(g.rcp_base + i) * LPC) + "]",
-                              "1.0 / A[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_]"});
+                              "EMT_RCP(A[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_])"});
             o << warp_copies(it, G, "  ", 16, solo);
         } else if (g.rcp_base >= 0) {
             std::ostringstream dg;
             for (int i = 0; i < s.dim; ++i) dg << (i ? "," : "") << s.u_row_ptr[static_cast<size_t>(i)];
             o << "  { const int kUd[" << s.dim << "] = {" << dg.str() << "};\n"
-              << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = 1.0 / A[(size_t)("
-              << s.u << " + kUd[q]) * W_]; }\n";
+              << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.dim << "; q += " << G << ") S[(" << g.rcp_base << " + q) * " << LPC << "] = EMT_RCP(A[(size_t)("
+              << s.u << " + kUd[q]) * W_]); }\n";
         }
     }
     if (g.lu_shared) {
@@ -2512,7 +2545,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             it.push_back({"SH[" + std::to_string(nl + q) + "]", "a.arena[(size_t)" + std::to_string(s.u + static_cast<long long>(q)) + " * W_ + " + base + "]"});
         for (int i = 0; i < s.dim; ++i)
             it.push_back({"SH[" + std::to_string(g.sh_rcp(i)) + "]",
-                          "1.0 / a.arena[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_ + " + base + "]"});
+                          "EMT_RCP(a.arena[(size_t)" + std::to_string(s.u + s.u_row_ptr[static_cast<size_t>(i)]) + " * W_ + " + base + "])"});
         o << warp_copies(it, G, "  ", 16, solo);
     }
     // watch slots not rewritten by region-A tasks (the dirty flag) are checked up front
@@ -2563,8 +2596,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             o << "      asm volatile(\"barrier.arrive 1, " << 32 * (n_berg_sync + 1) << ";\" ::: \"memory\");\n";
         o << "    }\n";
     } else {
-        o << (knob("EMTB200_CG_EXP_NOPOLL", 0) ? "    if (false) {\n"  // timing experiment only: unsynchronised line coupling
-                                               : "    if (a.progress != nullptr && s_cmin < step + 2 + pfok - a.min_k) {\n")
+        o << "    if (a.progress != nullptr && s_cmin < step + 2 + pfok - a.min_k) {\n"
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
       << "      __syncthreads();\n"
@@ -2768,8 +2800,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "  const double* C = ctab + ln; (void)C;\n"
           << "  double v = 0.0;\n  switch (j) {\n";
         for (size_t j = 0; j < g.tab_ck.size(); ++j)
-            o << "    case " << j << ": v = " << g.C(g.tab_ck[j][0]) << " * cos(" << g.C(g.tab_ck[j][1]) << " * t + "
-              << g.C(g.tab_ck[j][2]) << "); break;\n";
+            o << "    case " << j << ": { const double m_ = " << g.C(g.tab_ck[j][0]) << ", w_ = " << g.C(g.tab_ck[j][1])
+              << ", p_ = " << g.C(g.tab_ck[j][2]) << "; v = w_ == 0.0 ? m_ : m_ * emt_libm_cos(w_ * t + p_); } break;\n";
         o << "  }\n  tab[i] = v;\n}\n";
     }
     out.source = o.str();
@@ -2791,7 +2823,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         << " const=" << const_bytes << " phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
         << " est_span=" << static_cast<long>(span_a + span_b + span_c) << " est_work=" << work
         << (g.dmma ? " solve=dmma(G^-1 " + std::to_string(s.dim) + "x" + std::to_string(s.dim) + ")" : std::string(opt.tensor_solve ? " solve=lu(shared-G ineligible)" : ""));
-    out.summary = sum.str();
+    out.summary = sum.str() + dev_knob_note();
     return true;
 }
 
@@ -2827,8 +2859,8 @@ const char* ts_body(int kind) {
         case K_IND: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; S[RI(3)] = ip + g * vs;";
         case K_CAP: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; S[RI(3)] = -ip - g * vs;";
         case K_SRL: return "const double vs = S[RI(1)] - S[RI(0)]; const double ip = S[RI(2)]; const double g = S[KS(0)]; const double d = S[KS(1)]; S[RI(3)] = d * ip + g * vs;";
-        case K_VSRC: return "const double g = S[KS(0)]; const double m = S[KS(1)]; const double w = S[KS(2)]; const double p = S[KS(3)]; S[RI(0)] = g * (w == 0.0 ? m : m * cos(w * t + p));";
-        case K_ISRC: return "const double m = S[KS(0)]; const double w = S[KS(1)]; const double p = S[KS(2)]; S[RI(0)] = w == 0.0 ? m : m * cos(w * t + p);";
+        case K_VSRC: return "const double g = S[KS(0)]; const double m = S[KS(1)]; const double w = S[KS(2)]; const double p = S[KS(3)]; S[RI(0)] = g * (w == 0.0 ? m : m * emt_libm_cos(w * t + p));";
+        case K_ISRC: return "const double m = S[KS(0)]; const double w = S[KS(1)]; const double p = S[KS(2)]; S[RI(0)] = w == 0.0 ? m : m * emt_libm_cos(w * t + p);";
         case K_CSRC: return "const double k = S[KS(0)]; const double x = S[RI(1)]; S[RI(0)] = k * x;";
         case K_FINC: return "const double vs = S[RI(3)] - S[RI(2)]; const double h = S[RI(1)]; const double g = S[KS(0)]; S[RI(0)] = g * vs + h;";
         case K_FINS: return "const double vs = S[RI(3)] - S[RI(2)]; const double h = S[RI(1)]; const double g = S[RI(4)]; S[RI(0)] = g * vs + h;";
@@ -3043,6 +3075,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << " lanes (one CTA each), " << G << " warps, " << nt << " tasks, " << waves.size() << " waves\n";
     o << "#define W_ " << static_cast<long long>(lanes) << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ "
       << opt.lane_begin << "LL\n";
+    o << libm_cos_prelude();
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
       << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab;\n"
@@ -3157,7 +3190,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
     sum << "task-simt tasks=" << nt << " waves=" << waves.size() << " slots=" << nslots << " smem=" << out.smem_bytes
         << " rec=" << rec.size() * 4 << "B phasesA=" << sa.phases.size() << " phasesB=" << sb.phases.size() << " warps=" << G
         << " est_span=" << static_cast<long>(span_a + span_b);
-    out.summary = sum.str();
+    out.summary = sum.str() + dev_knob_note();
     return true;
 }
 

@@ -33,6 +33,17 @@
 
 namespace emtb200 {
 
+// Engine-side developer switches (kernel forcing, profiling counters, line-coupling
+// mode): read only in a developer build (build.py --dev), like the generator knobs.
+inline const char* dev_env(const char* name) {
+#ifdef EMTB200_DEV_KNOBS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr double kDefaultDivergence = 1e12;  // kDivergenceLimit, kernels.hpp:24
 
@@ -118,9 +129,24 @@ struct DevPlan {
 
 __device__ __forceinline__ double rd(const double* A, int slot) { return slot < 0 ? 0.0 : A[slot]; }
 
+// glibc's cos, operation for operation (libmcos.cuh): the reference's std::cos bits
+__device__ __forceinline__ int emt_lo32(double d) { return __double2loint(d); }
+#define EMT_LIBMCOS_TEXT(...) __VA_ARGS__
+#define EMT_HD __device__ __forceinline__
+#define EMT_TABLE __device__ const
+#include "libmcos.cuh"
+#undef EMT_LIBMCOS_TEXT
+#undef EMT_HD
+#undef EMT_TABLE
+
+__global__ void emt_cos_kernel(const double* __restrict__ x, double* __restrict__ y, long long n) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = emt_libm_cos(x[i]);
+}
+
 // kern::source_value (proj/include/emtgrid/kernels.hpp:68-70)
 __device__ __forceinline__ double source_value(double mag, double omega, double phase, double t) {
-    return omega == 0.0 ? mag : mag * cos(omega * t + phase);
+    return omega == 0.0 ? mag : mag * emt_libm_cos(omega * t + phase);
 }
 
 // One non-singleton process for this lane: Engine::run_proc, proj/src/exec.cpp:77-311.
@@ -827,7 +853,11 @@ extern "C" {
 const char* emt_last_error(void) { return g_last_error.c_str(); }
 
 const char* emt_version(void) {
+#ifdef EMTB200_DEV_KNOBS
+    return "emtb200 persistent-warp engine; sm_100a; -fmad=false; DEVELOPER BUILD (EMTB200_* environment knobs live)";
+#else
     return "emtb200 persistent-warp engine; sm_100a; -fmad=false";
+#endif
 }
 
 emt_status emt_engine_create(const char* schedule_text, const double* const_table, int32_t width,
@@ -866,7 +896,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     }
     e->kernel_mode = EMT_KERNEL_GENERIC;
     e->summary = "generic table-driven kernel, grid=" + std::to_string(e->grid) + " block=" + std::to_string(e->block);
-    const char* kenv = std::getenv("EMTB200_KERNEL");
+    const char* kenv = dev_env("EMTB200_KERNEL");
     if (c.kernel == EMT_KERNEL_AUTO && kenv && std::strcmp(kenv, "tsimt") == 0) c.kernel = EMT_KERNEL_TSIMT;
     if (c.kernel == EMT_KERNEL_TSIMT) {
         CodegenOptions opt;
@@ -884,7 +914,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
             log = "cuFuncSetAttribute(max dynamic smem) failed";
         }
         if (ok) {  // record tables are read through L1: leave it most of the SRAM
-            const int carve = std::getenv("EMTB200_TS_CARVEOUT") ? std::atoi(std::getenv("EMTB200_TS_CARVEOUT")) : 25;
+            const int carve = dev_env("EMTB200_TS_CARVEOUT") ? std::atoi(dev_env("EMTB200_TS_CARVEOUT")) : 25;
             driver()->FuncSetAttribute(e->jit.function, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carve);
         }
         if (!ok)
@@ -920,7 +950,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         }
         if (ok) {
             e->kernel_mode = EMT_KERNEL_SPECIALISED;
-            const char* pf = std::getenv("EMTB200_CG_PROF");
+            const char* pf = dev_env("EMTB200_CG_PROF");
             if (pf && std::strcmp(pf, "0") != 0) {
                 CUDA_TRY(cudaMalloc(&e->d_prof, 32 * 64 * sizeof(long long)));
                 CUDA_TRY(cudaMemset(e->d_prof, 0, 32 * 64 * sizeof(long long)));
@@ -930,7 +960,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
             // be co-resident: one 32-lane CTA per SM at most).
             int sms = 0;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device);
-            const char* pe = std::getenv("EMTB200_LINE_PERSISTENT");
+            const char* pe = dev_env("EMTB200_LINE_PERSISTENT");
             if (e->plan.ring != nullptr && e->max_chunk != INT_MAX && cta_count(e.get()) <= sms &&
                 !(pe && std::strcmp(pe, "0") == 0)) {
                 CUDA_TRY(cudaMalloc(&e->d_progress, sizeof(unsigned int) * static_cast<size_t>(cta_count(e.get()))));
@@ -1337,6 +1367,24 @@ emt_status emt_ipc_open(int32_t device, const void* handle, void** ptr) {
 
 emt_status emt_ipc_close(void* ptr) {
     CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return EMT_OK;
+}
+
+emt_status emt_source_cos(int32_t device, const double* x, double* y, int64_t n) {
+    if (n < 0 || (n > 0 && (x == nullptr || y == nullptr))) return set_error(EMT_NON_POSITIVE_INPUT, "bad arguments");
+    if (n == 0) return EMT_OK;
+    CUDA_TRY(cudaSetDevice(device));
+    double* d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, 2 * static_cast<size_t>(n) * sizeof(double)));
+    cudaError_t rc = cudaMemcpy(d, x, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice);
+    if (rc == cudaSuccess) {
+        const long long blocks = std::min<long long>((n + 255) / 256, 148LL * 8);
+        emt_cos_kernel<<<static_cast<unsigned>(blocks), 256>>>(d, d + n, n);
+        rc = cudaGetLastError();
+    }
+    if (rc == cudaSuccess) rc = cudaMemcpy(y, d + n, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (rc != cudaSuccess) return set_error(EMT_CUDA_ERROR, std::string("emt_source_cos: ") + cudaGetErrorString(rc));
     return EMT_OK;
 }
 

@@ -134,6 +134,7 @@ def lib():
                                   ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_char_p)]
         L.emt_waves_to_text.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int32, ctypes.c_int32, dp, dp,
                                         ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int64)]
+        L.emt_source_cos.argtypes = [ctypes.c_int32, dp, dp, ctypes.c_int64]
         L.emt_free.argtypes = [vp]
         L.emt_free.restype = None
         _lib = L
@@ -149,8 +150,16 @@ EXPORTED_SYMBOLS = [
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
     "emt_engine_attach_lines", "emt_ipc_alloc", "emt_ipc_open", "emt_ipc_close", "emt_ipc_free",
-    "emt_waves_to_text", "emt_free",
+    "emt_waves_to_text", "emt_free", "emt_source_cos",
 ]
+
+
+def device_cos(x: np.ndarray, device: int = 0) -> np.ndarray:
+    """cos as the engine evaluates AC sources on the device (emt_source_cos)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    _check(lib().emt_source_cos(device, _dp(x), _dp(y), x.size))
+    return y
 
 
 def _check(status: int) -> None:

@@ -128,3 +128,19 @@ def random_rlc(seed: int, nodes: int = 20, dt: float = 1e-5, duration: float = 0
     comps.append(comp("src", "current_source", {"magnitude": float(rng.uniform(0.5, 2.0)), "frequency": 60.0,
                                                 "phase": 0.3}, "1", "0"))
     return _doc([str(n) for n in range(1, nodes + 1)], comps, ["v:1", f"v:{nodes}"], dt, duration)
+
+
+def subnormal_decay(dt=1e-4, duration=0.6):
+    """RC ladder whose node voltages decay through the subnormal range to zero
+    (trapezoidal factors down to -1/3 per step): drives the backward sweep's
+    division x / u_ii with subnormal and zero x, where a reciprocal-multiply
+    division is no longer correctly rounded."""
+    return _doc(["1", "2", "3"], [
+        comp("c1", "capacitor", {"capacitance": 1e-4, "v0": 1.0}, "1", "0"),
+        comp("c2", "capacitor", {"capacitance": 5e-5, "v0": -0.5}, "2", "0"),
+        comp("c3", "capacitor", {"capacitance": 2e-4, "v0": 0.25}, "3", "0"),
+        comp("r1", "resistor", {"resistance": 1.0}, "1", "0"),
+        comp("r12", "resistor", {"resistance": 2.0}, "1", "2"),
+        comp("r23", "resistor", {"resistance": 0.5}, "2", "3"),
+        comp("r3", "resistor", {"resistance": 0.2}, "3", "0"),
+    ], ["v:1", "v:2", "v:3"], dt, duration)

@@ -1,8 +1,9 @@
 """CUDA engine vs the oracle / reference goldens (runs on the B200 box: -m gpu).
 
 Bar (north_star): waveforms within 1e-9 relative + 1e-12 absolute on every
-sample; switch events, topology and factor counts bit-exact. Cases without
-cos() sources must be bit-identical (same operation order, -fmad=false).
+sample; switch events, topology and factor counts bit-exact. Every case must be
+bit-identical: same operation order, -fmad=false, and cos evaluated as glibc
+does (csrc/libmcos.cuh), so the AC-source cases are bitwise too.
 """
 import numpy as np
 import pytest
@@ -12,10 +13,6 @@ from oracle import oracle
 from paper_1903_01081_b200 import engine
 
 pytestmark = pytest.mark.gpu
-
-# cases whose sources are all DC (omega == 0): no libm/CUDA cos difference possible
-BITWISE = {"rc_discharge", "switched_dc_w3", "control_only", "diverging", "singular_islands"}
-
 
 KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}
 
@@ -36,8 +33,7 @@ def test_engine_matches_golden(name, kernel):
     stats = engine.ExecStats()
     w = engine.interpret(g.schedule, g.initial, g.steps, engine.ExecOptions(stats=stats), kernel=k)
     assert within_tolerance(w.values, g.waves), (name, np.max(np.abs(w.values - g.waves)))
-    if name in BITWISE:
-        assert bitwise_equal(w.values, g.waves), name
+    assert bitwise_equal(w.values, g.waves), name
     assert bitwise_equal(w.time, g.time)
     assert stats.factor_count == g.factor_count
 
