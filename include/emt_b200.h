@@ -205,7 +205,7 @@ emt_status emt_engine_profile(emt_engine* engine, int64_t* cycles, int32_t n);
 /* Device-side exchange for a line-split system over several engines / GPUs:
  * every engine of the system attaches the SAME mirror (lanes x cols doubles,
  * lane-major, see emt_engine_ring) and the SAME progress array (total_ctas
- * uint32), this engine's CTAs being [cta_offset, cta_offset + ceil(lanes/32)).
+ * uint32), this engine's CTAs being [cta_offset, cta_offset + emt_engine_ctas()).
  * Each engine then runs its launches persistently: its CTAs write their
  * line-end histories straight into the shared mirror and wait on every CTA's
  * progress word (K-1 passes of slack), so no host exchange is needed. With
@@ -214,6 +214,10 @@ emt_status emt_engine_profile(emt_engine* engine, int64_t* cycles, int32_t n);
  * All engines' launches must be resident together. */
 emt_status emt_engine_attach_lines(emt_engine* engine, void* mirror, void* progress, int32_t cta_offset,
                                    int32_t total_ctas, int32_t system_scope);
+
+/* CTAs of this engine's launches and lanes per CTA (0 for the generic kernel):
+ * the progress-array span emt_engine_attach_lines expects from this engine. */
+emt_status emt_engine_ctas(const emt_engine* engine, int32_t* ctas, int32_t* lanes_per_cta);
 /* CUDA IPC helpers for the shared mirror / progress arrays: `handle` is 64 bytes. */
 emt_status emt_ipc_alloc(int32_t device, int64_t bytes, void** ptr, void* handle);
 emt_status emt_ipc_open(int32_t device, const void* handle, void** ptr);

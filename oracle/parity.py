@@ -40,14 +40,20 @@ def compare(got: np.ndarray, want: np.ndarray) -> dict:
     excess = d - (ABS + REL * np.abs(want))
     excess[bit] = -np.inf  # NaN == NaN bitwise counts as equal
     bad = ~(excess <= 0) & ~bit
-    return {"samples": int(want.size), "bitwise": int(bit.sum()), "fail": int(bad.sum()),
-            "max_abs_diff": float(np.nanmax(np.where(bit, 0.0, d))) if want.size else 0.0,
-            "max_excess": float(excess.max()) if want.size else float("-inf")}
+    out = {"samples": int(want.size), "bitwise": int(bit.sum()), "fail": int(bad.sum()),
+           "max_abs_diff": float(np.nanmax(np.where(bit, 0.0, d))) if want.size else 0.0,
+           "max_excess": float(excess.max()) if want.size else float("-inf")}
+    if not bit.all():  # first non-identical sample: (row, column) of this block
+        r, c = np.argwhere(~bit)[0]
+        out["first_diff"] = [int(r), int(c)]
+    return out
 
 
 def merge(parts) -> dict:
     out = {"samples": 0, "bitwise": 0, "fail": 0, "max_abs_diff": 0.0, "max_excess": float("-inf")}
     for p in parts:
+        if "first_diff" in p and ("first_diff" not in out or p["first_diff"][0] < out["first_diff"][0]):
+            out["first_diff"] = p["first_diff"]
         for k in ("samples", "bitwise", "fail"):
             out[k] += p[k]
         out["max_abs_diff"] = max(out["max_abs_diff"], p["max_abs_diff"])

@@ -42,6 +42,7 @@ std::string libm_cos_prelude() {
                        // pivot reciprocal for the guarded Markstein division: NaN outside [2^-960, 2^960]
                        "#define EMT_RCP(u) ((fabs(u) >= 0x1p-960 && fabs(u) <= 0x1p960) ? 1.0 / (u) : "
                        "__longlong_as_double(0x7ff8000000000000LL))\n"
+                       "__device__ __noinline__ double emt_div_ieee(double x, double d) { return x / d; }\n"
                        "#define EMT_HD __device__ __forceinline__\n#define EMT_TABLE __device__ const\n") +
            kLibmCosSrc + "\n";
 }
@@ -148,8 +149,10 @@ struct Gen {
     // division becomes q0 = x*r, x/u = fma(fma(-u, q0, x), r, q0) (Markstein; correctly
     // rounded for normal-range operands, tools/micro/divcheck.c). Range guard: the
     // reciprocal is stored as NaN when |u| leaves [2^-960, 2^960] (EMT_RCP), and a row
-    // whose q0 is NaN, zero, subnormal-bound or huge takes IEEE x / u instead, so the
-    // result is x / u bit for bit everywhere (tests/golden/subnormal_decay).
+    // whose q0 is NaN, zero or below 2^-960 calls IEEE x / u out of line (a branch, not
+    // a predicated division in every row), so the result is x / u bit for bit
+    // (tests/golden/subnormal_decay). Huge q0 needs no test: |x| > 1e12 already fails
+    // the divergence check, which reports the same node as IEEE division would.
     bool rcp = false;
     int rcp_base = -1;
     // shared factors: when G is the same constant matrix in every lane and nothing
@@ -1388,7 +1391,7 @@ std::string task_literal(const Task& t, const LitCtx& c) {
                     o << "{ const double r_ = " << (t.f[3] >= 0 ? "LD(" + std::to_string(t.f[3]) + ")" : "SH[" + std::to_string(c.sh_rcp0 - t.f[3] - 2) + "]")
                       << "; const double d_ = " << lu(t.f[1])
                       << "; const double q_ = x * r_; double m_ = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); "
-                         "if (__builtin_expect(!(fabs(q_) >= 0x1p-960 && fabs(q_) <= 0x1p960), 0)) m_ = x / d_; x = m_; } "
+                         "if (__builtin_expect(!(fabs(q_) >= 0x1p-960), 0)) m_ = emt_div_ieee(x, d_); x = m_; } "
                       << (c.dsum ? "dsum = dsum + fabs(x); " : "dok = dok & (fabs(x) <= dlim); ");
                 else
                     o << "x = x / " << lu(t.f[1]) << "; dok = dok & (fabs(x) <= dlim); ";
@@ -2419,6 +2422,16 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "};\n";
     std::vector<int> hot_arena(g.hot_slots.begin() + 1, g.hot_slots.end());
     carr_i("__device__ const", "kHot", hot_arena);
+    // Hot slots the launch-end block writes itself (lazily finalized currents, aliased
+    // control outputs): their shared copy is stale, so the write-back must skip them —
+    // two unordered stores to one arena word from different warps otherwise race.
+    std::set<int> late_slots;
+    for (const auto& kv : g.alias_of) late_slots.insert(kv.first);
+    for (int c : g.lazy_fin) late_slots.insert(s.finalize[5 * static_cast<size_t>(c)]);
+    std::vector<int> wb_q;  // hot indices (1-based) copied back at the launch end
+    for (int q = 0; q + 1 < nhot; ++q)
+        if (!late_slots.count(g.hot_slots[static_cast<size_t>(q) + 1])) wb_q.push_back(q + 1);
+    carr_i("__device__ const", "kWbQ", wb_q);
     std::vector<int> dslot, dconst, cslot, chot, csign;
     for (int x = 0; x < s.extent; ++x) {
         if (g.cls[static_cast<size_t>(x)] == kDerived) {
@@ -2471,6 +2484,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * G << ", 1) emt_cg_kernel(const KArgs a) {\n"
       << "  extern __shared__ double sm[];\n"
       << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
+      // dev check: a NaN-filled shared memory at entry turns any read-before-write of a
+      // slot the prologue does not load into a parity failure
+      << (knob("EMTB200_CG_POISON", 0) ? "  for (int q = threadIdx.x; q < " + std::to_string(smem / 8) +
+                                             "; q += blockDim.x) sm[q] = __longlong_as_double(0x7ff4000000000badLL);\n  __syncthreads();\n"
+                                       : std::string())
       << "  const int slane = lane < " << LPC << " ? lane : 0;  // shadow threads mirror lane 0\n"
       << "  const int graw = blockIdx.x * " << LPC << " + slane; const bool live = lane < " << LPC << " && graw < W_;\n"
       << "  const int gl = graw < W_ ? graw : (int)(W_ - 1);\n"
@@ -2722,12 +2740,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
 ;
     if (slcopy) {
         std::vector<std::pair<std::string, std::string>> it;
-        for (int q = 0; q + 1 < nhot; ++q)
-            it.push_back({"A[(size_t)" + std::to_string(g.hot_slots[static_cast<size_t>(q) + 1]) + " * W_]",
-                          "S[" + std::to_string(static_cast<long long>(q + 1) * LPC) + "]"});
+        for (int q : wb_q)
+            it.push_back({"A[(size_t)" + std::to_string(g.hot_slots[static_cast<size_t>(q)]) + " * W_]",
+                          "S[" + std::to_string(static_cast<long long>(q) * LPC) + "]"});
         o << warp_copies(it, G, "    ");
     } else {
-        o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << nhot - 1 << "; q += " << G << ") A[(size_t)kHot[q] * W_] = S[(q + 1) * " << LPC << "];\n";
+        o << "    _Pragma(\"unroll 8\") for (int j = warp; j < " << wb_q.size() << "; j += " << G
+          << ") { const int q = kWbQ[j]; A[(size_t)kHot[q - 1] * W_] = S[q * " << LPC << "]; }\n";
     }
     if (lu_smem) {
         o << "    _Pragma(\"unroll 8\") for (int q = warp; q < " << s.l_col.size() << "; q += " << G << ") A[(size_t)(" << s.l << " + q) * W_] = S[("
@@ -3089,6 +3108,13 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
     garr("kRec", rec);
     std::vector<int> hot_arena(g.hot_slots.begin() + 1, g.hot_slots.end());
     garr("kHot", hot_arena);
+    std::set<int> late_slots;  // written by the launch-end lazy finalize: not copied back (see generate_kernel)
+    for (const auto& kv : g.alias_of) late_slots.insert(kv.first);
+    for (int c : g.lazy_fin) late_slots.insert(s.finalize[5 * static_cast<size_t>(c)]);
+    std::vector<int> wb_q;
+    for (int q = 0; q + 1 < nhot; ++q)
+        if (!late_slots.count(g.hot_slots[static_cast<size_t>(q) + 1])) wb_q.push_back(q + 1);
+    garr("kWbQ", wb_q);
     garr("kCst", cslots);
     std::vector<int> dslot, dconst, cslot, chot, csign;
     for (int x = 0; x < s.extent; ++x) {
@@ -3164,7 +3190,7 @@ bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lane
       << "    }\n"
       << "  }\n"
       << "  __syncthreads();\n"
-      << "  for (int q = threadIdx.x; q < " << nhot - 1 << "; q += " << NTH << ") A[(size_t)kHot[q] * W_] = S[q + 1];\n"
+      << "  for (int j = threadIdx.x; j < " << wb_q.size() << "; j += " << NTH << ") { const int q = kWbQ[j]; A[(size_t)kHot[q - 1] * W_] = S[q]; }\n"
       << "  for (int q = threadIdx.x; q < " << s.l_col.size() << "; q += " << NTH << ") A[(size_t)(" << s.l << " + q) * W_] = S["
       << g.l_base_smem << " + q];\n"
       << "  for (int q = threadIdx.x; q < " << s.u_col.size() << "; q += " << NTH << ") A[(size_t)(" << s.u << " + q) * W_] = S["

@@ -813,6 +813,9 @@ emt_status check_lane_errors(emt_engine* e) {
     if (best == nullptr) return EMT_OK;
     e->failed = 1;
     const int glane = e->lane_begin + best_lane;
+    if (best->code == 64)  // written by the line-coupled persistent kernel (codegen.cpp)
+        return set_error(EMT_CUDA_ERROR, "line-coupling progress wait timed out or a peer CTA / rank failed (step " +
+                                             std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
     if (best->code == EMT_SINGULAR_MATRIX)
         return set_error(best->code, "row " + std::to_string(best->index) + ": zero pivot below tolerance" +
                                          (e->sched.width > 1 ? " in lane " + std::to_string(glane) : std::string()) +
@@ -1007,6 +1010,16 @@ emt_status emt_engine_reserve(emt_engine* e, int32_t capacity_steps) {
     if (capacity_steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative capacity");
     CUDA_TRY(cudaSetDevice(e->device));
     CUDA_TRY(cudaStreamSynchronize(e->stream));
+    if (e->rows > 0 && e->d_refactored) {
+        // the recording window restarts: carry its refactorisations into the base
+        // counts, so factor_count and the fcount slot keep counting from pass 0
+        std::vector<unsigned char> flags(static_cast<size_t>(e->rows));
+        CUDA_TRY(cudaMemcpy(flags.data(), e->d_refactored, flags.size(), cudaMemcpyDeviceToHost));
+        int fc = 0;
+        for (unsigned char f : flags) fc += f ? 1 : 0;
+        e->base_factor_count += fc;
+        for (double& x : e->initial_fcount) x += fc;
+    }
     if (capacity_steps > e->capacity) {
         if (e->d_waves) cudaFree(e->d_waves);
         if (e->d_refactored) cudaFree(e->d_refactored);
@@ -1289,7 +1302,11 @@ emt_status emt_engine_load(emt_engine* e, const double* initial, int64_t initial
     CUDA_TRY(cudaStreamSynchronize(e->stream));
     if (e->copy_stream) CUDA_TRY(cudaStreamSynchronize(e->copy_stream));
     EMT_TRY(emt_engine_stage(e, initial, initial_len, const_table));
-    return emt_engine_commit(e);
+    EMT_TRY(emt_engine_commit(e));
+    // commit's history copy into a shared line mirror and the progress-word reset are
+    // queued on the engine stream; other ranks read both as soon as the host returns
+    if (e->ring_shared || e->d_progress) CUDA_TRY(cudaStreamSynchronize(e->stream));
+    return EMT_OK;
 }
 
 emt_status emt_engine_profile(emt_engine* e, int64_t* cycles, int32_t n) {
@@ -1342,6 +1359,15 @@ emt_status emt_engine_attach_lines(emt_engine* e, void* mirror, void* progress, 
     e->prog_off = cta_offset;
     e->prog_total = total_ctas;
     e->sys_scope = system_scope ? 1 : 0;
+    // the D2D history copy and the memset may still be in flight on the legacy stream
+    CUDA_TRY(cudaDeviceSynchronize());
+    return EMT_OK;
+}
+
+emt_status emt_engine_ctas(const emt_engine* e, int32_t* ctas, int32_t* lanes_per_cta) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (ctas) *ctas = cta_count(e);
+    if (lanes_per_cta) *lanes_per_cta = e->kernel_mode == EMT_KERNEL_SPECIALISED ? e->gen.lpc : 0;
     return EMT_OK;
 }
 
@@ -1533,18 +1559,22 @@ emt_status emt_interpret(const char* schedule_text, const double* initial, int64
     if (options && options->divergence_limit > 0) e->plan.div_limit = options->divergence_limit;
     const int warm = options ? std::max(0, std::min<int>(options->warmup_steps, steps)) : 0;
     EMT_TRY(emt_engine_reserve(e.get(), steps));
-    cudaEvent_t t0, t1;
-    CUDA_TRY(cudaEventCreate(&t0));
-    CUDA_TRY(cudaEventCreate(&t1));
+    struct Events {  // released on every return path
+        cudaEvent_t t0 = nullptr, t1 = nullptr;
+        ~Events() {
+            if (t0) cudaEventDestroy(t0);
+            if (t1) cudaEventDestroy(t1);
+        }
+    } ev;
+    CUDA_TRY(cudaEventCreate(&ev.t0));
+    CUDA_TRY(cudaEventCreate(&ev.t1));
     EMT_TRY(emt_engine_advance(e.get(), warm, 0));
-    CUDA_TRY(cudaEventRecord(t0, e->stream));
+    CUDA_TRY(cudaEventRecord(ev.t0, e->stream));
     EMT_TRY(emt_engine_advance(e.get(), steps - warm, 0));
-    CUDA_TRY(cudaEventRecord(t1, e->stream));
+    CUDA_TRY(cudaEventRecord(ev.t1, e->stream));
     emt_status st = emt_engine_sync(e.get());
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, t0, t1);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
+    cudaEventElapsedTime(&ms, ev.t0, ev.t1);
     if (st != EMT_OK) return st;
     EMT_TRY(emt_engine_read_waves(e.get(), 0, steps, waves, time));
     if (stats) {

@@ -135,6 +135,7 @@ def lib():
         L.emt_waves_to_text.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int32, ctypes.c_int32, dp, dp,
                                         ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int64)]
         L.emt_source_cos.argtypes = [ctypes.c_int32, dp, dp, ctypes.c_int64]
+        L.emt_engine_ctas.argtypes = [vp, ip, ip]
         L.emt_free.argtypes = [vp]
         L.emt_free.restype = None
         _lib = L
@@ -150,7 +151,7 @@ EXPORTED_SYMBOLS = [
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
     "emt_engine_attach_lines", "emt_ipc_alloc", "emt_ipc_open", "emt_ipc_close", "emt_ipc_free",
-    "emt_waves_to_text", "emt_free", "emt_source_cos",
+    "emt_waves_to_text", "emt_free", "emt_source_cos", "emt_engine_ctas",
 ]
 
 
@@ -403,6 +404,12 @@ class Engine:
         """Device-side line exchange with other engines sharing `mirror` / `progress` (emt_engine_attach_lines)."""
         _check(lib().emt_engine_attach_lines(self._h, ctypes.c_void_p(mirror_ptr), ctypes.c_void_p(progress_ptr),
                                              int(cta_offset), int(total_ctas), 1 if system_scope else 0))
+
+    def ctas(self):
+        """(CTAs of this engine's launches, lanes per CTA; 0 for the generic kernel) — emt_engine_ctas."""
+        c, l = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().emt_engine_ctas(self._h, ctypes.byref(c), ctypes.byref(l)))
+        return c.value, l.value
 
     def sync(self) -> None:
         _check(lib().emt_engine_sync(self._h))

@@ -119,8 +119,13 @@ class LineSplitShard:
             return
         if self.exchange == "device" and self.eng.kernel == engine.KERNEL_SPECIALISED:
             rank = dist.get_rank()
-            spans = [shard_bounds(batch.width, self.world, r) for r in range(self.world)]
-            ctas = [(b - a + 31) // 32 for a, b in spans]
+            # each engine's own CTA count (emt_engine_ctas), gathered: no lanes-per-CTA assumption
+            mine = torch.tensor([self.eng.ctas()[0]], dtype=torch.int64)
+            if dist.get_backend() == "nccl":
+                mine = mine.cuda(device)
+            parts = [torch.zeros_like(mine) for _ in range(self.world)]
+            dist.all_gather(parts, mine)
+            ctas = [int(p.item()) for p in parts]
             total = sum(ctas)
             offset = sum(ctas[:rank])
             mb, pb = lanes * cols * 8, total * 4
@@ -169,5 +174,6 @@ class LineSplitShard:
         """New batch on every rank: reset (own progress words), then a barrier so no
         rank launches against another rank's stale progress."""
         self.eng.load(initial, const_table)
+        self.eng.sync()  # the mirror rows and progress resets have landed before peers launch
         if self.world > 1:
             self.dist.barrier()
