@@ -1254,6 +1254,8 @@ struct LitCtx {
     bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
     std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
+    int divguard = 1;                      // reciprocal-multiply division: 1 = detect |q| < 2^-960 (stop the
+                                           // launch, EMT_INEXACT_DIVISION), 2 = branch to IEEE x/u, 0 = none (dev)
     bool zterm = false;                    // drop zero-slot terms from sums
     int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
     int task_id = -1;                      // the task's index (per-task registers)
@@ -1391,8 +1393,11 @@ std::string task_literal(const Task& t, const LitCtx& c) {
                     o << "{ const double r_ = " << (t.f[3] >= 0 ? "LD(" + std::to_string(t.f[3]) + ")" : "SH[" + std::to_string(c.sh_rcp0 - t.f[3] - 2) + "]")
                       << "; const double d_ = " << lu(t.f[1])
                       << "; const double q_ = x * r_; double m_ = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); "
-                         "if (__builtin_expect(!(fabs(q_) >= 0x1p-960), 0)) m_ = emt_div_ieee(x, d_); x = m_; } "
-                      << (c.dsum ? "dsum = dsum + fabs(x); " : "dok = dok & (fabs(x) <= dlim); ");
+                      << (c.divguard == 2 ? "if (__builtin_expect(!(fabs(q_) >= 0x1p-960), 0)) m_ = emt_div_ieee(x, d_); " : "")
+                      << "x = m_; "
+                      << (c.dsum ? "dsum = dsum + fabs(x); } "
+                                 : c.divguard == 1 ? "dok = dok & (fabs(x) <= dlim) & (fabs(q_) >= 0x1p-960); } "
+                                                   : "dok = dok & (fabs(x) <= dlim); } ");
                 else
                     o << "x = x / " << lu(t.f[1]) << "; dok = dok & (fabs(x) <= dlim); ";
             else
@@ -1876,6 +1881,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     LitCtx lctx;
     if (knob("EMTB200_CG_SWFOLD", 1)) lctx.lit_init = [&](int k) -> int { return g.invariant(k) ? (g.c0(k) != 0.0 ? 1 : 0) : -1; };
     lctx.dsum = knob("EMTB200_CG_DSUM", 0) != 0;  // measured 0.6% slower than the AND-ed predicate
+    lctx.divguard = opt.exact_division ? 2 : knob("EMTB200_CG_DIVGUARD", 1);  // 0: dev A/B only (may misround)
     const bool dok_mode = straight && (knob("EMTB200_CG_DOK", 1) != 0 || g.dmma);
     lctx.dok = dok_mode;
     lctx.sh_rcp0 = g.sh_rcp(0);
@@ -2716,6 +2722,13 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "        for (int i = 0; i < " << s.nodes << "; ++i) if (!(fabs(LD(kVoff[i])) <= a.div_limit)) { bad = i; break; }\n"
           << "        if (bad != 0x7fffffff) { serr[lane] = bad; a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
           << g.solve_layer << "; }\n"
+          // no divergence: a quotient below the Markstein bound (the only other cause
+          // of !dok); its node voltage is below 2^-959 (or zero)
+          << (lctx.divguard == 1
+                  ? "        else { for (int i = 0; i < " + std::to_string(s.nodes) + "; ++i) if (fabs(LD(kVoff[i])) < 0x1p-959) { bad = i; break; }\n"
+                    "          if (bad != 0x7fffffff) { serr[lane] = bad; a.lane_err[4*gl] = 66; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = " +
+                        std::to_string(g.solve_layer) + "; } }\n"
+                  : std::string())
           << "      }\n"
           << "      if (__syncthreads_or(warp == 0 && live && serr[lane] != 0x7fffffff)) { FAILPUB(); return; }\n"
           << "    }\n"

@@ -22,6 +22,7 @@ struct CodegenOptions {
     bool lu_in_smem = true;         // keep L/U factors on chip when they fit
     int mode = 0;                   // 0 auto, 1 straight-line tasks, 2 compact per-type loops
     long long lane_begin = 0;       // first batch lane of the engine (line-end peer lanes are batch indices)
+    bool exact_division = false;    // IEEE fallback branch in every backward row (EMT_FLAG_EXACT_DIVISION)
     bool tensor_solve = false;      // shared-G batches: V = G^-1 I on the FP64 tensor cores (not bit-exact)
     int lanes_per_cta = 0;          // scenario lanes per CTA (32, 16 or 8; 0 = EMTB200_CG_LPC or 32)
 };

@@ -801,9 +801,13 @@ emt_status check_lane_errors(emt_engine* e) {
     // lowest row/node index, then the lowest lane (sparse.cpp:135-143, exec.cpp:229-237).
     const LaneError* best = nullptr;
     int best_lane = -1;
+    // a failing CTA releases its line-coupled peers, which then record code 64: the
+    // cause is the other error, so 64 is reported only when it is the only one
+    bool cause = false;
+    for (const LaneError& x : errs) cause = cause || (x.code != 0 && x.code != 64);
     for (int l = 0; l < e->W; ++l) {
         const LaneError& x = errs[static_cast<size_t>(l)];
-        if (x.code == 0) continue;
+        if (x.code == 0 || (cause && x.code == 64)) continue;
         if (best == nullptr || x.step < best->step || (x.step == best->step && x.layer < best->layer) ||
             (x.step == best->step && x.layer == best->layer && x.index < best->index)) {
             best = &x;
@@ -813,6 +817,11 @@ emt_status check_lane_errors(emt_engine* e) {
     if (best == nullptr) return EMT_OK;
     e->failed = 1;
     const int glane = e->lane_begin + best_lane;
+    if (best->code == EMT_INEXACT_DIVISION)
+        return set_error(EMT_INEXACT_DIVISION, "node index " + std::to_string(best->index) +
+                                                   ": backward-substitution quotient below 2^-960 (step " +
+                                                   std::to_string(best->step) + ", lane " + std::to_string(glane) +
+                                                   "); rerun with EMT_FLAG_EXACT_DIVISION");
     if (best->code == 64)  // written by the line-coupled persistent kernel (codegen.cpp)
         return set_error(EMT_CUDA_ERROR, "line-coupling progress wait timed out or a peer CTA / rank failed (step " +
                                              std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
@@ -934,6 +943,7 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
         opt.tensor_solve = (c.flags & EMT_FLAG_TENSOR_SOLVE) != 0;
+        opt.exact_division = (c.flags & EMT_FLAG_EXACT_DIVISION) != 0;
         int dev_smem = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
         opt.smem_budget = static_cast<size_t>(dev_smem);
@@ -1545,15 +1555,30 @@ const char* emt_engine_summary(const emt_engine* e) { return e ? e->summary.c_st
 void* emt_engine_device_waves(emt_engine* e) { return e ? e->d_waves : nullptr; }
 void* emt_engine_stream(emt_engine* e) { return e ? e->stream : nullptr; }
 
+static emt_status interpret_once(const char* schedule_text, const double* initial, int64_t initial_len, int32_t steps,
+                                 const emt_exec_options* options, emt_config c, double* waves, double* time,
+                                 emt_exec_stats* stats);
+
 emt_status emt_interpret(const char* schedule_text, const double* initial, int64_t initial_len, int32_t steps,
                          const emt_exec_options* options, const emt_config* cfg, double* waves, double* time,
                          emt_exec_stats* stats) {
     if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
-    emt_engine* raw = nullptr;
     emt_config c{};
     if (cfg) c = *cfg;
     c.lane_begin = 0;
     c.lane_count = 0;
+    const emt_status st = interpret_once(schedule_text, initial, initial_len, steps, options, c, waves, time, stats);
+    if (st != EMT_INEXACT_DIVISION || (c.flags & EMT_FLAG_EXACT_DIVISION)) return st;
+    // a quotient left the fast division's exact range: the same run with the IEEE
+    // fallback compiled into every backward row (bit-identical to the reference)
+    c.flags |= EMT_FLAG_EXACT_DIVISION;
+    return interpret_once(schedule_text, initial, initial_len, steps, options, c, waves, time, stats);
+}
+
+static emt_status interpret_once(const char* schedule_text, const double* initial, int64_t initial_len, int32_t steps,
+                                 const emt_exec_options* options, emt_config c, double* waves, double* time,
+                                 emt_exec_stats* stats) {
+    emt_engine* raw = nullptr;
     EMT_TRY(emt_engine_create(schedule_text, nullptr, 0, initial, initial_len, &c, &raw));
     std::unique_ptr<emt_engine> e(raw);
     if (options && options->divergence_limit > 0) e->plan.div_limit = options->divergence_limit;

@@ -40,6 +40,8 @@ class EmtError(RuntimeError):
             self.code = ERROR_CODES[status - 1]
         elif status == 64:
             self.code = "CudaError"
+        elif status == 66:
+            self.code = "InexactDivision"
         else:
             self.code = f"Status{status}"
         self.detail = detail
@@ -54,6 +56,7 @@ class _Config(ctypes.Structure):
 
 KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT = 0, 1, 2, 3
 FLAG_TENSOR_SOLVE = 1
+FLAG_EXACT_DIVISION = 2  # IEEE fallback in every backward row (include/emt_b200.h)
 
 
 class _Options(ctypes.Structure):
@@ -308,13 +311,14 @@ class Engine:
 
     def __init__(self, schedule: str, initial: np.ndarray, const_table: Optional[np.ndarray] = None,
                  width: int = 0, device: int = 0, lane_begin: int = 0, lane_count: int = 0,
-                 lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO, tensor_solve: bool = False):
+                 lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO, tensor_solve: bool = False,
+                 exact_division: bool = False):
         L = lib()
         self._h = ctypes.c_void_p()
         init = np.ascontiguousarray(initial, dtype=np.float64)
         ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
         cfg = _config(device, lane_begin, lane_count, lanes_per_block, warps, kernel,
-                      FLAG_TENSOR_SOLVE if tensor_solve else 0)
+                      (FLAG_TENSOR_SOLVE if tensor_solve else 0) | (FLAG_EXACT_DIVISION if exact_division else 0))
         _check(L.emt_engine_create(schedule.encode(), _dp(ct) if ct is not None else None, int(width), _dp(init),
                                    init.size, ctypes.byref(cfg), ctypes.byref(self._h)))
         vals = [ctypes.c_int32() for _ in range(9)]

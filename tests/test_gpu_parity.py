@@ -277,3 +277,21 @@ def test_run_async_two_engines_alternating():
     for k, e in enumerate(engs):
         e.wait()
         assert bitwise_equal(outs[k], want.values)
+
+
+def test_fast_division_detects_subnormal_quotients_exact_mode_is_bitwise():
+    """Backward-sweep quotients below 2^-960 (a decay through the subnormals): the fast
+    kernel stops with InexactDivision instead of misrounding, EMT_FLAG_EXACT_DIVISION
+    (IEEE fallback per row) is bit-identical to the reference, and interpret() retries
+    by itself (test_engine_matches_golden covers it through the golden)."""
+    g = load_golden("subnormal_decay")
+    eng = engine.Engine(g.schedule, g.initial)
+    assert eng.kernel == engine.KERNEL_SPECIALISED
+    eng.reserve(g.steps)
+    with pytest.raises(engine.EmtError) as ei:
+        eng.advance(g.steps, sync=True)
+    assert ei.value.code == "InexactDivision"
+    ex = engine.Engine(g.schedule, g.initial, exact_division=True)
+    ex.reserve(g.steps)
+    ex.advance(g.steps, sync=True)
+    assert bitwise_equal(ex.waves().values, g.waves)
