@@ -269,6 +269,18 @@ const char* emt_engine_summary(const emt_engine* engine);
 emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,
                        int32_t compile, const char* arch, const char** source, const char** summary);
 
+/* ---- the "sm100a" code-database dialect ---------------------------------- */
+
+/* emit_source(schedule, "sm100a") (proj/include/emtgrid/codegen.hpp:28; the
+ * reference registers only "cpp", proj/src/codegen.cpp:84-87): a standalone CUDA
+ * program for this schedule — its specialised step-loop kernel plus a host main()
+ * with the emitted "cpp" program's CLI (--state <file> --steps <n> --out <file>;
+ * exit 2 usage/I/O, 3 singular matrix, 4 divergence; proj/data/codedb/cpp/
+ * prologue.tpl:87,165,198-224) and the same waveform text, byte for byte. Build
+ * with nvcc -gencode arch=compute_100a,code=sm_100a -fmad=false. *source is
+ * malloc'd (release with emt_free). Line-coupled schedules: EMT_UNKNOWN_KIND. */
+emt_status emt_emit_program(const char* schedule_text, char** source);
+
 /* ---- waveform text (WaveformSet::to_text, proj/src/waveform.cpp:22-42) ---- */
 
 /* Formats `rows` waveform rows as the reference's text form: a header line

@@ -12,7 +12,11 @@
 #include <filesystem>
 #include <string>
 
+#include <cstdlib>
+#include <sys/wait.h>
+
 #include "emtgrid/bench.hpp"
+#include "emtgrid/codegen.hpp"
 #include "emtgrid/grid.hpp"
 
 using namespace emtgrid;
@@ -157,6 +161,69 @@ void singular_error() {
                dev_where + "'");
 }
 
+// criterion 5 in the "sm100a" dialect (acceptance.cpp:150-187): the emitted program,
+// built with nvcc, reproduces the interpreter — here byte for byte — with the "cpp"
+// program's CLI; exit codes 3 (singular) and 4 (divergence); "cuda" stays unknown
+int run_program(const std::string& bin, const std::string& dir, const CompiledTask& task, int steps) {
+    write_file(dir + "/state.txt", serialize_state(task.initial, task.schedule.arena_extent, task.schedule.width));
+    const std::string cmd = "\"" + bin + "\" --state \"" + dir + "/state.txt\" --steps " + std::to_string(steps) +
+                            " --out \"" + dir + "/waves.txt\" 2> \"" + dir + "/stderr.txt\"";
+    const int rc = std::system(cmd.c_str());
+    return WIFEXITED(rc) ? WEXITSTATUS(rc) : -1;
+}
+
+void criterion_emitted_sm100a(const std::string& doc, const std::string& scratch) {
+    const char* nv = std::getenv("EMTGRID_NVCC");
+    const Toolchain tc{nv != nullptr && *nv != '\0' ? nv : "/usr/local/cuda/bin/nvcc", sm100a_flags()};
+    const int steps = 1000;
+    const CompiledTask task = compile_document(doc);
+    const WaveformSet expected = interpret(task.schedule, task.initial, steps);
+    const std::string dir = scratch + "/emit_feeder";
+    const std::string bin = compile_emitted(emit_source(task.schedule, "sm100a"), tc, dir);
+    const int rc = run_program(bin, dir, task, steps);
+    const bool same = rc == 0 && WaveformSet::load(dir + "/waves.txt").to_text() == expected.to_text();
+
+    bool cuda_unknown = false;
+    try {
+        emit_source(task.schedule, "cuda");
+    } catch (const Error& e) {
+        cuda_unknown = e.code() == ErrorCode::UnknownDialect;
+    }
+    const std::string islands = R"({"nodes": ["1", "2", "3", "4"], "components": [
+      {"id": "la", "kind": "inductor", "params": {"inductance": 0.001}, "terminals": ["1", "2"]},
+      {"id": "lb", "kind": "inductor", "params": {"inductance": 0.002}, "terminals": ["3", "4"]}],
+     "control": [], "couplings": [],
+     "task": {"dt": 1e-4, "duration": 1e-3, "channels": ["v:1"], "device_profile": "cpu-serial", "strategy": "serial"}})";
+    const std::string diverging = R"({"nodes": ["1"], "components": [
+      {"id": "r1", "kind": "resistor", "params": {"resistance": 1000.0}, "terminals": ["1", "0"]},
+      {"id": "cs", "kind": "controlled_current_source", "params": {"gain": 1.0}, "terminals": ["1", "0"]}],
+     "control": [{"id": "m2", "kind": "gain", "params": {"k": 4.0}, "inputs": ["v1"]},
+                 {"id": "b1", "kind": "sum", "params": {}, "inputs": ["m2", "one"]},
+                 {"id": "one", "kind": "constant", "params": {"value": 1.0}, "inputs": []}],
+     "couplings": [{"direction": "meter", "electrical_ref": "1", "signal_ref": "v1"},
+                   {"direction": "actuator", "electrical_ref": "cs", "signal_ref": "b1"}],
+     "task": {"dt": 1e-3, "duration": 1.0, "channels": ["v:1"], "device_profile": "cpu-serial", "strategy": "serial"}})";
+    const CompiledTask ti = compile_document(islands), td = compile_document(diverging);
+    const int rc3 = run_program(compile_emitted(emit_source(ti.schedule, "sm100a"), tc, scratch + "/emit_islands"),
+                                scratch + "/emit_islands", ti, 10);
+    const int rc4 = run_program(compile_emitted(emit_source(td.schedule, "sm100a"), tc, scratch + "/emit_div"),
+                                scratch + "/emit_div", td, 1000);
+    // the rows before the divergence are written, like the cpp program's
+    std::size_t div_rows = 0;
+    try {
+        interpret(td.schedule, td.initial, 1000);
+    } catch (const Error&) {
+    }
+    const std::string div_text = read_file(scratch + "/emit_div/waves.txt");
+    for (char ch : div_text) div_rows += ch == '\n' ? 1 : 0;
+    const bool pass = same && cuda_unknown && rc3 == 3 && rc4 == 4 && div_rows > 1;
+    report("criterion 5 (sm100a)", pass,
+           "emit_source(feeder, \"sm100a\") built with nvcc: 1000 steps byte-identical to interpret (" +
+               std::string(same ? "yes" : "NO") + "); exit codes singular " + std::to_string(rc3) + " (3), divergence " +
+               std::to_string(rc4) + " (4) after " + std::to_string(div_rows - 1) + " rows; \"cuda\" " +
+               (cuda_unknown ? "UnknownDialect" : "ACCEPTED"));
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -175,6 +242,7 @@ int main(int argc, char** argv) {
         }
     }
     try {
+        criterion_emitted_sm100a(doc, scratch);
         vse_device_package(doc, scratch);
         profile_dispatch();
         singular_error();

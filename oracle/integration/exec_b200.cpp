@@ -11,7 +11,10 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "emt_b200.h"
+#include "emtgrid/codegen.hpp"
 #include "emtgrid/exec.hpp"
 
 namespace emtgrid {
@@ -60,6 +63,21 @@ WaveformSet execute_b200(const ScheduleProgram& s, const Eigen::VectorXd& initia
         options.stats->measured_steps = st.measured_steps;
     }
     return w;
+}
+
+std::string emit_source_sm100a(const ScheduleProgram& s) {
+    // emit_source's "sm100a" dialect (proj/src/codegen.cpp:84 + reference_b200.patch)
+    const std::string text = s.serialize();
+    char* src = nullptr;
+    const emt_status rc = emt_emit_program(text.c_str(), &src);
+    if (rc != EMT_OK) rethrow(rc);
+    std::string out(src);
+    emt_free(src);
+    return out;
+}
+
+std::vector<std::string> sm100a_flags() {
+    return {"-x", "cu", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false", "-std=c++17", "-O3", "-w"};
 }
 
 }  // namespace emtgrid

@@ -52,4 +52,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
 bool generate_tsimt(const Schedule& s, const std::vector<double>& ctab, int lanes, const CodegenOptions& opt,
                     GeneratedKernel& out, Failure& fail);
 
+/// The "sm100a" code-DB dialect (emit_program.cpp): a standalone CUDA program —
+/// this schedule's specialised kernel plus a host main() with the "cpp" dialect's
+/// CLI (--state --steps --out; exit 2 I/O, 3 singular, 4 divergence) and waveform text.
+bool emit_program(const Schedule& s, const std::vector<double>& ctab, int lanes, std::string& out, Failure& fail);
+
 }  // namespace emtb200

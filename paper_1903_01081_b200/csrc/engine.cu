@@ -1489,6 +1489,20 @@ emt_status emt_engine_run(emt_engine* e, int32_t steps, int32_t chunk, double* w
     return emt_engine_wait(e);
 }
 
+emt_status emt_emit_program(const char* schedule_text, char** source) {
+    if (schedule_text == nullptr || source == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
+    Schedule s;
+    Failure f;
+    if (!parse_schedule(schedule_text, s, f)) return set_error(f.code ? f.code : EMT_MALFORMED_DOCUMENT, f.where + ": " + f.message);
+    lu_symbolic(s);
+    std::string out;
+    if (!emit_program(s, s.const_table, s.width, out, f)) return set_error(f.code ? f.code : EMT_CAPACITY_EXCEEDED, f.where + ": " + f.message);
+    *source = static_cast<char*>(std::malloc(out.size() + 1));
+    if (*source == nullptr) return set_error(EMT_CUDA_ERROR, "out of host memory");
+    std::memcpy(*source, out.c_str(), out.size() + 1);
+    return EMT_OK;
+}
+
 emt_status emt_codegen(const char* schedule_text, const double* const_table, int32_t width, int32_t warps,
                        int32_t compile, const char* arch, const char** source, const char** summary) {
     thread_local std::string src_out, sum_out;

@@ -139,6 +139,7 @@ def lib():
                                         ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int64)]
         L.emt_source_cos.argtypes = [ctypes.c_int32, dp, dp, ctypes.c_int64]
         L.emt_engine_ctas.argtypes = [vp, ip, ip]
+        L.emt_emit_program.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
         L.emt_free.argtypes = [vp]
         L.emt_free.restype = None
         _lib = L
@@ -154,8 +155,18 @@ EXPORTED_SYMBOLS = [
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
     "emt_engine_attach_lines", "emt_ipc_alloc", "emt_ipc_open", "emt_ipc_close", "emt_ipc_free",
-    "emt_waves_to_text", "emt_free", "emt_source_cos", "emt_engine_ctas",
+    "emt_waves_to_text", "emt_free", "emt_source_cos", "emt_engine_ctas", "emt_emit_program",
 ]
+
+
+def emit_program(schedule: str) -> str:
+    """emit_source(schedule, "sm100a"): a standalone CUDA program (emt_emit_program)."""
+    out = ctypes.c_void_p()
+    _check(lib().emt_emit_program(schedule.encode(), ctypes.byref(out)))
+    try:
+        return ctypes.cast(out, ctypes.c_char_p).value.decode()
+    finally:
+        lib().emt_free(out)
 
 
 def device_cos(x: np.ndarray, device: int = 0) -> np.ndarray:
