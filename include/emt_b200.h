@@ -45,7 +45,7 @@ typedef enum emt_status {
     EMT_NON_POSITIVE_INPUT = 20,/* steps < 0, width < 1, ... */
     EMT_CUDA_ERROR = 64,        /* CUDA runtime failure (message has the detail) */
     EMT_INVALID_HANDLE = 65,
-    EMT_INEXACT_DIVISION = 66,  /* a backward-sweep quotient fell below 2^-960 (or to zero), where the
+    EMT_INEXACT_DIVISION = 66,  /* a nonzero backward-sweep quotient fell below 2^-900, where the
                                    fast reciprocal division may misround: rerun the batch with
                                    EMT_FLAG_EXACT_DIVISION (emt_interpret does this itself) */
 } emt_status;
@@ -72,11 +72,11 @@ typedef struct emt_config {
 enum { EMT_FLAG_TENSOR_SOLVE = 1 };
 
 /* The specialised kernel divides by a pivot as q = x*r, x/u = fma(fma(-u, q, x), r, q)
- * with r = 1/u (Markstein: the IEEE quotient bit for bit while |q| >= 2^-960). By
- * default each backward row only checks that bound (one compare, no branch) and a
- * pass that breaks it stops the launch with EMT_INEXACT_DIVISION; with this flag
- * every row branches to IEEE x / u below the bound instead (exact everywhere,
- * ~20% slower). */
+ * with r = 1/u (Markstein: the IEEE quotient bit for bit while q is zero or
+ * |q| >= 2^-900 and |u| is in [2^-60, 2^960]). By default each backward row only
+ * checks that bound (one compare, no branch) and a pass that breaks it stops the
+ * launch with EMT_INEXACT_DIVISION; with this flag every row branches to IEEE
+ * x / u below the bound instead (exact everywhere, ~20% slower). */
 enum { EMT_FLAG_EXACT_DIVISION = 2 };
 
 /* Step-loop kernel selection. AUTO generates and JIT-compiles (NVRTC) a kernel

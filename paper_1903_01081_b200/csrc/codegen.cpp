@@ -39,8 +39,8 @@ namespace {
 
 std::string libm_cos_prelude() {
     return std::string("__device__ __forceinline__ int emt_lo32(double d) { return __double2loint(d); }\n"
-                       // pivot reciprocal for the guarded Markstein division: NaN outside [2^-960, 2^960]
-                       "#define EMT_RCP(u) ((fabs(u) >= 0x1p-960 && fabs(u) <= 0x1p960) ? 1.0 / (u) : "
+                       // pivot reciprocal for the guarded Markstein division: NaN outside [2^-60, 2^960]
+                       "#define EMT_RCP(u) ((fabs(u) >= 0x1p-60 && fabs(u) <= 0x1p960) ? 1.0 / (u) : "
                        "__longlong_as_double(0x7ff8000000000000LL))\n"
                        "__device__ __noinline__ double emt_div_ieee(double x, double d) { return x / d; }\n"
                        "#define EMT_HD __device__ __forceinline__\n#define EMT_TABLE __device__ const\n") +
@@ -148,10 +148,13 @@ struct Gen {
     // pivot reciprocals 1/u_ii in shared memory (rcp_base + row): the backward sweep's
     // division becomes q0 = x*r, x/u = fma(fma(-u, q0, x), r, q0) (Markstein; correctly
     // rounded for normal-range operands, tools/micro/divcheck.c). Range guard: the
-    // reciprocal is stored as NaN when |u| leaves [2^-960, 2^960] (EMT_RCP), and a row
-    // whose q0 is NaN, zero or below 2^-960 calls IEEE x / u out of line (a branch, not
-    // a predicated division in every row), so the result is x / u bit for bit
-    // (tests/golden/subnormal_decay). Huge q0 needs no test: |x| > 1e12 already fails
+    // reciprocal is NaN when |u| leaves [2^-60, 2^960] (EMT_RCP); with |q0| >= 2^-900
+    // that keeps r and q0 normal and |x| >= 2^-960, so the remainder fma is exact and
+    // the result is x / u bit for bit. Rows only AND |q0| >= 2^-900 into the divergence
+    // predicate; the cold path tells a zero quotient (exact: x is never -0) from a
+    // nonzero one below the bound, which stops the launch (EMT_INEXACT_DIVISION, and
+    // emt_interpret reruns with the IEEE branch per row, EMT_FLAG_EXACT_DIVISION;
+    // tests/golden/subnormal_decay). Huge q0 needs no test: |x| > 1e12 already fails
     // the divergence check, which reports the same node as IEEE division would.
     bool rcp = false;
     int rcp_base = -1;
@@ -1254,7 +1257,7 @@ struct LitCtx {
     bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
     std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
     bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
-    int divguard = 1;                      // reciprocal-multiply division: 1 = detect |q| < 2^-960 (stop the
+    int divguard = 1;                      // reciprocal-multiply division: 1 = detect 0 < |q| < 2^-900 (stop the
                                            // launch, EMT_INEXACT_DIVISION), 2 = branch to IEEE x/u, 0 = none (dev)
     bool zterm = false;                    // drop zero-slot terms from sums
     int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
@@ -1393,10 +1396,11 @@ std::string task_literal(const Task& t, const LitCtx& c) {
                     o << "{ const double r_ = " << (t.f[3] >= 0 ? "LD(" + std::to_string(t.f[3]) + ")" : "SH[" + std::to_string(c.sh_rcp0 - t.f[3] - 2) + "]")
                       << "; const double d_ = " << lu(t.f[1])
                       << "; const double q_ = x * r_; double m_ = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); "
-                      << (c.divguard == 2 ? "if (__builtin_expect(!(fabs(q_) >= 0x1p-960), 0)) m_ = emt_div_ieee(x, d_); " : "")
+                      << (c.divguard == 2 ? "if (__builtin_expect(!(fabs(q_) >= 0x1p-900), 0)) m_ = emt_div_ieee(x, d_); " : "")
                       << "x = m_; "
                       << (c.dsum ? "dsum = dsum + fabs(x); } "
-                                 : c.divguard == 1 ? "dok = dok & (fabs(x) <= dlim) & (fabs(q_) >= 0x1p-960); } "
+                                 : c.divguard == 1 ? "dok = dok & (fabs(x) <= dlim) & (fabs(q_) >= 0x1p-900); } "
+                                 : c.divguard == 3 ? "dok = dok & (fabs(x) <= dlim) & !((fabs(q_) < 0x1p-900) & (q_ != 0.0)); } "
                                                    : "dok = dok & (fabs(x) <= dlim); } ");
                 else
                     o << "x = x / " << lu(t.f[1]) << "; dok = dok & (fabs(x) <= dlim); ";
@@ -2722,12 +2726,17 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "        for (int i = 0; i < " << s.nodes << "; ++i) if (!(fabs(LD(kVoff[i])) <= a.div_limit)) { bad = i; break; }\n"
           << "        if (bad != 0x7fffffff) { serr[lane] = bad; a.lane_err[4*gl] = 7; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = "
           << g.solve_layer << "; }\n"
-          // no divergence: a quotient below the Markstein bound (the only other cause
-          // of !dok); its node voltage is below 2^-959 (or zero)
+          // no divergence: some row's quotient was below the Markstein bound or zero
+          // (the other causes of !dok). Zero is exact (x is never -0 here); a nonzero
+          // quotient below 2^-900 leaves a node voltage in (0, 2^-899): stop the launch
           << (lctx.divguard == 1
-                  ? "        else { for (int i = 0; i < " + std::to_string(s.nodes) + "; ++i) if (fabs(LD(kVoff[i])) < 0x1p-959) { bad = i; break; }\n"
+                  ? "        else { for (int i = 0; i < " + std::to_string(s.nodes) + "; ++i) { const double v_ = fabs(LD(kVoff[i])); "
+                    "if (v_ < 0x1p-899 && v_ != 0.0) { bad = i; break; } }\n"
                     "          if (bad != 0x7fffffff) { serr[lane] = bad; a.lane_err[4*gl] = 66; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = bad; a.lane_err[4*gl+3] = " +
                         std::to_string(g.solve_layer) + "; } }\n"
+                  : lctx.divguard == 3
+                  ? "        else { bad = -1; serr[lane] = -1; a.lane_err[4*gl] = 66; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = " +
+                        std::to_string(g.solve_layer) + "; }\n"
                   : std::string())
           << "      }\n"
           << "      if (__syncthreads_or(warp == 0 && live && serr[lane] != 0x7fffffff)) { FAILPUB(); return; }\n"

@@ -818,8 +818,7 @@ emt_status check_lane_errors(emt_engine* e) {
     e->failed = 1;
     const int glane = e->lane_begin + best_lane;
     if (best->code == EMT_INEXACT_DIVISION)
-        return set_error(EMT_INEXACT_DIVISION, "node index " + std::to_string(best->index) +
-                                                   ": backward-substitution quotient below 2^-960 (step " +
+        return set_error(EMT_INEXACT_DIVISION, "backward-substitution quotient below 2^-900 (step " +
                                                    std::to_string(best->step) + ", lane " + std::to_string(glane) +
                                                    "); rerun with EMT_FLAG_EXACT_DIVISION");
     if (best->code == 64)  // written by the line-coupled persistent kernel (codegen.cpp)

@@ -280,7 +280,7 @@ def test_run_async_two_engines_alternating():
 
 
 def test_fast_division_detects_subnormal_quotients_exact_mode_is_bitwise():
-    """Backward-sweep quotients below 2^-960 (a decay through the subnormals): the fast
+    """Backward-sweep quotients below 2^-900 (a decay through the subnormals): the fast
     kernel stops with InexactDivision instead of misrounding, EMT_FLAG_EXACT_DIVISION
     (IEEE fallback per row) is bit-identical to the reference, and interpret() retries
     by itself (test_engine_matches_golden covers it through the golden)."""
