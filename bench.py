@@ -53,6 +53,14 @@ def load_case(name="ieee39"):
     return s, st, ids
 
 
+def load_scale_case(k: int):
+    """gen_scale_case(feeder33_pv3, k) as compiled by the reference (tools/make_scale_cases.py)."""
+    from paper_1903_01081_b200 import schedule as sch
+    s = gzip.open(os.path.join(DATA, f"feeder_scale{k}.cgmsched.gz"), "rt").read()
+    st, _ = sch.parse_state(gzip.open(os.path.join(DATA, f"feeder_scale{k}.state.gz"), "rt").read())
+    return s, st
+
+
 WORKLOADS = {
     "c3": ("ieee39-n1-sweep (BASELINE C3)", "ieee39", 1000),
     "c5": ("feeder33-pv-sweep shared G (BASELINE C5)", "feeder33_pv3", 4096),

@@ -84,7 +84,12 @@ enum { EMT_FLAG_EXACT_DIVISION = 2 };
  * emit_source (proj/src/codegen.cpp:84-230) retargeted to sm_100a — and uses
  * the table-driven generic kernel only when the specialised one cannot be
  * built (e.g. the hot arena exceeds shared memory). Both run on the GPU. */
-enum { EMT_KERNEL_AUTO = 0, EMT_KERNEL_SPECIALISED = 1, EMT_KERNEL_GENERIC = 2, EMT_KERNEL_TSIMT = 3 };
+enum { EMT_KERNEL_AUTO = 0, EMT_KERNEL_SPECIALISED = 1, EMT_KERNEL_GENERIC = 2, EMT_KERNEL_TSIMT = 3, EMT_KERNEL_SYSTEM = 4 };
+/* EMT_KERNEL_SYSTEM: one 1024-thread CTA per lane for large single systems (the
+ * reference's gen_scale_case, proj/src/bench.cpp:54-117): the arena stays in HBM,
+ * layers run in parallel over the block, the forward sweep in 32-column blocks and
+ * the backward sweep streams U through a TMA ring. AUTO selects it when a lane's
+ * arena does not fit in shared memory. Bit-identical to the other kernels. */
 /* EMT_KERNEL_TSIMT: generated task-SIMT kernel — one CTA per scenario lane, one
  * thread per task of a DAG wave (codegen.cpp, generate_tsimt); for few lanes
  * (latency) and for batches that should spread over every SM. */

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libemtb200.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("engine.cu", "host_schedule.cpp", "codegen.cpp", "emit_program.cpp", "jit.cpp", "waveform_text.cpp")]
-HEADERS = [os.path.join(HERE, "csrc", f) for f in ("host_schedule.hpp", "codegen.hpp", "jit.hpp", "libmcos.cuh")] + [
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("host_schedule.hpp", "codegen.hpp", "jit.hpp", "libmcos.cuh", "system_kernel.cuh")] + [
     os.path.join(ROOT, "include", "emt_b200.h")]
 CUDA = "/usr/local/cuda"
 

@@ -462,6 +462,8 @@ emt_step_kernel(const DevPlan P, const int step0, const int nsteps, const int ro
     for (int s = tl; s < P.extent; s += 32) P.arena[static_cast<size_t>(s) * P.W + lane] = A[s];
 }
 
+#include "system_kernel.cuh"
+
 // ----------------------------------------------------------------- host side
 
 thread_local std::string g_last_error;
@@ -531,6 +533,8 @@ struct emt_engine {
     double divergence_limit = kDefaultDivergence;
     std::vector<double> host_ctab;       // consts x W (this engine's lanes)
     int kernel_mode = EMT_KERNEL_GENERIC;
+    SysPlan sys{};               // EMT_KERNEL_SYSTEM tables (system_kernel.cuh)
+    size_t sys_smem = 0;
     GeneratedKernel gen;
     JitModule jit;
     std::string summary;
@@ -794,6 +798,173 @@ emt_status build_plan(emt_engine* e, const double* const_table, int width, const
     return EMT_OK;
 }
 
+/// Tables of the one-CTA-per-lane system kernel (system_kernel.cuh): forward column
+/// blocks of 32 with their tiles and trailing segments, and the backward stream
+/// (rows descending: the row's U entries past the diagonal, the diagonal, its reciprocal).
+emt_status build_system_plan(emt_engine* e) {
+    const Schedule& s = e->sched;
+    const DevPlan& P = e->plan;
+    SysPlan& S = e->sys;
+    if (s.nodes > 0 && s.dim != s.nodes)
+        return set_error(EMT_MALFORMED_DOCUMENT, "system kernel: matrix dimension differs from the node count");
+    const int dim = s.dim;
+    S.nblk = (dim + 31) / 32;
+    std::vector<int> kin(static_cast<size_t>(dim));
+    std::vector<unsigned> mask(static_cast<size_t>(dim), 0u), blk(static_cast<size_t>(std::max(1, S.nblk)), 0u);
+    std::vector<std::vector<int4>> segs(static_cast<size_t>(std::max(1, S.nblk)));
+    for (int r = 0; r < dim; ++r) {
+        const int b = r / 32, kb = s.l_row_ptr[static_cast<size_t>(r)], ke = s.l_row_ptr[static_cast<size_t>(r) + 1];
+        int k = kb;
+        while (k < ke) {  // runs of entries per column block, ascending
+            const int cb = s.l_col[static_cast<size_t>(k)] / 32;
+            int k1 = k;
+            while (k1 < ke && s.l_col[static_cast<size_t>(k1)] / 32 == cb) ++k1;
+            if (cb < b) {
+                segs[static_cast<size_t>(cb)].push_back(make_int4(r, k, k1, 0));
+            } else {  // cb == b: the row's own tile (strictly lower: columns < r)
+                kin[static_cast<size_t>(r)] = k;
+                for (int q = k; q < k1; ++q) mask[static_cast<size_t>(r)] |= 1u << (s.l_col[static_cast<size_t>(q)] - 32 * b);
+            }
+            k = k1;
+        }
+        if (mask[static_cast<size_t>(r)] == 0u) kin[static_cast<size_t>(r)] = ke;
+        blk[static_cast<size_t>(b)] |= mask[static_cast<size_t>(r)];
+    }
+    // forward rounds: each block's trailing segments (one row's terms in the block's
+    // columns, <= 32) packed into rounds whose products fit the shared buffer in a
+    // transposed layout: term j of the round's piece p sits at j * P' + p (P' = pieces
+    // rounded up to odd), so a warp reading term j of 32 pieces is bank-conflict free
+    std::vector<int> rnd_ptr{0}, fsrc, fcol, fdst;
+    std::vector<int4> rnd, piece;
+    for (int b = 0; b < std::max(1, S.nblk); ++b) {
+        const auto& sv = segs[static_cast<size_t>(b)];
+        size_t i0 = 0;
+        do {  // one round: pieces [i0, i1)
+            size_t i1 = i0;
+            int maxlen = 0;
+            while (i1 < sv.size()) {
+                const int len = sv[i1].z - sv[i1].y;
+                const int np = (static_cast<int>(i1 - i0) + 1) | 1;
+                if (i1 > i0 && np * std::max(maxlen, len) > kSysFcap) break;
+                maxlen = std::max(maxlen, len);
+                ++i1;
+            }
+            const int pp = static_cast<int>(i1 - i0) | 1;
+            const int e0 = static_cast<int>(fsrc.size()), p0 = static_cast<int>(piece.size());
+            for (size_t i = i0; i < i1; ++i) {
+                const int4& sg = sv[i];
+                const int pi = static_cast<int>(i - i0);
+                piece.push_back(make_int4(sg.x, pi, sg.z - sg.y, pp));
+                for (int q = sg.y; q < sg.z; ++q) {
+                    fsrc.push_back(q);
+                    fcol.push_back(s.l_col[static_cast<size_t>(q)]);
+                    fdst.push_back((q - sg.y) * pp + pi);
+                }
+            }
+            rnd.push_back(make_int4(e0, static_cast<int>(fsrc.size()), p0, static_cast<int>(piece.size())));
+            i0 = i1;
+        } while (i0 < sv.size());  // every block has >= 1 (possibly empty) round: it stages the next tile
+        rnd_ptr.push_back(static_cast<int>(rnd.size()));
+    }
+    if (fsrc.empty()) {
+        fsrc.push_back(0);
+        fcol.push_back(0);
+        fdst.push_back(0);
+    }
+    std::vector<int> tsrc(static_cast<size_t>(std::max(1, S.nblk)) * 1024, -1);
+    for (int r = 0; r < dim; ++r) {
+        const int b = r / 32, j = r % 32;
+        for (int q = kin[static_cast<size_t>(r)]; q < s.l_row_ptr[static_cast<size_t>(r) + 1]; ++q)
+            tsrc[static_cast<size_t>(b) * 1024 + j * 32 + (s.l_col[static_cast<size_t>(q)] - 32 * b)] = q;
+    }
+    if (s.l_col.empty()) std::fill(tsrc.begin(), tsrc.end(), -1);
+    S.fstream_len = static_cast<long long>(fsrc.size());
+    std::vector<int> bcol, bsrc, brow_len;
+    S.pmax = 1;
+    for (int i = dim - 1; i >= 0; --i) {
+        const int ub = s.u_row_ptr[static_cast<size_t>(i)], ue = s.u_row_ptr[static_cast<size_t>(i) + 1];
+        brow_len.push_back(2 * (ue - ub - 1) + (ue - ub > 1 && s.u_col[static_cast<size_t>(ub) + 1] == i + 1 ? 1 : 0));
+        S.pmax = std::max(S.pmax, ue - ub - 1);
+        for (int k = ub + 1; k < ue; ++k) {
+            bcol.push_back(s.u_col[static_cast<size_t>(k)]);
+            bsrc.push_back(k);
+        }
+        bcol.push_back(0);  // diagonal
+        bsrc.push_back(ub);
+        bcol.push_back(0);  // its reciprocal
+        bsrc.push_back(-1 - ub);
+    }
+    const size_t padded = std::max<size_t>(kSysChunk, (bcol.size() + kSysChunk - 1) / kSysChunk * kSysChunk);
+    bcol.resize(padded, 0);
+    bsrc.resize(padded, INT_MIN);
+    S.stream_len = static_cast<long long>(padded);
+    S.stream_chunks = static_cast<int>(padded / kSysChunk);
+    const int* d = nullptr;
+    EMT_TRY(e->upload(kin, S.fwd_kin));
+    EMT_TRY(e->upload(mask, S.fwd_mask));
+    EMT_TRY(e->upload(blk, S.blk_cols));
+    EMT_TRY(e->upload(rnd_ptr, S.rnd_ptr));
+    EMT_TRY(e->upload(rnd, S.rnd));
+    EMT_TRY(e->upload(piece, S.piece));
+    EMT_TRY(e->upload(fsrc, S.fsrc));
+    EMT_TRY(e->upload(fcol, S.fcol));
+    EMT_TRY(e->upload(fdst, S.fdst));
+    EMT_TRY(e->upload(tsrc, S.tsrc));
+    EMT_TRY(e->upload(bcol, S.bcol));
+    EMT_TRY(e->upload(bsrc, S.bsrc));
+    EMT_TRY(e->upload(brow_len, d));
+    S.brow = d;
+    CUDA_TRY(cudaMalloc(&S.bval, padded * sizeof(double) * static_cast<size_t>(e->W)));
+    e->allocations.push_back(S.bval);
+    CUDA_TRY(cudaMalloc(&S.fval, static_cast<size_t>(S.fstream_len) * sizeof(double) * static_cast<size_t>(e->W)));
+    e->allocations.push_back(S.fval);
+    CUDA_TRY(cudaMalloc(&S.tval, tsrc.size() * sizeof(double) * static_cast<size_t>(e->W)));
+    e->allocations.push_back(S.tval);
+    S.work = nullptr;
+    if (e->W > 1) {
+        CUDA_TRY(cudaMalloc(&S.work, static_cast<size_t>(P.lane_stride) * sizeof(double) * static_cast<size_t>(e->W)));
+        e->allocations.push_back(S.work);
+    }
+    // dynamic shared memory: TMA ring (values, columns), mbarriers, the forward tile, v
+    size_t off = 0;
+    S.smem_ring_v = static_cast<int>(off);
+    off += static_cast<size_t>(kSysRing) * kSysChunk * sizeof(double);
+    S.smem_ring_c = static_cast<int>(off);
+    off += static_cast<size_t>(kSysRing) * kSysChunk * sizeof(int);
+    S.smem_mbar = static_cast<int>(off);
+    off += static_cast<size_t>(kSysRing) * 8;
+    S.smem_flags = static_cast<int>(off);
+    off += 16;
+    S.smem_desc = static_cast<int>(off);
+    off += 2 * 4 * sizeof(double);
+    S.smem_pbuf = static_cast<int>(off);
+    S.pmax += 8;  // room for the zero padding to a multiple of eight terms
+    off += 2 * static_cast<size_t>(S.pmax) * sizeof(double);
+    S.smem_fp = static_cast<int>(off);
+    off += static_cast<size_t>(kSysFcap) * sizeof(double);
+    S.smem_tile = static_cast<int>(off);
+    off += 32 * 33 * sizeof(double);
+    S.smem_xs = static_cast<int>(off);
+    off += static_cast<size_t>(std::max(1, dim)) * sizeof(double);
+    if (S.pmax + 2 > (kSysRing - 1) * kSysChunk)  // a row's stream entries must fit in the ring at once
+        return set_error(EMT_CAPACITY_EXCEEDED, "system kernel: a U row of " + std::to_string(S.pmax) + " entries");
+    int dev_smem = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    if (off + 1024 > static_cast<size_t>(dev_smem))  // static shared: s_flag, s_bad
+        return set_error(EMT_CAPACITY_EXCEEDED, "system kernel: " + std::to_string(dim) +
+                                                    " nodes exceed the shared-memory copy of v");
+    e->sys_smem = off;
+    S.prof = nullptr;
+    const char* pf = dev_env("EMTB200_CG_PROF");
+    if (pf && std::strcmp(pf, "0") != 0) {
+        CUDA_TRY(cudaMalloc(&e->d_prof, 32 * 64 * sizeof(long long)));
+        CUDA_TRY(cudaMemset(e->d_prof, 0, 32 * 64 * sizeof(long long)));
+        S.prof = e->d_prof;
+    }
+    CUDA_TRY(cudaFuncSetAttribute(emt_system_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(off)));
+    return EMT_OK;
+}
+
 emt_status check_lane_errors(emt_engine* e) {
     std::vector<LaneError> errs(static_cast<size_t>(e->W));
     CUDA_TRY(cudaMemcpy(errs.data(), e->plan.lane_err, errs.size() * sizeof(LaneError), cudaMemcpyDeviceToHost));
@@ -821,6 +992,9 @@ emt_status check_lane_errors(emt_engine* e) {
         return set_error(EMT_INEXACT_DIVISION, "backward-substitution quotient below 2^-900 (step " +
                                                    std::to_string(best->step) + ", lane " + std::to_string(glane) +
                                                    "); rerun with EMT_FLAG_EXACT_DIVISION");
+    if (best->code == 64 && best->index == -2)  // system kernel (system_kernel.cuh)
+        return set_error(EMT_CUDA_ERROR, "system kernel: backward-sweep handoff wait timed out (step " +
+                                             std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
     if (best->code == 64)  // written by the line-coupled persistent kernel (codegen.cpp)
         return set_error(EMT_CUDA_ERROR, "line-coupling progress wait timed out or a peer CTA / rank failed (step " +
                                              std::to_string(best->step) + ", lane " + std::to_string(glane) + ")");
@@ -907,6 +1081,15 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
     }
     e->kernel_mode = EMT_KERNEL_GENERIC;
     e->summary = "generic table-driven kernel, grid=" + std::to_string(e->grid) + " block=" + std::to_string(e->block);
+    if (c.kernel == EMT_KERNEL_SYSTEM) {
+        EMT_TRY(build_system_plan(e.get()));
+        e->kernel_mode = EMT_KERNEL_SYSTEM;
+        e->summary = "system kernel: one " + std::to_string(kSysThreads) + "-thread CTA per lane, grid=" +
+                     std::to_string(e->W) + " fwd_blocks=" + std::to_string(e->sys.nblk) +
+                     " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " smem=" + std::to_string(e->sys_smem);
+        *out = e.release();
+        return EMT_OK;
+    }
     const char* kenv = dev_env("EMTB200_KERNEL");
     if (c.kernel == EMT_KERNEL_AUTO && kenv && std::strcmp(kenv, "tsimt") == 0) c.kernel = EMT_KERNEL_TSIMT;
     if (c.kernel == EMT_KERNEL_TSIMT) {
@@ -988,6 +1171,13 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         } else if (c.kernel == EMT_KERNEL_SPECIALISED) {
             return set_error(gf.code ? gf.code : EMT_CUDA_ERROR,
                              "specialised kernel unavailable: " + (gf.message.empty() ? log : gf.message));
+        } else if (!e->plan.use_smem && build_system_plan(e.get()) == EMT_OK) {
+            // the lane does not fit in shared memory: a whole CTA per lane instead of one warp
+            e->kernel_mode = EMT_KERNEL_SYSTEM;
+            e->summary = "system kernel: one " + std::to_string(kSysThreads) + "-thread CTA per lane, grid=" +
+                         std::to_string(e->W) + " fwd_blocks=" + std::to_string(e->sys.nblk) +
+                         " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " smem=" + std::to_string(e->sys_smem) +
+                         " (specialised kernel unavailable: " + (gf.message.empty() ? log.substr(0, 300) : gf.message) + ")";
         } else {
             e->summary += " (specialised kernel unavailable: " + (gf.message.empty() ? log.substr(0, 300) : gf.message) + ")";
         }
@@ -1097,6 +1287,12 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
             driver()->GetErrorString(r, &msg);
             return set_error(EMT_CUDA_ERROR, std::string("cuLaunchKernel: ") + (msg ? msg : "?"));
         }
+    } else if (e->kernel_mode == EMT_KERNEL_SYSTEM) {
+        DevPlan P = e->plan;
+        P.waves = e->d_waves;
+        P.refactored = e->d_refactored;
+        emt_system_kernel<<<e->W, kSysThreads, e->sys_smem, e->stream>>>(P, e->sys, e->step, steps, e->rows);
+        CUDA_TRY(cudaGetLastError());
     } else {
         DevPlan P = e->plan;
         P.waves = e->d_waves;
@@ -1199,7 +1395,7 @@ emt_status emt_engine_stage(emt_engine* e, const double* initial, int64_t initia
                                                      " x width " + std::to_string(e->width));
     if (e->staged) return set_error(EMT_NON_POSITIVE_INPUT, "a staged batch is waiting for emt_engine_commit");
     const size_t W = static_cast<size_t>(e->W), width = static_cast<size_t>(e->width), lb = static_cast<size_t>(e->lane_begin);
-    if (const_table != nullptr && e->kernel_mode != EMT_KERNEL_GENERIC) {
+    if (const_table != nullptr && (e->kernel_mode == EMT_KERNEL_SPECIALISED || e->kernel_mode == EMT_KERNEL_TSIMT)) {
         // constants compiled in as immediates must keep their values (an isomorphic batch)
         for (size_t q = 0; q < e->inv_slots.size(); ++q) {
             const double* row = const_table + static_cast<size_t>(e->inv_slots[q]) * width + lb;

@@ -54,7 +54,7 @@ class _Config(ctypes.Structure):
                 ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
-KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT, KERNEL_SYSTEM = 0, 1, 2, 3, 4
 FLAG_TENSOR_SOLVE = 1
 FLAG_EXACT_DIVISION = 2  # IEEE fallback in every backward row (include/emt_b200.h)
 

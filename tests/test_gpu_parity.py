@@ -14,7 +14,8 @@ from paper_1903_01081_b200 import engine
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT}
+KERNELS = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "tsimt": engine.KERNEL_TSIMT,
+           "system": engine.KERNEL_SYSTEM}
 
 
 @pytest.mark.parametrize("kernel", sorted(KERNELS))
