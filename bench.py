@@ -66,11 +66,15 @@ WORKLOADS = {
     "c5": ("feeder33-pv-sweep shared G (BASELINE C5)", "feeder33_pv3", 4096),
     "c2": ("ieee39 single scenario (BASELINE C2)", "ieee39", 1),
     "c4": ("ieee39 x120 line-coupled single system, split at Bergeron lines (BASELINE C4)", "ieee39_c4", 120),
+    # the reference's own large-scale case (gen_scale_case, proj/src/bench.cpp:54-117):
+    # k feeder copies joined at the root node, one system, --scenarios = k (replicas only across GPUs)
+    "scale": ("gen_scale_case(feeder33_pv3, k) single large system (reference format)", "feeder_scale", 128),
 }
 
 
 METRIC = {"c3": "scenario-steps/sec for N-1 EMT batch", "c5": "scenario-steps/sec for shared-G EMT batch",
-          "c2": "us per time step on single case", "c4": "us per time step on large single case"}
+          "c2": "us per time step on single case", "c4": "us per time step on large single case",
+          "scale": "us per time step on large single case"}
 
 
 def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3"):
@@ -88,6 +92,9 @@ def build_batch(scenarios: int, lo: int = 0, hi: int = -1, workload: str = "c3")
         while len(grid) < scenarios:  # weak scaling beyond a square grid: shifted repeats
             grid += [(i + 1e-3 * len(grid), t) for i, t in grid[: scenarios - len(grid)]]
         return sch.pv_sweep_batch(s, st, pvm, grid[lo:hi]), sch.parse_info(s)
+    if workload == "scale":  # one lane: gen_scale_case with k = scenarios, compiled by the reference
+        s, st = load_scale_case(scenarios)
+        return sch.Batch(s, sch.parse_info(s).const_table, st, 1), sch.parse_info(s)
     if workload == "c4":  # one system of `scenarios` IEEE-39 copies (one lane each) coupled by lines
         from paper_1903_01081_b200 import lines
         s, st, ids = load_case("ieee39_c4")
@@ -232,10 +239,14 @@ def run_ours(args):
     # `--scenarios` lanes are split into contiguous shards, one per GPU; weak scaling
     # (`--scaling weak`): `--scenarios` per GPU. C4 is ONE system of `--scenarios`
     # line-coupled copies split over the GPUs (always strong).
-    weak = args.scaling == "weak" and args.workload != "c4"
+    weak = args.scaling == "weak" and args.workload not in ("c4", "scale")
     W = args.scenarios * world if weak else args.scenarios
-    lo, hi = sharding.shard_bounds(W, world, rank)
-    batch, info = build_batch(W, lo, hi, args.workload)
+    if args.workload == "scale":  # one unsplittable system (shared root node): replicas only, one per GPU
+        batch, info = build_batch(args.scenarios, workload="scale")
+        W, lo, hi = 1, 0, 1
+    else:
+        lo, hi = sharding.shard_bounds(W, world, rank)
+        batch, info = build_batch(W, lo, hi, args.workload)
     S = args.emt_steps
     total_steps = (args.warmup + args.steps) * S
 
@@ -392,7 +403,7 @@ def run_ours(args):
         h2d = batch.const_table.nbytes + batch.initial.nbytes  # per bench step (S passes)
         d2h = S * len(info.channels) * (hi - lo) * 8
         metric, unit, hib, val, e2e_val = (METRIC[args.workload], "scenario-steps/s", True, value, W * S / e2e_max)
-        if args.workload in ("c2", "c4"):  # latency of one system: µs per EMT time step
+        if args.workload in ("c2", "c4", "scale"):  # latency of one system: µs per EMT time step
             metric, unit, hib = METRIC[args.workload], "us/step", False
             val, e2e_val = 1e3 * max_ms / (args.steps * S), 1e6 * e2e_max / S
         out = {
@@ -411,8 +422,10 @@ def run_ours(args):
             "config": {"workload": wl_name, "scenarios": W, "scenarios_per_gpu": hi - lo,
                        "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
                        "components": info.comps, "case": WORKLOADS[args.workload][1],
-                       "parallelism": f"{W} scenario lanes in contiguous shards over {world} GPU(s), no per-step "
-                                      "traffic" if args.workload != "c4" else f"{W} line-coupled copies split over {world} GPU(s)",
+                       "parallelism": (f"{W} line-coupled copies split over {world} GPU(s)" if args.workload == "c4"
+                                       else f"one k={args.scenarios} system per GPU (replicas only: the shared root "
+                                            "node couples every copy into one LU)" if args.workload == "scale"
+                                       else f"{W} scenario lanes in contiguous shards over {world} GPU(s), no per-step traffic"),
                        "l2": "flushed (256 MiB write) between timed launches"},
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "matches_device_run": e2e_digest_ok,
@@ -445,6 +458,20 @@ def run_ours(args):
                                     "frac": dflops / dpeak, "flops_per_scenario_step": 2.0 * n * n,
                                     "peak_source": "torch.matmul float64 8192^3 on this GPU, best of 10",
                                     "note": "the solve is one part of the pass: the kernel as a whole is in 'roofline'"}
+        if args.workload == "scale":
+            # the bound that matters: in the reference's order every backward row
+            # subtracts its smallest column first, the row finished last, so with the shared root's
+            # fill the sweep is ONE chain of u_nnz dependent FP64 subtractions; floor = u_nnz x the
+            # dependent DADD latency (8.1 cycles, tools/micro/lat.cu on B200) at the sampled SM clock
+            mat = next(l for l in batch.schedule.splitlines() if l.startswith("MATRIX")).split()
+            unnz = int(mat[4].split("=")[1])
+            mhz = clk.get("sm_mhz") or 1965.0
+            floor_us = unnz * 8.1 / mhz
+            out["roofline_chain"] = {"bound": "latency", "chain_ops": unnz, "dadd_latency_cycles": 8.1,
+                                     "sm_mhz": mhz, "floor_us_per_step": floor_us, "achieved_us_per_step": val,
+                                     "frac": floor_us / val,
+                                     "note": "backward-sweep dependency chain of the reference's row order "
+                                             "(sparse.cpp:161-170); HBM 'roofline' above is far from binding"}
         if cpu is not None:
             out["cpu_baseline"] = cpu
         if par is not None:
@@ -489,9 +516,9 @@ def cpu_baseline(args, batch, got, total_steps):
     rep.update({"against": "reference emtgrid::interpret (oracle/_ref/libemtref.so) on lane shards",
                 "lanes": W, "passes": total_steps})
     timed = S * args.steps
-    if args.workload == "c2":
+    if args.workload in ("c2", "scale"):
         cpu = {"value": 1e6 * res["seconds"] / timed, "unit": "us/step", "cores": 1, "kind": "reference",
-               "sample": f"1 scenario x {total_steps} EMT steps ({S * args.warmup} warm-up), emtgrid::interpret "
+               "sample": f"1 system x {total_steps} EMT steps ({S * args.warmup} warm-up), emtgrid::interpret "
                          "(oracle/_ref/libemtref.so), single thread"}
     else:
         cpu = {"value": W * timed / res["seconds"], "unit": "scenario-steps/s", "cores": res["procs"],
@@ -510,7 +537,7 @@ def run_reference(args):
         return
     from oracle import parity
     S = args.cpu_emt_steps_per_step or args.emt_steps
-    weak = args.scaling == "weak" and args.workload != "c4"
+    weak = args.scaling == "weak" and args.workload not in ("c4", "scale")
     W0 = args.scenarios * world if weak else args.scenarios
     batch, info = build_batch(W0, workload=args.workload)
     kind = "reference"
@@ -522,7 +549,7 @@ def run_reference(args):
         res = parity.reference_sweep(batch, S * (args.warmup + args.steps), warmup=S * args.warmup)
         W, secs, procs = batch.width, res["seconds"], res["procs"]
     metric, unit, hib, value = METRIC[args.workload], "scenario-steps/s", True, W * S * args.steps / secs
-    if args.workload in ("c2", "c4"):
+    if args.workload in ("c2", "c4", "scale"):
         metric, unit, hib, value = METRIC[args.workload], "us/step", False, 1e6 * secs / (S * args.steps)
     out = {
         "impl": "reference",
@@ -552,7 +579,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3",
-                    help="c3 = IEEE-39 N-1 sweep (headline), c5 = feeder PV shared-G sweep, c2 = single scenario")
+                    help="c3 = IEEE-39 N-1 sweep (headline), c5 = feeder PV shared-G sweep, c2 = single scenario, "
+                         "c4 = line-coupled 120-copy system, scale = gen_scale_case k (--scenarios) single system")
     ap.add_argument("--scenarios", type=int, default=None,
                     help="scenarios in total (strong scaling) or per GPU (--scaling weak)")
     ap.add_argument("--emt-steps", type=int, default=1000, help="EMT passes per bench step (one launch)")
@@ -574,6 +602,8 @@ def main():
         args.warmup = 3
     if args.scenarios is None:
         args.scenarios = WORKLOADS[args.workload][2]
+    if args.workload == "scale" and args.emt_steps == 1000:
+        args.emt_steps = 50  # k=128: ~8 ms per pass here and in the reference
     if args.impl == "reference":
         run_reference(args)
     else:
