@@ -302,6 +302,7 @@ def run_ours(args):
     # whole arena + constant table), runs S passes and streams the waveform rows back
     # into pinned host memory chunk by chunk (D2H overlapped with the next chunk).
     e2e_local, e2e_digest_ok = float('nan'), None
+    cold = None
     if not args.skip_e2e and args.workload == "c4" and world > 1:
         # line-split across ranks: reload the shard from pinned host, step with the
         # exchange, read the shard's waveform rows back
@@ -366,6 +367,16 @@ def run_ours(args):
         e2e_digest_ok = bool(np.array_equal(host_waves, eng.waves(0, S).values))
         for x in engs:
             x.close()
+        if world == 1 and args.workload != "scale":
+            # cold start: a fresh process with empty in-memory and on-disk cubin caches (JIT included)
+            with tempfile.TemporaryDirectory() as cdir:
+                r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "cold_start.py"), args.workload,
+                                    str(W), str(S), str(dev)], capture_output=True, text=True, timeout=600,
+                                   env=dict(os.environ, EMTB200_CACHE=cdir))
+            try:
+                cold = json.loads(r.stdout.strip().splitlines()[-1])
+            except (ValueError, IndexError):
+                cold = {"error": (r.stderr or r.stdout)[-300:]}
 
     if world > 1:
         max_ms = sharding.reduce_max(dist, local_ms, device=cdev)
@@ -447,6 +458,14 @@ def run_ours(args):
                                  "kernel is bound by its per-pass instruction latency, not HBM (DESIGN.md §3.3)"},
             "clocks": clk,
         }
+        if cold is not None and "total_s" in cold:
+            out["e2e_cold"] = {"value": (1e6 * cold["total_s"] / S) if unit == "us/step" else W * S / cold["total_s"],
+                               "unit": unit, "seconds": cold["total_s"], "engine_create_s": cold["create_s"],
+                               "jit_s": cold["jit_s"], "first_step_s": cold["run_s"],
+                               "note": "one bench step from a fresh process with empty cubin caches: engine creation "
+                                       "(parse + code generation + NVRTC + module load) + H2D + S passes + D2H"}
+        elif cold is not None:
+            out["e2e_cold"] = cold
         if args.tensor_solve and "solve=dmma" in eng.summary:
             # the batched V = G^-1 I product on the FP64 tensor cores, 2 n^2 flops
             # per scenario-step, against this GPU's FP64 GEMM rate measured here (cuBLAS DGEMM
