@@ -234,3 +234,113 @@ def single_line_spec(zc: float, tau: float, width: int = 1) -> LineSpec:
         peers[l, 0] = (l, 1)
         peers[l, 1] = (l, 0)
     return LineSpec(["la", "lb"], [zc, zc], [tau, tau], peers)
+
+
+# ---------------------------------------------------------------- document kind
+
+LINE_KIND = "transmission_line"
+LINE_PARAMS = ("surge_impedance", "travel_time")
+
+
+class LineDocumentError(ValueError):
+    """A `transmission_line` component failed validation; `code` names the reference's
+    ErrorCode (proj/include/emtgrid/common.hpp:11-33) the check mirrors, `where` its id."""
+
+    def __init__(self, code: str, where: str, message: str):
+        super().__init__(f"{code}: {message} (at {where})")
+        self.code, self.where = code, where
+
+
+def line_end_names(line_id: str) -> Tuple[str, str]:
+    """The two ends of line `line_id` (placeholder pairs `<end>_h` / `<end>_z`)."""
+    return f"{line_id}__a", f"{line_id}__b"
+
+
+def expand_document(document: str) -> Tuple[str, LineSpec]:
+    """The `transmission_line` document kind (EXTENSION): parse and
+    validate every line the way the reference's check_component validates its kinds
+    (proj/src/model.cpp:154-222: arity, allowed parameter keys, strictly positive
+    finite values; identifiers and node references as in parse, model.cpp), then
+    stamp each line as its two placeholder ends (add_line_end: surge resistor +
+    history current source at each terminal bus). Returns the reference-schema
+    document (compile it with the reference's parse_model -> compile_task) and the
+    width-1 LineSpec pairing each line's two ends, for `bergeron_batch`.
+
+        {"id": "L1", "kind": "transmission_line", "terminals": ["b16", "b03"],
+         "params": {"surge_impedance": 300.0, "travel_time": 3.3e-4}}
+
+    A line's ends are Norton equivalents to ground at its two buses (lossless
+    Bergeron model); it adds no off-diagonal term to G, so the buses it joins may
+    lie in otherwise separate subnetworks (each needs its own ground path)."""
+    doc = json.loads(document)
+    comps = doc.get("components", [])
+    nodes = set(doc.get("nodes", []))
+    dt = float(doc.get("task", {}).get("dt", 0.0))
+    ids = [c.get("id", "") for c in comps]
+    out = dict(doc)
+    out["components"] = []
+    ends, zcs, taus = [], [], []
+    for c in comps:
+        if c.get("kind") != LINE_KIND:
+            out["components"].append(c)
+            continue
+        where = c.get("id", "")
+        if not where:
+            raise LineDocumentError("MalformedDocument", "components", "transmission line without an id")
+        if ids.count(where) > 1:
+            raise LineDocumentError("DuplicateIdentifier", where, "component id declared twice")
+        terms = c.get("terminals", [])
+        if len(terms) != 2:
+            raise LineDocumentError("InvalidParameter", where,
+                                    f"transmission_line needs 2 terminals, got {len(terms)}")
+        for t in terms:
+            if t == "0":
+                raise LineDocumentError("InvalidParameter", where, "a line end must sit at a bus, not ground")
+            if t not in nodes:
+                raise LineDocumentError("DanglingReference", t, f"terminal of {where} is not a declared node")
+        if terms[0] == terms[1]:
+            raise LineDocumentError("InvalidParameter", where, "line ends must be two different buses")
+        params = c.get("params", {})
+        for k in params:
+            if k not in LINE_PARAMS:
+                raise LineDocumentError("InvalidParameter", where, f"unknown parameter '{k}'")
+        vals = []
+        for k in LINE_PARAMS:
+            v = params.get(k)
+            if not isinstance(v, (int, float)) or isinstance(v, bool):
+                raise LineDocumentError("InvalidParameter", where, f"missing numeric parameter '{k}'")
+            v = float(v)
+            if not (v > 0.0) or not math.isfinite(v):
+                raise LineDocumentError("InvalidParameter", where, f"{k} must be strictly positive")
+            vals.append(v)
+        zc, tau = vals
+        if dt > 0.0 and delay_split(tau, dt)[0] < 2:
+            raise LineDocumentError("InvalidParameter", where, "travel_time must be at least 2 dt")
+        for end, bus in zip(line_end_names(where), terms):
+            for pid in end_ids(end):
+                if pid in ids:
+                    raise LineDocumentError("DuplicateIdentifier", pid, "collides with a line-end placeholder id")
+            add_line_end(out, end, bus, zc)
+            ends.append(end)
+            zcs.append(zc)
+            taus.append(tau)
+    E = len(ends)
+    peers = np.zeros((1, E, 2), dtype=np.int64)
+    for e in range(0, E, 2):  # the two ends of one line point at each other
+        peers[0, e] = (0, e + 1)
+        peers[0, e + 1] = (0, e)
+    return json.dumps(out, indent=1) + "\n", LineSpec(ends, zcs, taus, peers)
+
+
+def document_batch(document: str, compile_fn) -> sch.Batch:
+    """A document with `transmission_line` components -> executable width-1 batch:
+    expand_document, then `compile_fn(reference_document) -> (schedule text, initial
+    arena)` (the reference compiler, parse_model -> compile_task), then the line ends
+    become NortonBergeron processes (bergeron_batch)."""
+    expanded, spec = expand_document(document)
+    schedule, initial = compile_fn(expanded)
+    cids = [c["id"] for c in json.loads(expanded)["components"]]
+    if not spec.ends:
+        info = sch.parse_info(schedule)
+        return sch.Batch(schedule, info.const_table, np.asarray(initial, dtype=np.float64), 1)
+    return bergeron_batch(schedule, np.asarray(initial, dtype=np.float64), cids, spec)

@@ -255,3 +255,19 @@ def test_line_split_two_processes_bitwise(mode):
                          cwd=root, env=env, capture_output=True, text=True, timeout=600)
     lines = [l for l in out.stdout.splitlines() if l.startswith("linesplit") and "bitwise" in l]
     assert lines and "bitwise OK" in lines[-1], out.stdout[-2000:] + out.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["auto", "generic", "system"])
+def test_document_declared_line_on_device(kernel):
+    """A document with a `transmission_line` component (tests/golden/lines/line_doc.document.json,
+    compiled by tools/make_line_doc_fixture.py) runs bit-identically to the C oracle."""
+    from paper_1903_01081_b200 import engine
+    d = os.path.join(GOLDEN, "lines")
+    s = gzip.open(os.path.join(d, "line_doc.cgmsched.gz"), "rt").read()
+    st, _ = sch.parse_state(gzip.open(os.path.join(d, "line_doc.state.gz"), "rt").read())
+    k = {"auto": engine.KERNEL_AUTO, "generic": engine.KERNEL_GENERIC, "system": engine.KERNEL_SYSTEM}[kernel]
+    got = engine.interpret(s, st, 400, kernel=k)
+    want = oracle.Schedule(s).interpret(st, 400)
+    assert bitwise_equal(got.values, want.waves)
+    assert np.abs(want.waves[:, 1]).max() > 0.0  # the wave reached the far bus
