@@ -1256,15 +1256,11 @@ struct LitCtx {
     bool sw_slim = false;                  // switch hot path only tests for a change; stores go to the cold path
     bool fused_pass = false;               // emit fused Norton tasks in their fused form (passes after the first)
     std::function<int(int)> lit_init;      // switch initial state: 0/1 when lane-invariant, -1 otherwise
-    bool dsum = true;                      // divergence: sum of |x| per thread (cold exact scan on alarm)
     int divguard = 1;                      // reciprocal-multiply division: 1 = detect 0 < |q| < 2^-900 (stop the
                                            // launch, EMT_INEXACT_DIVISION), 2 = branch to IEEE x/u, 0 = none (dev)
     bool zterm = false;                    // drop zero-slot terms from sums
-    int hoist = -1;                        // >= 0: the task's global loads were issued at the phase start (ids)
     int task_id = -1;                      // the task's index (per-task registers)
     int sh_rcp0 = 0;                       // SH index of the first pivot reciprocal (shared factors)
-    bool berg_pf = false;                  // line ends: peer histories loaded one pass ahead into registers
-    std::string* deferred = nullptr;       // hoisted line end: its global stores go here (phase end)
 };
 
 std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c, const std::string& sfx = "_") {
@@ -1285,84 +1281,9 @@ std::string expand_lit(const char* tpl, const Task& t, const LitCtx& c, const st
     return out;
 }
 
-/// Loads / compute / store of one task as separate statement strings with
-/// variables suffixed `sfx`, so a batch of independent tasks can issue all of
-/// its shared-memory loads before any compute (the compiler does not hoist
-/// loads over the stores of earlier tasks on its own). False for kinds
-/// without a split form.
-bool task_literal_parts(const Task& t, const LitCtx& c, const std::string& sfx, std::string& ld, std::string& cp,
-                        std::string& st) {
-    if (t.fused && c.fused_pass) {
-        const std::string vb = std::to_string(t.f[1]), va = std::to_string(t.f[0]), h = std::to_string(t.f[3]);
-        ld = "const double vb" + sfx + " = LD(" + vb + "); const double va" + sfx + " = LD(" + va + "); const double hp" + sfx +
-             " = LD(" + h + "); const double g" + sfx + " = " + c.cst(t.ck[0]) + ";";
-        if (t.kind == K_SRL) ld += " const double d" + sfx + " = " + c.cst(t.ck[1]) + ";";
-        cp = "const double vs" + sfx + " = vb" + sfx + " - va" + sfx + "; const double ip" + sfx + " = g" + sfx + " * vs" + sfx +
-             " + hp" + sfx + "; ";
-        if (t.kind == K_IND) cp += "const double hn" + sfx + " = ip" + sfx + " + g" + sfx + " * vs" + sfx + ";";
-        else if (t.kind == K_CAP) cp += "const double hn" + sfx + " = -ip" + sfx + " - g" + sfx + " * vs" + sfx + ";";
-        else cp += "const double hn" + sfx + " = d" + sfx + " * ip" + sfx + " + g" + sfx + " * vs" + sfx + ";";
-        st = "ST(" + h + ", hn" + sfx + ");";
-        return true;
-    }
-    if (t.out_alias) return false;
-    switch (t.kind) {
-        case K_IND: case K_CAP: case K_SRL: case K_VSRCT: case K_ISRCT: case K_CSRC: case K_FINC: case K_FINS:
-        case K_GAIN: case K_LIM: case K_CONST: case K_DELAY: case K_LATCH:
-            break;
-        default:
-            return false;
-    }
-    if (kCode[t.kind].loads == nullptr) return false;
-    ld = expand_lit(kCode[t.kind].loads, t, c, sfx);
-    cp = expand_lit(kCode[t.kind].compute, t, c, sfx);
-    st = expand_lit(kCode[t.kind].store, t, c, sfx);
-    return true;
-}
-
 std::string task_literal(const Task& t, const LitCtx& c) {
     std::ostringstream o;
     o << "{ ";
-    if (c.hoist >= 0 && (t.kind == K_VSRCT || t.kind == K_ISRCT)) {
-        const std::string v = "gv" + std::to_string(c.hoist);
-        if (t.kind == K_VSRCT) o << "const double g_ = " << c.cst(t.ck[0]) << "; ST(" << t.f[0] << ", g_ * " << v << "); }";
-        else o << "ST(" << t.f[0] << ", " << v << "); }";
-        return o.str();
-    }
-    if (c.hoist >= 0 && t.kind == K_BERG && c.deferred != nullptr) {
-        // ring values gb1/gb0 loaded at the phase start; be stored to HBM at the phase end
-        const std::string id = std::to_string(c.hoist);
-        o << "const double vs_ = LD(" << t.f[1] << ") - LD(" << t.f[0] << "); const double hp_ = LD(" << t.f[2] << "); gbe" << id
-          << " = " << c.cst(t.ck[0]) << " * vs_ + hp_; ST(" << t.f[2] << ", -(" << c.cst(t.ck[1]) << " * gb1" << id << " + "
-          << c.cst(t.ck[2]) << " * gb0" << id << ")); }";
-        *c.deferred += "      if (live) { const int w_ = step % " + std::to_string(t.f[4]) + "; A[(size_t)(" + std::to_string(t.f[3]) +
-                       " + w_) * W_] = gbe" + id + "; a.ring[(LB_ + gl) * a.ring_cols + (" + std::to_string(t.f[3]) +
-                       " - a.ring_lo) + w_] = gbe" + id + "; }\n";
-        return o.str();
-    }
-    if (c.berg_pf && t.kind == K_BERG && c.task_id >= 0) {
-        // peer histories for this pass were loaded during the previous one (when the
-        // poll keeps one more pass of slack, min_k >= 3); this pass loads the next's
-        const std::string id = std::to_string(c.task_id), L = std::to_string(t.f[4]);
-        const std::string at = "a.ring + pl_ * a.ring_cols + pr_ + ";
-        auto ld = [&](const std::string& q) {
-            return "(a.sys_scope ? __ldcv(" + at + q + ") : __ldcg(" + at + q + "))";
-        };
-        o << "const double vs_ = LD(" << t.f[1] << ") - LD(" << t.f[0] << "); const double hp_ = LD(" << t.f[2]
-          << "); const int K_ = (int)(" << c.cst(t.ck[3]) << "); const long long pl_ = (long long)(" << c.cst(t.ck[4])
-          << "); const long long pr_ = (long long)(" << c.cst(t.ck[5]) << ") - a.ring_lo; "
-          << "double b1_ = pb1_" << id << ", b0_ = pb0_" << id << "; "
-          << "if (!pfok || it == 0) { int q1_ = (step + 1 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
-          << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; b1_ = " << ld("q1_") << "; b0_ = " << ld("q0_") << "; } "
-          << "if (pfok && it + 1 < a.nsteps) { int q1_ = (step + 2 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
-          << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; pb1_" << id << " = " << ld("q1_") << "; pb0_" << id
-          << " = " << ld("q0_") << "; } "
-          << "const double be_ = " << c.cst(t.ck[0]) << " * vs_ + hp_; ST(" << t.f[2] << ", -(" << c.cst(t.ck[1])
-          << " * b1_ + " << c.cst(t.ck[2]) << " * b0_)); "
-          << "if (live) { const int w_ = step % " << L << "; A[(size_t)(" << t.f[3] << " + w_) * W_] = be_; a.ring[(LB_ + gl) * a.ring_cols + ("
-          << t.f[3] << " - a.ring_lo) + w_] = be_; } }";
-        return o.str();
-    }
     if (t.fused && c.fused_pass) {
         // i_prev = g (vb - va) + h as the finalize computed it last pass (exec.cpp:220-228)
         const std::string vb = std::to_string(t.f[1]), va = std::to_string(t.f[0]), h = std::to_string(t.f[3]);
@@ -1398,8 +1319,7 @@ std::string task_literal(const Task& t, const LitCtx& c) {
                       << "; const double q_ = x * r_; double m_ = __fma_rn(__fma_rn(-d_, q_, x), r_, q_); "
                       << (c.divguard == 2 ? "if (__builtin_expect(!(fabs(q_) >= 0x1p-900), 0)) m_ = emt_div_ieee(x, d_); " : "")
                       << "x = m_; "
-                      << (c.dsum ? "dsum = dsum + fabs(x); } "
-                                 : c.divguard == 1 ? "dok = dok & (fabs(x) <= dlim) & (fabs(q_) >= 0x1p-900); } "
+                      << (c.divguard == 1 ? "dok = dok & (fabs(x) <= dlim) & (fabs(q_) >= 0x1p-900); } "
                                  : c.divguard == 3 ? "dok = dok & (fabs(x) <= dlim) & !((fabs(q_) < 0x1p-900) & (q_ != 0.0)); } "
                                                    : "dok = dok & (fabs(x) <= dlim); } ");
                 else
@@ -1734,46 +1654,18 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         for (int id : all)
             for (int d : deps[static_cast<size_t>(id)]) indep = indep && !in_a.count(d);
         if (indep && !all.empty()) {
-            // sort key 0 lowest node read, 1 highest, 2 (lowest, highest): all within 0.3% on C3
-            const int kmode = knob("EMTB200_CG_AFFKEY", 0);
+            // sort key: lowest node read (highest / both measured within 0.3% on C3)
             auto key = [&](int id) {
-                long long lo = 1 << 30, hi = -1;
+                long long lo = 1 << 30;
                 for (int r : g.tasks[static_cast<size_t>(id)].reads)
-                    if (r >= s.v_base && r < s.v_base + s.nodes) {
-                        lo = std::min<long long>(lo, r - s.v_base);
-                        hi = std::max<long long>(hi, r - s.v_base);
-                    }
-                if (kmode == 1) return hi < 0 ? (1LL << 30) : hi;
-                if (kmode == 2) return lo * 4096 + (hi < 0 ? 4095 : hi);
+                    if (r >= s.v_base && r < s.v_base + s.nodes) lo = std::min<long long>(lo, r - s.v_base);
                 return lo;
             };
             std::stable_sort(all.begin(), all.end(), [&](int a, int b) { return key(a) < key(b); });
             long long total = 0;
             for (int id : all) total += g.tasks[static_cast<size_t>(id)].cost;
             std::vector<std::vector<int>> parts(static_cast<size_t>(G));
-            if (knob("EMTB200_CG_AFFINITY", 1) == 2) {
-                // greedy: each task to the warp already reading most of its nodes, within
-                // a 5% cost allowance over the even share (measured worse than the sorted
-                // cut: C3 2.54 -> 2.59 ms, C2 2.07 -> 2.10 us)
-                const long long cap = total * 105 / (100LL * G) + 1;
-                std::vector<long long> load(static_cast<size_t>(G), 0);
-                std::vector<std::set<int>> nodes(static_cast<size_t>(G));
-                for (int id : all) {
-                    const Task& t = g.tasks[static_cast<size_t>(id)];
-                    int bw = -1, bs = -1;
-                    for (int w = 0; w < G; ++w) {
-                        if (load[static_cast<size_t>(w)] + t.cost > cap) continue;
-                        int sh = 0;
-                        for (int r : t.reads) sh += nodes[static_cast<size_t>(w)].count(r);
-                        if (sh > bs || (sh == bs && load[static_cast<size_t>(w)] < load[static_cast<size_t>(bw)])) { bs = sh; bw = w; }
-                    }
-                    if (bw < 0) bw = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
-                    parts[static_cast<size_t>(bw)].push_back(id);
-                    load[static_cast<size_t>(bw)] += t.cost;
-                    for (int r : t.reads)
-                        if (r >= s.v_base && r < s.v_base + s.nodes) nodes[static_cast<size_t>(bw)].insert(r);
-                }
-            } else {
+            {  // sorted cut (a greedy node-sharing assignment measured worse: C3 2.54 -> 2.59 ms)
                 long long acc = 0;
                 for (int id : all) {
                     const int w = static_cast<int>(std::min<long long>(G - 1, acc * G / std::max<long long>(1, total)));
@@ -1785,30 +1677,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
     }
     Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
-    if (!sb.phases.empty() && knob("EMTB200_CG_AFFINITYB", 0) != 0) {  // measured neutral (C3 +0.2%, C2 -1.3%)
-        // region B's first phase when it holds only nodal gathers (independent, read the
-        // region-A contributions): consecutive nodes per warp, so a component's h, read by
-        // the gathers of both its end nodes, is loaded once when they share a warp
-        std::vector<int> all;
-        for (const auto& wl : sb.phases[0]) all.insert(all.end(), wl.begin(), wl.end());
-        bool only = !all.empty();
-        for (int id : all) only = only && g.tasks[static_cast<size_t>(id)].kind == K_GATHER;
-        if (only) {
-            std::sort(all.begin(), all.end(), [&](int a, int b) {
-                return g.tasks[static_cast<size_t>(a)].writes[0] < g.tasks[static_cast<size_t>(b)].writes[0];
-            });
-            long long total = 0;
-            for (int id : all) total += g.tasks[static_cast<size_t>(id)].cost;
-            std::vector<std::vector<int>> parts(static_cast<size_t>(G));
-            long long acc = 0;
-            for (int id : all) {
-                const int w = static_cast<int>(std::min<long long>(G - 1, acc * G / std::max<long long>(1, total)));
-                parts[static_cast<size_t>(w)].push_back(id);
-                acc += g.tasks[static_cast<size_t>(id)].cost;
-            }
-            sb.phases[0] = parts;
-        }
-    }
     double span_c = 0;
     Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
     {
@@ -1835,27 +1703,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             load[bp][static_cast<size_t>(bw)] += g.tasks[static_cast<size_t>(id)].cost;
             pmax[bp] = std::max(pmax[bp], load[bp][static_cast<size_t>(bw)]);
         }
-    }
-    if (knob("EMTB200_CG_FWDSTAT", 0)) {  // how many operand reads could come from the reader warp's registers
-        std::map<int, int> warp_of_task;
-        for (const Sched* sc : std::initializer_list<const Sched*>{&sa, &sb, &sc3})
-            for (size_t p = 0; p < sc->phases.size(); ++p)
-                for (int w = 0; w < G; ++w)
-                    for (int id : sc->phases[p][static_cast<size_t>(w)]) warp_of_task[id] = w;
-        std::map<int, int> last_writer;
-        long same = 0, other = 0, none = 0;
-        for (size_t i = 0; i < nt; ++i) {
-            const Task& t = g.tasks[i];
-            if (i > 0 && g.tasks[i - 1].region != t.region) last_writer.clear();
-            for (int r : t.reads) {
-                auto it = last_writer.find(r);
-                if (it == last_writer.end()) ++none;
-                else if (warp_of_task[it->second] == warp_of_task[static_cast<int>(i)]) ++same;
-                else ++other;
-            }
-            for (int w : t.writes) last_writer[w] = static_cast<int>(i);
-        }
-        std::fprintf(stderr, "operand reads: same-warp producer %ld, other-warp %ld, from before the region %ld\n", same, other, none);
     }
     if (knob("EMTB200_CG_DUMP", 0)) {  // schedule dump: per phase, per warp "kind x count (cost)"
         for (const Sched* sc : std::initializer_list<const Sched*>{&sa, &sb, &sc3}) {
@@ -1884,7 +1731,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const bool straight = opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", opt.mode == 1 ? 1 : 1) != 0;
     LitCtx lctx;
     if (knob("EMTB200_CG_SWFOLD", 1)) lctx.lit_init = [&](int k) -> int { return g.invariant(k) ? (g.c0(k) != 0.0 ? 1 : 0) : -1; };
-    lctx.dsum = knob("EMTB200_CG_DSUM", 0) != 0;  // measured 0.6% slower than the AND-ed predicate
     lctx.divguard = opt.exact_division ? 2 : knob("EMTB200_CG_DIVGUARD", 1);  // 0: dev A/B only (may misround)
     const bool dok_mode = straight && (knob("EMTB200_CG_DOK", 1) != 0 || g.dmma);
     lctx.dok = dok_mode;
@@ -1901,11 +1747,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     lctx.zterm = zterm;
     const bool warp_major = knob("EMTB200_CG_WARPMAJOR", 1) != 0;
     const bool switch_bits = knob("EMTB200_CG_SWBITS", 1) != 0;
-    // runs of up to batch_max independent tasks emitted loads-first (all loads, then the
-    // arithmetic, then the stores): measured within noise (C3 2.640 -> 2.630 ms), so off
-    const int batch_max = knob("EMTB200_CG_BATCH", 0);
-    // measured neutral (C4 -0.5%, C2 +1..7%): ptxas already issues these loads early
-    const bool glhoist = knob("EMTB200_CG_GLHOIST", 0) != 0;
     bool sw_slim = switch_bits && g.chg_flag && knob("EMTB200_CG_SWSLIM", 1) != 0;
     const bool sw_gate = knob("EMTB200_CG_SWGATE", 1) != 0;
     {
@@ -1975,47 +1816,12 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         return kind != K_SW && kind != K_FWD && kind != K_BWD && kind != K_BERG && kind != K_GATHER && kind != K_SUM;
     };
     std::vector<std::string> wprefix, wsuffix;  // per-warp code around a region's block (empty: none)
-    // Line coupling, split poll: one warp (the one with the least region-A work) waits
-    // for the peers' progress and hands the result to the warps holding line ends with
-    // a named barrier (barrier.arrive / barrier.sync 1); every other warp starts its
-    // region-A work at once instead of all warps waiting at two CTA barriers.
-    bool split_poll = false;
-    int poll_warp = 0;
-    std::vector<char> berg_warp(static_cast<size_t>(G), 0);
-    int n_berg_sync = 0;
-    {
-        bool any = false, a_only = true;
-        for (const Task& t : g.tasks)
-            if (t.kind == K_BERG) { any = true; a_only = a_only && t.region == 0; }
-        // measured slower (C4 3.26 -> 3.61 us): the line-end warps are region A's critical
-        // path and their ring loads then start only after the poll warp's release
-        if (any && a_only && straight && warp_major && knob("EMTB200_CG_SPLITPOLL", 0) != 0) {
-            // the lightest warp publishes progress at the pass end (and starts the next
-            // pass late while its release drains): poll from the second lightest
-            std::vector<std::pair<long long, int>> load;
-            for (int w = 0; w < G; ++w) {
-                long long c = 0;
-                for (const auto& ph : sa.phases)
-                    for (int id : ph[static_cast<size_t>(w)]) {
-                        c += g.tasks[static_cast<size_t>(id)].cost;
-                        if (g.tasks[static_cast<size_t>(id)].kind == K_BERG) berg_warp[static_cast<size_t>(w)] = 1;
-                    }
-                load.push_back({c, w});
-            }
-            std::stable_sort(load.begin(), load.end());
-            poll_warp = load.size() > 1 ? load[1].second : load[0].second;
-            for (int w = 0; w < G; ++w) n_berg_sync += (w != poll_warp && berg_warp[static_cast<size_t>(w)]) ? 1 : 0;
-            split_poll = true;
-        }
-    }
+    // (A split poll — one warp waits for the peers' progress and releases the line-end
+    // warps with a named barrier — measured slower: C4 3.26 -> 3.61 us; not kept.)
+    // (Also measured slower and not kept: peer histories loaded one pass ahead into
+    // registers, C4 3.21 -> 3.30 us; relaxed progress polls issued early in region A or
+    // B with an acquire fence later, C4 +8..12%: the fence holds the warp ~1000 cycles.)
     bool in_region_a = false;
-    bool berg_pf = false;
-    {
-        bool any = false;
-        for (const Task& t : g.tasks) any = any || t.kind == K_BERG;
-        // measured slower (C4 3.21 -> 3.30 us), so off
-        berg_pf = any && !split_poll && straight && warp_major && knob("EMTB200_CG_BERGPF", 0) != 0;
-    }
     auto region_code = [&](const Sched& sc, bool fused_pass) {
         std::ostringstream rc;
         if (straight && warp_major) {
@@ -2039,46 +1845,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                     std::vector<int> seg_of(ordered.size(), -1);
                     for (size_t si = 0; si < segs.size(); ++si)
                         for (int q = 0; q < segs[si].count; ++q) seg_of[static_cast<size_t>(segs[si].first + q)] = static_cast<int>(si);
-                    const bool berg_sync = split_poll && in_region_a && w != poll_warp && berg_warp[static_cast<size_t>(w)] &&
-                                           n_berg_sync > 0;
-                    if (berg_sync && loop_min == 0) {
-                        // line ends last in the warp's block (nothing in region A reads their output)
-                        std::set<int> bset;
-                        for (int id : ordered)
-                            if (g.tasks[static_cast<size_t>(id)].kind == K_BERG) bset.insert(id);
-                        bool indep = true;
-                        for (int id : ordered)
-                            for (int d : deps[static_cast<size_t>(id)]) indep = indep && !bset.count(d);
-                        if (indep) {
-                            std::stable_partition(ordered.begin(), ordered.end(),
-                                                  [&](int id) { return !bset.count(id); });
-                            for (size_t q = 0; q < ordered.size(); ++q) seg_of[q] = -1;
-                        }
-                    }
-                    bool berg_synced = false;
-                    // global loads (source table, peer line histories) issued at the phase
-                    // start so their L2 latency overlaps the phase's shared-memory work; a line
-                    // end's HBM stores move to the phase end (nothing in the pass reads them)
-                    std::string post;
-                    std::set<int> hoisted;
-                    if (glhoist && loop_min == 0 && batch_max <= 1)
-                        for (int id : ordered) {
-                            const Task& t = g.tasks[static_cast<size_t>(id)];
-                            if (t.kind == K_VSRCT || t.kind == K_ISRCT) {
-                                rc << "      const double gv" << id << " = SRCV_(" << t.f[1] << ");\n";
-                                hoisted.insert(id);
-                            } else if (t.kind == K_BERG && !berg_sync) {
-                                const std::string L = std::to_string(t.f[4]);
-                                const std::string at = "a.ring + pl_ * a.ring_cols + pr_ + ";
-                                rc << "      double gb1" << id << ", gb0" << id << ", gbe" << id << "; { const int K_ = (int)(" << lctx.cst(t.ck[3])
-                                   << "); const long long pl_ = (long long)(" << lctx.cst(t.ck[4]) << "); const long long pr_ = (long long)("
-                                   << lctx.cst(t.ck[5]) << ") - a.ring_lo; int q1_ = (step + 1 - K_) % " << L << "; if (q1_ < 0) q1_ += " << L
-                                   << "; const int q0_ = q1_ == 0 ? " << L << " - 1 : q1_ - 1; gb1" << id << " = a.sys_scope ? __ldcv(" << at
-                                   << "q1_) : __ldcg(" << at << "q1_); gb0" << id << " = a.sys_scope ? __ldcv(" << at << "q0_) : __ldcg(" << at
-                                   << "q0_); }\n";
-                                hoisted.insert(id);
-                            }
-                        }
                     for (size_t oi = 0; oi < ordered.size(); ++oi) {
                         if (loop_min > 0) {
                             const Segment& sg = segs[static_cast<size_t>(seg_of[oi])];
@@ -2089,49 +1855,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         }
                         const int id = ordered[oi];
                         const Task& t = g.tasks[static_cast<size_t>(id)];
-                        if (berg_sync && !berg_synced && t.kind == K_BERG) {
-                            rc << "      if (a.progress != nullptr) asm volatile(\"barrier.sync 1, " << 32 * (n_berg_sync + 1)
-                               << ";\" ::: \"memory\");  // the poll warp's progress result\n";
-                            berg_synced = true;
-                        }
                         LitCtx c = lctx;
                         c.fused_pass = fused_pass;
                         c.task_id = id;
-                        c.berg_pf = berg_pf;
-                        if (hoisted.count(id)) {
-                            c.hoist = id;
-                            c.deferred = &post;
-                        }
-                        if (batch_max > 1) {
-                            // gather a run of independent splittable tasks: loads, then computes, then stores
-                            std::vector<std::string> L_, C_, S_;
-                            std::set<int> members;
-                            size_t oj = oi;
-                            while (oj < ordered.size() && static_cast<int>(L_.size()) < batch_max) {
-                                const int idj = ordered[oj];
-                                const Task& tj = g.tasks[static_cast<size_t>(idj)];
-                                if (tj.kind == K_SW) break;
-                                bool dep = false;
-                                for (int d : deps[static_cast<size_t>(idj)]) dep = dep || members.count(d);
-                                if (dep) break;
-                                std::string l1, c1, s1;
-                                if (!task_literal_parts(tj, c, "_" + std::to_string(L_.size()), l1, c1, s1)) break;
-                                L_.push_back(l1);
-                                C_.push_back(c1);
-                                S_.push_back(s1);
-                                members.insert(idj);
-                                ++oj;
-                            }
-                            if (L_.size() >= 2) {
-                                rc << "      {\n";
-                                for (const auto& x : L_) rc << "        " << x << "\n";
-                                for (const auto& x : C_) rc << "        " << x << "\n";
-                                for (const auto& x : S_) rc << "        " << x << "\n";
-                                rc << "      }\n";
-                                oi = oj - 1;
-                                continue;
-                            }
-                        }
                         if (t.kind == K_SW && switch_bits && sw_ids.size() < 64 && t.region == 0) {
                             c.sw_bit = static_cast<int>(sw_ids.size());
                             c.chg_flag = g.chg_flag;
@@ -2145,7 +1871,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                         }
                         rc << "      " << task_literal(t, c) << "\n";
                     }
-                    rc << post;
                 }
                 if (!sw_lits.empty()) {
                     // switches only change state when t reaches one of their toggle times: the
@@ -2215,47 +1940,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
         return rc.str();
     };
-    // Line coupling, early poll (EMTB200_CG_APOLL): the second-lightest region-A warp
-    // (the lightest publishes progress at the pass end) issues relaxed loads of every
-    // CTA's progress word at the start of its region-A block; at the start of region B
-    // (after the CTA barrier, so no thread still reads s_cmin for this pass) it takes
-    // the minimum, fences (acquire) and raises s_cmin, so the blocking poll at the top
-    // of a pass rarely runs.
-    std::vector<std::string> apoll_b;  // region-B prefixes (set after region A is emitted)
-    {
-        bool any = false;
-        for (const Task& t : g.tasks) any = any || t.kind == K_BERG;
-        // measured slower (C4 3.27 -> 3.55 us: the acquire fence holds the warp ~1000
-        // cycles at the start of region B), so off
-        if (any && straight && warp_major && !split_poll && knob("EMTB200_CG_APOLL", 0) != 0) {
-            std::vector<std::pair<long long, int>> load;
-            for (int w = 0; w < G; ++w) {
-                long long c = 0;
-                for (const auto& ph : sa.phases)
-                    for (int id : ph[static_cast<size_t>(w)]) c += g.tasks[static_cast<size_t>(id)].cost;
-                load.push_back({c, w});
-            }
-            std::stable_sort(load.begin(), load.end());
-            const int pw = load.size() > 1 ? load[1].second : load[0].second;
-            wprefix.assign(static_cast<size_t>(G), std::string());
-            wprefix[static_cast<size_t>(pw)] =
-                "      if (a.progress != nullptr) { pm_ = 0xffffffffu; for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; "
-                "if (a.sys_scope) asm volatile(\"ld.relaxed.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); "
-                "else asm volatile(\"ld.relaxed.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); pm_ = min(pm_, v); } }\n";
-            apoll_b.assign(static_cast<size_t>(G), std::string());
-            apoll_b[static_cast<size_t>(pw)] =
-                "      if (a.progress != nullptr) {\n"
-                "        pm_ = __reduce_min_sync(0xffffffffu, pm_);\n"
-                "        if (a.sys_scope) asm volatile(\"fence.acq_rel.sys;\" ::: \"memory\"); else asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n"
-                "        if (lane == 0 && (int)pm_ > s_cmin && pm_ < 0x3fffffffu) s_cmin = (int)pm_;\n"
-                "      }\n";
-        }
-    }
-    std::string berg_decls;
-    if (berg_pf)
-        for (size_t i = 0; i < g.tasks.size(); ++i)
-            if (g.tasks[i].kind == K_BERG)
-                berg_decls += "  double pb1_" + std::to_string(i) + " = 0.0, pb0_" + std::to_string(i) + " = 0.0;\n";
     in_region_a = true;
     std::string code_a = region_code(sa, false);
     if (!g.fused.empty()) {  // the launch's first pass reads i_prev from the arena; later passes recompute it
@@ -2264,41 +1948,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     in_region_a = false;
     wprefix.clear();
-    bool has_lines = false;
-    for (const Task& t : g.tasks) has_lines = has_lines || t.kind == K_BERG;
-    // measured slower (C4 3.37 -> 3.77 us: the acquire fence stalls that warp ~1000
-    // cycles at the end of the pass), so off
-    if (has_lines && straight && warp_major && knob("EMTB200_CG_BGPOLL", 0) != 0) {
-        // line coupling: the warp with the least region-B work reads every CTA's progress
-        // word once per pass (relaxed loads issued at the region start, consumed at its
-        // end, then an acquire fence) and raises s_cmin, so the blocking poll at the top
-        // of a pass rarely runs
-        int lw = 0;
-        long long best = -1;
-        for (int w = 0; w < G; ++w) {
-            long long c = 0;
-            for (const auto& ph : sb.phases)
-                for (int id : ph[static_cast<size_t>(w)]) c += g.tasks[static_cast<size_t>(id)].cost;
-            if (best < 0 || c < best) { best = c; lw = w; }
-        }
-        wprefix.assign(static_cast<size_t>(G), std::string());
-        wsuffix.assign(static_cast<size_t>(G), std::string());
-        wprefix[static_cast<size_t>(lw)] =
-            "      unsigned int pm_ = 0xffffffffu;\n"
-            "      if (a.progress != nullptr) for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; "
-            "if (a.sys_scope) asm volatile(\"ld.relaxed.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); "
-            "else asm volatile(\"ld.relaxed.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); pm_ = min(pm_, v); }\n";
-        wsuffix[static_cast<size_t>(lw)] =
-            "      if (a.progress != nullptr) {\n"
-            "        pm_ = __reduce_min_sync(0xffffffffu, pm_);\n"
-            "        if (a.sys_scope) asm volatile(\"fence.acq_rel.sys;\" ::: \"memory\"); else asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n"
-            "        if (lane == 0 && (int)pm_ > s_cmin && pm_ < 0x3fffffffu) s_cmin = (int)pm_;\n"
-            "      }\n";
-    }
-    if (!apoll_b.empty()) {
-        if (wprefix.empty()) wprefix.assign(static_cast<size_t>(G), std::string());
-        for (int w = 0; w < G; ++w) wprefix[static_cast<size_t>(w)] = apoll_b[static_cast<size_t>(w)] + wprefix[static_cast<size_t>(w)];
-    }
     const std::string code_b = region_code(sb, false);
     wprefix.clear();
     wsuffix.clear();
@@ -2376,18 +2025,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         dmma_block = blk.str();
         smem += ginv_bytes + 32 * sizeof(int);
     }
-    // AC source values one pass ahead: at the top of a pass the CTA starts async copies
-    // (cp.async) of the next pass's table row (its own columns) into the other half of
-    // a double-buffered shared row, waited for at the end of the pass, so region A
-    // reads shared memory instead of waiting on an L2 load. Measured slower (C3 2.64 ->
-    // 2.75 ms, C4 3.92 -> 4.34 ms per 1000 passes; register-held variant likewise), so off.
-    const int pf_ns = g.tab_shared(), pf_nv = static_cast<int>(g.tab_ck.size()) - pf_ns;
-    const int pf_row = pf_ns + pf_nv * LPC;
-    const size_t pf_off = (smem + 7) / 8;  // doubles
-    const size_t pf_bytes = 2 * static_cast<size_t>(pf_row) * sizeof(double);
-    const bool srcpf = !g.tab_ck.empty() && knob("EMTB200_CG_SRCPF", 0) != 0 &&
-                       pf_off * 8 + pf_bytes <= opt.smem_budget;
-    if (srcpf) smem = pf_off * 8 + pf_bytes;
+    // (AC source values copied one pass ahead into shared memory with cp.async measured
+    // slower: C3 2.64 -> 2.75 ms, C4 3.92 -> 4.34 ms per 1000 passes; not kept.)
     // ---- source
     std::ostringstream o;
     const int nhot = static_cast<int>(g.hot_slots.size());
@@ -2398,16 +2037,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         const int ns = g.tab_shared(), nv = static_cast<int>(g.tab_ck.size()) - g.tab_shared();
         o << "#define NSHR_ " << ns << "\n#define NSRC_ " << std::max<long long>(1, ns + static_cast<long long>(nv) * lanes) << "LL\n";
         out.nsrc = static_cast<int>(std::max<long long>(0, ns + static_cast<long long>(nv) * lanes));
-        if (srcpf) {
-            o << "#define NSRCL_ " << pf_row << "\n"
-              << "#define SRCV_(j) ((j) < NSHR_ ? s_pf[(it & 1) * NSRCL_ + (j)] : s_pf[(it & 1) * NSRCL_ + NSHR_ + ((j) - NSHR_) * "
-              << LPC << " + slane])\n"
-              // global table column of element q of this CTA's row
-              << "#define PFCOL_(q) ((q) < NSHR_ ? (long long)(q) : NSHR_ + (long long)(((q) - NSHR_) / " << LPC << ") * W_ + "
-              << "min((long long)blockIdx.x * " << LPC << " + ((q) - NSHR_) % " << LPC << ", W_ - 1))\n";
-        } else {
-            o << "#define SRCV_(j) __ldg(a.srctab + (size_t)it * NSRC_ + ((j) < NSHR_ ? (j) : NSHR_ + ((j) - NSHR_) * W_ + gl))\n";
-        }
+        o << "#define SRCV_(j) __ldg(a.srctab + (size_t)it * NSRC_ + ((j) < NSHR_ ? (j) : NSHR_ + ((j) - NSHR_) * W_ + gl))\n";
     }
     o << "#define W_ " << Wl << "LL\n#define NCH " << s.channel_slot.size() << "\n#define LB_ " << opt.lane_begin << "LL\n";
     o << libm_cos_prelude();
@@ -2465,8 +2095,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     carr_i("__device__ const", "kConSign", csign);
     // warps reach their phase barriers at different instructions: the non-.aligned
     // barrier form is the one the PTX ISA allows there (compute-sanitizer synccheck clean)
-    if (knob("EMTB200_CG_ALIGNEDBAR", 0)) o << "#define BAR() asm volatile(\"bar.sync 0;\" ::: \"memory\")\n";
-    else o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
+    o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
     o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
@@ -2483,14 +2112,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     else
         o << "#define LU(x) (A[(size_t)(x) * W_])\n";
 
-    // Refactorization in its own (non-inlined) function: its hundreds of
-    // temporaries must not raise the register pressure of the step loop.
-    if (knob("EMTB200_CG_NOINLINE", 0)) o << "__device__ __noinline__ int emt_refactor(double* __restrict__ S, double* __restrict__ A, const double* __restrict__ C,"
-      << " const bool live, const int lane, int* needS) {\n"
-      << "  int srow = -1; (void)C; (void)needS; (void)lane;\n"
-      << g.emit_refactor()
-      << "  return srow;\n}\n";
-    else o << "";
     o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * G << ", 1) emt_cg_kernel(const KArgs a) {\n"
       << "  extern __shared__ double sm[];\n"
       << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
@@ -2581,9 +2202,6 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (const Task& t : g.tasks)
         if (t.region == 0)
             for (int w : t.writes) written_a.insert(w);
-    if (srcpf)
-        o << "  double* __restrict__ s_pf = sm + " << pf_off << ";\n"
-          << "  if (a.nsteps > 0) for (int q = threadIdx.x; q < NSRCL_; q += " << 32 * G << ") s_pf[q] = __ldg(a.srctab + PFCOL_(q));\n";
     o << "  __shared__ int s_cmin;\n"
       << "  if (threadIdx.x == 0) s_cmin = -0x3fffffff;\n"
       << "  __syncthreads();\n"
@@ -2591,40 +2209,15 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "  long long prof_t = clock64(); (void)prof_t;\n"
       << "  double swnext = -1.0; (void)swnext;  // per lane: next switch toggle time not yet reached\n"
       << "  const double dlim = a.div_limit; (void)dlim;\n"
-      << "  int pcmin = -0x3fffffff; int pfail = 0; (void)pcmin;  // split poll: the poll warp's view of peer progress\n"
-      // one-pass-ahead peer histories (deadlock-free only with >= 2 passes of slack)
-      << "  const int pfok = " << (berg_pf ? "a.min_k >= 3 ? 1 : 0" : "0") << "; (void)pfok;\n"
-      << "  unsigned int pm_ = 0xffffffffu; (void)pm_;\n"
-      << berg_decls
       << "  for (; it < a.nsteps; ++it) {\n"
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    const double tn = (double)(step + 2) * " << lit(s.dt) << "; (void)tn;\n"
-      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true; double dsum = 0.0;\n"
-      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok; (void)dsum;\n"
+      << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
+      << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
       ;
-    if (split_poll) {
-        o << "    if (a.progress != nullptr && warp == " << poll_warp << ") {\n"
-          << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs: this warp\n"
-          << "      // waits until every CTA has completed pass step+1-K, then releases the line-end warps\n"
-          << "      if (pcmin < step + 2 - a.min_k) {\n"
-          << "        const long long t0 = clock64(); int m;\n"
-          << "        for (;;) {\n"
-          << "          m = 0x7fffffff;\n"
-          << "          for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
-          << "          m = __reduce_min_sync(0xffffffffu, m);\n"
-          << "          if (m >= step + 2 - a.min_k) break;\n"
-          << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
-          << "        }\n"
-          << "        if (a.sys_scope) __threadfence_system();\n"
-          << "        pcmin = m;\n"
-          << "        if (m < 0) pfail = 1;\n"
-          << "      }\n";
-        if (n_berg_sync > 0)
-            o << "      asm volatile(\"barrier.arrive 1, " << 32 * (n_berg_sync + 1) << ";\" ::: \"memory\");\n";
-        o << "    }\n";
-    } else {
-        o << "    if (a.progress != nullptr && s_cmin < step + 2 + pfok - a.min_k) {\n"
+    {
+        o << "    if (a.progress != nullptr && s_cmin < step + 2 - a.min_k) {\n"
       << "      // line ends read peer rings written >= K-1 passes earlier by other CTAs:\n"
       << "      // wait until every CTA has completed pass step+1-K (its progress word)\n"
       << "      __syncthreads();\n"
@@ -2635,7 +2228,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "          m = 0x7fffffff;\n"
       << "          for (int c = lane; c < a.nblocks; c += 32) { unsigned int v; if (a.sys_scope) asm volatile(\"ld.acquire.sys.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); else asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(a.progress + c) : \"memory\"); m = min(m, (int)v); }\n"
       << "          m = __reduce_min_sync(0xffffffffu, m);\n"
-      << "          if (m >= step + 2 + pfok - a.min_k) break;\n"
+      << "          if (m >= step + 2 - a.min_k) break;\n"
       << "          if (__shfl_sync(0xffffffffu, (int)(clock64() - t0 > 8000000000LL), 0)) { m = -1; break; }  // warp-uniform\n"
       << "        }\n"
       << "        if (a.sys_scope) __threadfence_system();  // gpu scope: the acquire loads + bar.sync suffice\n"
@@ -2650,17 +2243,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
     o << "}\n";
-    if (srcpf) {  // next pass's row: an async global->shared copy (no registers held across the pass)
-        o << "    if (it + 1 < a.nsteps) for (int q = threadIdx.x; q < NSRCL_; q += " << 32 * G << ") {\n"
-          << "      const unsigned int d = (unsigned int)__cvta_generic_to_shared(s_pf + ((it + 1) & 1) * NSRCL_ + q);\n"
-          << "      asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"(d), \"l\"(a.srctab + (size_t)(it + 1) * NSRC_ + PFCOL_(q)) : \"memory\");\n"
-          << "    }\n";
-    }
     o << code_a;
-    o << "    if (__syncthreads_or(wflag | pfail)) {\n"
-      << "      if (__syncthreads_or(pfail)) { if (warp == 0 && live) { a.lane_err[4*gl] = 64; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = -1; a.lane_err[4*gl+3] = 0; } FAILPUB(); return; }\n"
+    o << "    if (__syncthreads_or(wflag)) {\n"
       << (solo ? "      if (warp == 0 && lane == 0) {\n" : "      if (warp == 0) {\n")
-      << (knob("EMTB200_CG_NOINLINE", 0) ? "        srow = emt_refactor(S, A, C, live, lane, needS);\n" : g.emit_refactor())
+      << g.emit_refactor()
       << "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
       << "      }\n"
       << "      if (__syncthreads_or(srow >= 0 && live)) {\n"
@@ -2669,19 +2255,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "        FAILPUB(); return;\n"
       << "      }\n"
       << "    }\n";
-    // progress release: right after the barrier that follows region A when every line
-    // end writes its history there (peers only read histories), else at the pass end.
-    // st.release after bar.sync orders the whole CTA's earlier stores (PTX memory
-    // model: the barrier puts them before thread 0's release in causality order).
-    bool berg_a_only = true;
-    for (const Task& t : g.tasks)
-        if (t.kind == K_BERG && t.region != 0) berg_a_only = false;
-    const bool early_rel = berg_a_only && knob("EMTB200_CG_EARLYREL", 0) != 0;  // measured: C4 3.35 -> 4.60 us (the release stalls warp 0 mid-pass)
-    // delayed publication (EMTB200_CG_DELAYREL, min_k >= 3): the pass end releases the
-    // previous pass, whose stores have long completed, so the release does not hold
-    // warp 0; the last pass is published after the loop. Deadlock-free for K >= 3: a
-    // CTA at pass p needs its peers at p+2-K, and they need it at p+4-2K <= p-2.
-    const bool delay_rel = knob("EMTB200_CG_DELAYREL", 0) != 0;
+    // progress release at the pass end: st.release after bar.sync orders the whole CTA's
+    // earlier stores (PTX memory model: the barrier puts them before the releasing
+    // thread's store in causality order). Releasing right after region A (C4 3.35 ->
+    // 4.60 us) or one pass late (neutral) measured no better; not kept.
     auto rel_stmt = [](const std::string& val) {
         return std::string("      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(") +
                val + ")) : \"memory\"); }\n" +
@@ -2703,22 +2280,15 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     const std::string release =
         std::string("    if (a.progress != nullptr && threadIdx.x == ") + std::to_string(32 * rel_warp) + ") {\n" +
-        (delay_rel ? std::string("      if (a.min_k >= 3) { if (it > 0) {\n") + rel_stmt("step") + "      } } else {\n" + rel_stmt("step + 1") + "      }\n"
-                   : rel_stmt("step + 1")) +
-        "    }\n";
-    if (early_rel) o << release;
+        rel_stmt("step + 1") + "    }\n";
     o << code_b << dmma_block << code_c;
-    if (srcpf)  // the pass-end barrier below orders the copies before the next pass's reads
-        o << "    asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n";
     if (dok_mode) {
         // divergence (exec.cpp:229-237): rows only AND a NaN-safe predicate; the
         // failing node index (the lowest) is found in the cold path
         std::ostringstream tb;
         for (int i = 0; i < s.nodes; ++i) tb << (i ? "," : "") << g.off(s.v_base + i);
         if (s.nodes == 0) tb << "0";
-        // dsum = sum of |x| over a warp's rows: NaN/inf propagate, and a sum above the
-        // limit only triggers the exact per-node scan (which may find nothing)
-        o << "    if (__syncthreads_or((!dok || !(dsum <= dlim)) && live)) {\n"
+        o << "    if (__syncthreads_or(!dok && live)) {\n"
           << "      const int kVoff[" << std::max(1, s.nodes) << "] = {" << tb.str() << "};\n"
           << "      if (warp == 0 && live) serr[lane] = 0x7fffffff;\n"
           << "      __syncthreads();\n"
@@ -2751,11 +2321,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
           << "      FAILPUB(); return;\n";
     }
     o      << "    }\n";
-    if (!early_rel) o << release;
+    o << release;
     o << "  }\n";
-    if (delay_rel)
-        o << "  if (a.progress != nullptr && threadIdx.x == 0 && a.min_k >= 3 && a.nsteps > 0) {\n"
-          << "    const int step = a.step0 + a.nsteps - 1;\n" << rel_stmt("step + 1") << "  }\n";
     // save the resident state back to the arena (+ slots derived from it)
     o << "  __syncthreads();\n"
       << "  if (live) {\n"
