@@ -920,6 +920,8 @@ emt_status build_system_plan(emt_engine* e) {
     e->allocations.push_back(S.fval);
     CUDA_TRY(cudaMalloc(&S.tval, tsrc.size() * sizeof(double) * static_cast<size_t>(e->W)));
     e->allocations.push_back(S.tval);
+    CUDA_TRY(cudaMalloc(&S.frcp, static_cast<size_t>(std::max(1, dim)) * sizeof(double) * static_cast<size_t>(e->W)));
+    e->allocations.push_back(S.frcp);
     S.work = nullptr;
     if (e->W > 1) {
         CUDA_TRY(cudaMalloc(&S.work, static_cast<size_t>(P.lane_stride) * sizeof(double) * static_cast<size_t>(e->W)));

@@ -8,9 +8,9 @@
 //
 //  * layers (exec.cpp:364-374): the layer's processes in parallel over 1024
 //    threads (write sets are disjoint per layer), __syncthreads between layers;
-//  * FactorizeSystem (exec.cpp:175-204): warp-cooperative up-looking rows
-//    (warp_factorize, the reference's lu_factor order), then the block rebuilds
-//    the backward stream below;
+//  * FactorizeSystem (exec.cpp:175-204): the reference's up-looking rows, each
+//    elimination's scratch-row update spread over the block (sys_factorize), then
+//    the block rebuilds the factor streams below;
 //  * SolveSystem (exec.cpp:205-239): the gather in parallel per node into a
 //    shared-memory copy of v; the forward sweep in column blocks of 32 — warp 0
 //    resolves the block's own lower-triangular tile with register shuffles, then
@@ -59,6 +59,7 @@ struct SysPlan {
     const int* brow;         // dim, rows descending: 2 * off-diagonal entries + (first column == row + 1)
     double* bval;            // W x stream_len: the lane's stream values (rebuilt at launch start and after each factorisation)
     double* work;            // lane-major working arena when W > 1 (W == 1 runs on the arena itself)
+    double* frcp;            // W x dim: pivot reciprocals 1/U(c,c) of the lane's current factors
     int smem_xs;             // byte offsets in dynamic shared memory
     int smem_tile;
     int smem_ring_v;
@@ -148,6 +149,82 @@ __device__ __forceinline__ void sys_build_stream(const DevPlan& P, const SysPlan
         const int s = __ldg(&S.tsrc[q]);
         tv[q] = s >= 0 ? Lv[s] : 0.0;
     }
+}
+
+// FactorizeSystem for one lane on the whole block (exec.cpp:175-204 + lu_factor,
+// sparse.cpp:79-145): the reference's up-looking rows, one row at a time; within a
+// row the eliminations run in ascending column order, each one's update of the
+// scratch row spread over the block (the scratch row lives in shared memory). The
+// quotient S[c] / U(c,c) is the guarded Markstein division (the IEEE quotient bit
+// for bit) with the reciprocal kept per row. Returns the block-uniform error flag.
+__device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restrict__ A, unsigned char* sm, int lane,
+                             int step, int row, int layer) {
+    const int tid = threadIdx.x, tl = tid & 31, wid = tid >> 5;
+    double* Sx = reinterpret_cast<double*>(sm + S.smem_xs);
+    __shared__ double s_max[32];
+    double* G = A + P.mat;
+    double m = 0.0;  // max |A| of the lane, sparse.cpp:84-90 (std::max keeps m on NaN)
+    for (int k = tid; k < P.nnz; k += kSysThreads) {
+        double d = 0.0;
+        for (int q = __ldg(&P.ment_ptr[k]); q < __ldg(&P.ment_ptr[k + 1]); ++q)
+            d += __ldg(&P.ment_sign[q]) * A[__ldg(&P.ment_slot[q])];
+        G[k] = d;
+        const double x = fabs(d);
+        m = m < x ? x : m;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(kFull, m, off);
+        m = m < o ? o : m;
+    }
+    if (tl == 0) s_max[wid] = m;
+    __syncthreads();
+    m = 0.0;
+    for (int w = 0; w < kSysThreads / 32; ++w) m = m < s_max[w] ? s_max[w] : m;
+    double* Lv = A + P.l;
+    double* Uv = A + P.u;
+    double* R = S.frcp + static_cast<size_t>(lane) * static_cast<size_t>(P.dim > 0 ? P.dim : 1);
+    for (int i = 0; i < P.dim; ++i) {
+        const int lb = __ldg(&P.l_row_ptr[i]), le = __ldg(&P.l_row_ptr[i + 1]);
+        const int ub = __ldg(&P.u_row_ptr[i]), ue = __ldg(&P.u_row_ptr[i + 1]);
+        // scatter row i of A over the union pattern, fill positions zero (sparse.cpp:94-110)
+        for (int q = lb + tid; q < le; q += kSysThreads) Sx[__ldg(&P.l_col[q])] = 0.0;
+        for (int q = ub + tid; q < ue; q += kSysThreads) Sx[__ldg(&P.u_col[q])] = 0.0;
+        __syncthreads();
+        for (int q = __ldg(&P.row_ptr[i]) + tid; q < __ldg(&P.row_ptr[i + 1]); q += kSysThreads)
+            Sx[__ldg(&P.col_idx[q])] = G[q];
+        __syncthreads();
+        // eliminate with the settled rows, ascending columns (sparse.cpp:112-124)
+        for (int k = lb; k < le; ++k) {
+            const int c = __ldg(&P.l_col[k]);
+            const int cb = __ldg(&P.u_row_ptr[c]), ce = __ldg(&P.u_row_ptr[c + 1]);
+            const double x = Sx[c], d = Uv[cb], r = R[c];
+            const double q0 = x * r;
+            const double lik = (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900) ? __fma_rn(__fma_rn(-d, q0, x), r, q0) : x / d;
+            if (tid == 0) Lv[k] = lik;
+            for (int j = cb + 1 + tid; j < ce; j += kSysThreads) {
+                const int cj = __ldg(&P.u_col[j]);
+                Sx[cj] = Sx[cj] - lik * Uv[j];
+            }
+            __syncthreads();
+        }
+        for (int q = ub + tid; q < ue; q += kSysThreads) Uv[q] = Sx[__ldg(&P.u_col[q])];
+        const double piv = Sx[i];  // U(i, i), first in its row (sparse.cpp:126-131)
+        if (tid == 0) R[i] = sys_rcp(piv);
+        if (!(fabs(piv) > 1e-12 * m)) {  // sparse.cpp:133-143
+            if (tid == 0) lane_fail(P, lane, 8 /*SingularMatrix*/, step, i, layer, 0);
+            return 1;
+        }
+        __syncthreads();
+    }
+    // the scratch row's final contents (every column is some row's diagonal, so all are written)
+    double* scr = A + P.scratch;
+    for (int c = tid; c < P.dim; c += kSysThreads) scr[c] = Sx[c];
+    for (int q = tid; q < P.nwatch; q += kSysThreads) A[__ldg(&P.watch[q])] = 0.0;
+    if (tid == 0) {
+        A[P.fcount] += 1.0;
+        P.refactored[row] = 1;
+    }
+    return 0;
 }
 
 // SolveSystem for one lane on the whole block (exec.cpp:205-239 + lu_solve, sparse.cpp:147-172).
@@ -429,7 +506,6 @@ emt_system_kernel(const DevPlan P, const SysPlan S, const int step0, const int n
     const int tid = threadIdx.x, wid = tid >> 5, tl = tid & 31;
     const int lane = blockIdx.x;
     if (P.lane_err[lane].code != 0) return;  // lane already failed: frozen
-    __shared__ int s_flag;
     double* A;
     const double* C;
     if (P.W == 1) {  // the arena and constant table are the lane's own (slot-major with one lane)
@@ -475,13 +551,9 @@ emt_system_kernel(const DevPlan P, const SysPlan S, const int step0, const int n
                     bool set = false;
                     for (int q = tid; q < P.nwatch; q += kSysThreads) set |= (A[__ldg(&P.watch[q])] != 0.0);
                     if (__syncthreads_or(set)) {
-                        if (wid == 0) {
-                            const int r = warp_factorize(P, A, tl, lane, step, row, layer);
-                            if (tl == 0) s_flag = r;
-                        }
+                        err = sys_factorize(P, S, A, sys_smem, lane, step, row, layer);
                         __syncthreads();
                         sys_mark(S, tp, 1);  // factorisation
-                        err = s_flag;
                         if (!err) {
                             sys_build_stream(P, S, A, bv, fv, tv);
                             asm volatile("fence.proxy.async.global;\n" ::: "memory");
