@@ -79,6 +79,14 @@ enum { EMT_FLAG_TENSOR_SOLVE = 1 };
  * x / u below the bound instead (exact everywhere, ~20% slower). */
 enum { EMT_FLAG_EXACT_DIVISION = 2 };
 
+/* Cold start: engine creation returns at once and the engine runs the generic
+ * kernel (bit-identical) while the specialised kernel is generated and
+ * NVRTC-compiled on a host thread; the first launch after the compile finishes
+ * switches to it. AUTO kernel selection only; ignored for line-coupled batches,
+ * the tensor-core solve and lanes too large for the generic kernel's shared
+ * memory. emt_engine_wait_jit() blocks until the switch. */
+enum { EMT_FLAG_ASYNC_JIT = 4 };
+
 /* Step-loop kernel selection. AUTO generates and JIT-compiles (NVRTC) a kernel
  * specialised to the schedule — the code generator of the reference's
  * emit_source (proj/src/codegen.cpp:84-230) retargeted to sm_100a — and uses
@@ -258,6 +266,10 @@ emt_status emt_engine_read_refactor_steps(emt_engine* engine, int32_t* steps, in
  * and the CUDA stream the engine launches on (cudaStream_t as void*). */
 void* emt_engine_device_waves(emt_engine* engine);
 void* emt_engine_stream(emt_engine* engine);
+
+/* Blocks until an asynchronous JIT (EMT_FLAG_ASYNC_JIT) has finished and adopts its
+ * kernel for the following launches; a no-op otherwise. */
+emt_status emt_engine_wait_jit(emt_engine* engine);
 
 /* Which kernel the engine runs (EMT_KERNEL_SPECIALISED or _GENERIC), the
  * generated CUDA source (empty for the generic kernel) and a one-line plan

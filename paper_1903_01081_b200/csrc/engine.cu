@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <memory>
 #include <string>
 #include <vector>
@@ -484,6 +485,18 @@ emt_status set_error(int code, const std::string& msg) {
 
 using namespace emtb200;
 
+// A specialised kernel being generated and compiled on a host thread while the
+// engine already runs the (bit-identical) generic kernel (EMT_FLAG_ASYNC_JIT).
+struct PendingJit {
+    std::future<void> done;
+    GeneratedKernel gen;
+    JitModule jit;
+    Failure fail;
+    std::string log;
+    double gen_s = 0.0;
+    bool ok = false;
+};
+
 struct emt_engine {
     Schedule sched;
     int device = 0;
@@ -541,8 +554,13 @@ struct emt_engine {
     std::vector<double> initial_fcount;  // per owned lane, from the initial arena
     int base_factor_count = 0;           // global lane 0's initial fcount (ExecStats, exec.cpp:376)
 
+    std::unique_ptr<PendingJit> pending;  // async JIT in flight (EMT_FLAG_ASYNC_JIT)
+    int switched_at = -1;                 // pass at which the engine moved to the specialised kernel
+
     ~emt_engine() {
+        if (pending && pending->done.valid()) pending->done.wait();  // the thread reads sched
         if (device >= 0) cudaSetDevice(device);
+        if (pending && pending->ok && pending->jit.module && driver()) driver()->ModuleUnload(pending->jit.module);
         if (jit.module && driver()) driver()->ModuleUnload(jit.module);
         for (void* p : allocations) cudaFree(p);
         if (d_ring && ring_owned) cudaFree(d_ring);
@@ -967,6 +985,31 @@ emt_status build_system_plan(emt_engine* e) {
     return EMT_OK;
 }
 
+/// Adopts the asynchronously compiled specialised kernel once it is ready (or, with
+/// `block`, waits for it). Launches stay stream-ordered, so switching between two
+/// launches needs no synchronisation; both kernels produce the same bits.
+void adopt_pending(emt_engine* e, bool block) {
+    if (!e->pending) return;
+    PendingJit& p = *e->pending;
+    if (!block && p.done.wait_for(std::chrono::seconds(0)) != std::future_status::ready) return;
+    p.done.get();
+    if (p.ok) {
+        e->gen = std::move(p.gen);
+        e->jit = p.jit;
+        p.jit = JitModule{};
+        p.ok = false;
+        e->kernel_mode = EMT_KERNEL_SPECIALISED;
+        e->switched_at = e->step;
+        char b[200];
+        std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s (async JIT: generic kernel for passes 0..%d)", p.gen_s,
+                      e->jit.compile_seconds, e->jit.cached ? " (cached)" : "", e->step - 1);
+        e->summary = "specialised kernel: " + e->gen.summary + b;
+    } else {
+        e->summary += " (specialised kernel unavailable: " + (p.fail.message.empty() ? p.log.substr(0, 300) : p.fail.message) + ")";
+    }
+    e->pending.reset();
+}
+
 emt_status check_lane_errors(emt_engine* e) {
     std::vector<LaneError> errs(static_cast<size_t>(e->W));
     CUDA_TRY(cudaMemcpy(errs.data(), e->plan.lane_err, errs.size() * sizeof(LaneError), cudaMemcpyDeviceToHost));
@@ -1123,6 +1166,38 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         *out = e.release();
         return EMT_OK;
     }
+    if (c.kernel == EMT_KERNEL_AUTO && (c.flags & EMT_FLAG_ASYNC_JIT) && e->plan.use_smem && e->plan.ring == nullptr &&
+        !(c.flags & EMT_FLAG_TENSOR_SOLVE)) {
+        // run the generic kernel now; generate + NVRTC-compile the specialised one on a
+        // host thread and switch to it at the first launch after it is ready
+        CodegenOptions opt;
+        opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
+        opt.exact_division = (c.flags & EMT_FLAG_EXACT_DIVISION) != 0;
+        int dev_smem = 0;
+        CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+        opt.smem_budget = static_cast<size_t>(dev_smem);
+        opt.lane_begin = e->lane_begin;
+        e->pending = std::make_unique<PendingJit>();
+        PendingJit* p = e->pending.get();
+        const Schedule* sc = &e->sched;
+        const std::vector<double>* ct = &e->host_ctab;
+        const int W = e->W, dev = e->device;
+        p->done = std::async(std::launch::async, [p, sc, ct, W, dev, opt]() {
+            cudaSetDevice(dev);
+            const auto t0 = std::chrono::steady_clock::now();
+            p->ok = generate_kernel(*sc, *ct, W, opt, p->gen, p->fail);
+            p->gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (p->ok) p->ok = jit_load(p->gen.source, p->gen.name, dev, p->jit, p->log);
+            if (p->ok && driver()->FuncSetAttribute(p->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                                    static_cast<int>(p->gen.smem_bytes)) != CUDA_SUCCESS) {
+                p->ok = false;
+                p->log = "cuFuncSetAttribute(max dynamic smem) failed";
+            }
+        });
+        e->summary += " (async JIT of the specialised kernel in flight)";
+        *out = e.release();
+        return EMT_OK;
+    }
     if (c.kernel != EMT_KERNEL_GENERIC) {
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
@@ -1244,6 +1319,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
     if (e->rows + steps > e->capacity)
         return set_error(EMT_CAPACITY_EXCEEDED, "waveform store holds " + std::to_string(e->capacity) + " rows");
     CUDA_TRY(cudaSetDevice(e->device));
+    adopt_pending(e, false);
     if (steps > e->max_chunk) {
         for (int done = 0; done < steps;) {
             const int n = std::min(e->max_chunk, steps - done);
@@ -1760,6 +1836,13 @@ emt_status emt_engine_read_refactor_steps(emt_engine* e, int32_t* steps, int32_t
 }
 
 int32_t emt_engine_kernel(const emt_engine* e) { return e ? e->kernel_mode : 0; }
+
+emt_status emt_engine_wait_jit(emt_engine* e) {
+    if (e == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    CUDA_TRY(cudaSetDevice(e->device));
+    adopt_pending(e, true);
+    return EMT_OK;
+}
 const char* emt_engine_source(const emt_engine* e) { return e ? e->gen.source.c_str() : ""; }
 const char* emt_engine_summary(const emt_engine* e) { return e ? e->summary.c_str() : ""; }
 

@@ -57,6 +57,7 @@ class _Config(ctypes.Structure):
 KERNEL_AUTO, KERNEL_SPECIALISED, KERNEL_GENERIC, KERNEL_TSIMT, KERNEL_SYSTEM = 0, 1, 2, 3, 4
 FLAG_TENSOR_SOLVE = 1
 FLAG_EXACT_DIVISION = 2  # IEEE fallback in every backward row (include/emt_b200.h)
+FLAG_ASYNC_JIT = 4  # run the generic kernel while the specialised one compiles (include/emt_b200.h)
 
 
 class _Options(ctypes.Structure):
@@ -129,6 +130,7 @@ def lib():
         L.emt_ipc_free.argtypes = [vp]
         L.emt_engine_kernel.argtypes = [vp]
         L.emt_engine_kernel.restype = ctypes.c_int32
+        L.emt_engine_wait_jit.argtypes = [vp]
         L.emt_engine_source.argtypes = [vp]
         L.emt_engine_source.restype = ctypes.c_char_p
         L.emt_engine_summary.argtypes = [vp]
@@ -150,7 +152,7 @@ EXPORTED_SYMBOLS = [
     "emt_interpret", "emt_last_error", "emt_engine_create", "emt_engine_destroy", "emt_engine_shape",
     "emt_engine_reserve", "emt_engine_advance", "emt_engine_sync", "emt_engine_read_waves",
     "emt_engine_read_state", "emt_engine_read_events", "emt_engine_stats", "emt_engine_device_waves",
-    "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_source", "emt_engine_summary",
+    "emt_engine_stream", "emt_version", "emt_engine_kernel", "emt_engine_wait_jit", "emt_engine_source", "emt_engine_summary",
     "emt_codegen", "emt_engine_read_refactor_steps", "emt_engine_load", "emt_engine_run",
     "emt_engine_ring", "emt_engine_attach_ring", "emt_engine_stage", "emt_engine_commit",
     "emt_engine_profile", "emt_engine_run_async", "emt_engine_wait",
@@ -323,13 +325,14 @@ class Engine:
     def __init__(self, schedule: str, initial: np.ndarray, const_table: Optional[np.ndarray] = None,
                  width: int = 0, device: int = 0, lane_begin: int = 0, lane_count: int = 0,
                  lanes_per_block: int = 0, warps: int = 0, kernel: int = KERNEL_AUTO, tensor_solve: bool = False,
-                 exact_division: bool = False):
+                 exact_division: bool = False, async_jit: bool = False):
         L = lib()
         self._h = ctypes.c_void_p()
         init = np.ascontiguousarray(initial, dtype=np.float64)
         ct = None if const_table is None else np.ascontiguousarray(const_table, dtype=np.float64)
         cfg = _config(device, lane_begin, lane_count, lanes_per_block, warps, kernel,
-                      (FLAG_TENSOR_SOLVE if tensor_solve else 0) | (FLAG_EXACT_DIVISION if exact_division else 0))
+                      (FLAG_TENSOR_SOLVE if tensor_solve else 0) | (FLAG_EXACT_DIVISION if exact_division else 0)
+                      | (FLAG_ASYNC_JIT if async_jit else 0))
         _check(L.emt_engine_create(schedule.encode(), _dp(ct) if ct is not None else None, int(width), _dp(init),
                                    init.size, ctypes.byref(cfg), ctypes.byref(self._h)))
         vals = [ctypes.c_int32() for _ in range(9)]
@@ -464,6 +467,10 @@ class Engine:
     @property
     def kernel(self) -> int:
         return int(lib().emt_engine_kernel(self._h))
+
+    def wait_jit(self) -> None:
+        """Blocks until an asynchronous JIT (async_jit=True) is done; later launches use its kernel."""
+        _check(lib().emt_engine_wait_jit(self._h))
 
     @property
     def summary(self) -> str:

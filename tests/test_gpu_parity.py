@@ -296,3 +296,31 @@ def test_fast_division_detects_subnormal_quotients_exact_mode_is_bitwise():
     ex.reserve(g.steps)
     ex.advance(g.steps, sync=True)
     assert bitwise_equal(ex.waves().values, g.waves)
+
+
+def test_async_jit_runs_generic_then_switches_bitwise(tmp_path, monkeypatch):
+    """EMT_FLAG_ASYNC_JIT: creation returns at once, the generic kernel runs while the
+    specialised one compiles on a host thread (empty cubin cache here), and the switch
+    at a launch boundary leaves every sample bit-identical to a synchronous run."""
+    import bench
+    monkeypatch.setenv("EMTB200_CACHE", str(tmp_path))
+    batch, _ = bench.build_batch(48)  # a width no other test compiles: no in-memory cache hit
+    steps = 1200
+    eng = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width,
+                        async_jit=True)
+    eng.reserve(steps)
+    eng.advance(100)
+    eng.advance(100)
+    first = eng.kernel
+    eng.wait_jit()
+    eng.advance(steps - 200)
+    assert eng.kernel == engine.KERNEL_SPECIALISED, eng.summary
+    assert "async JIT" in eng.summary
+    assert first == engine.KERNEL_GENERIC  # NVRTC takes seconds: the first launches ran generic
+    ref = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width)
+    ref.reserve(steps)
+    ref.advance(steps)
+    assert bitwise_equal(eng.waves().values, ref.waves().values)
+    assert np.array_equal(eng.events(), ref.events())
+    assert eng.stats().factor_count == ref.stats().factor_count
+    assert bitwise_equal(eng.state(), ref.state())

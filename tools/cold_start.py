@@ -1,15 +1,19 @@
 """Cold-start end-to-end time of one bench step through the public API, JIT included.
 
-    EMTB200_CACHE=<empty dir> python tools/cold_start.py <workload> <scenarios> <emt_steps> [device]
+    python tools/cold_start.py <workload> <scenarios> <emt_steps> <device> <sync|async>
 
 Runs in a fresh process (empty in-memory cubin cache) with an empty on-disk cache:
-engine creation (schedule parse, code generation, NVRTC compile, module load) +
-the batch's H2D from pinned host memory + `emt_steps` passes + the waveform D2H.
-Prints one JSON object (seconds). Called by bench.py for the `e2e_cold` key.
+engine creation + the batch's H2D from pinned host memory + `emt_steps` passes +
+the waveform D2H, either with the JIT before the first pass (`sync`) or with
+EMT_FLAG_ASYNC_JIT (`async`: the generic kernel runs while NVRTC compiles; the
+engine switches to the specialised kernel when it is ready). Prints one JSON
+object (seconds) and writes the waveform digest. Called twice by bench.py for
+the `e2e_cold` key.
 """
 import json
 import os
 import sys
+import tempfile
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -28,16 +32,22 @@ def main():
     batch, info = bench.build_batch(n, workload=wl)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     ct, init = pin(batch.const_table), pin(batch.initial)
+    mode = sys.argv[5] if len(sys.argv) > 5 else "sync"
+    os.environ["EMTB200_CACHE"] = tempfile.mkdtemp()
     out = torch.empty((S, len(info.channels) * batch.width), dtype=torch.float64, pin_memory=True).numpy()
     t0 = time.perf_counter()
-    eng = engine.Engine(batch.schedule, init, const_table=ct, width=batch.width, device=dev)
+    eng = engine.Engine(batch.schedule, init, const_table=ct, width=batch.width, device=dev, async_jit=mode == "async")
     t1 = time.perf_counter()
-    eng.run(S, out, chunk=min(S, 1000))
+    eng.run(S, out, chunk=min(S, 100 if mode == "async" else 1000))
     t2 = time.perf_counter()
+    ran = eng.summary
+    eng.wait_jit()
     summ = eng.summary
     jit = float(summ.split("jit=")[1].split("s")[0]) if "jit=" in summ else None
-    print(json.dumps({"create_s": t1 - t0, "run_s": t2 - t1, "total_s": t2 - t0, "jit_s": jit,
-                      "cached": "(cached)" in summ, "kernel": summ[:120]}))
+    import hashlib
+    res = {"mode": mode, "total_s": t2 - t0, "create_s": t1 - t0, "run_s": t2 - t1, "jit_s": jit,
+           "kernel_during_run": ran[:90], "digest": hashlib.sha1(out.tobytes()).hexdigest()}
+    print(json.dumps(res))
 
 
 if __name__ == "__main__":
