@@ -897,6 +897,14 @@ emt_status build_system_plan(emt_engine* e) {
     }
     if (s.l_col.empty()) std::fill(tsrc.begin(), tsrc.end(), -1);
     S.fstream_len = static_cast<long long>(fsrc.size());
+    int max_urow = 1;
+    for (int r = 0; r < dim; ++r) max_urow = std::max(max_urow, s.u_row_ptr[static_cast<size_t>(r) + 1] - s.u_row_ptr[static_cast<size_t>(r)] - 1);
+    S.fact_threads = std::min(kSysThreads, 32 * ((max_urow + 31) / 32));
+    std::vector<int4> lent(std::max<size_t>(1, s.l_col.size()), make_int4(0, 0, 0, 0));
+    for (size_t k = 0; k < s.l_col.size(); ++k) {
+        const int c = s.l_col[k];
+        lent[k] = make_int4(c, s.u_row_ptr[static_cast<size_t>(c)], s.u_row_ptr[static_cast<size_t>(c) + 1], 0);
+    }
     std::vector<int> bcol, bsrc, brow_len;
     S.pmax = 1;
     for (int i = dim - 1; i >= 0; --i) {
@@ -928,6 +936,7 @@ emt_status build_system_plan(emt_engine* e) {
     EMT_TRY(e->upload(fcol, S.fcol));
     EMT_TRY(e->upload(fdst, S.fdst));
     EMT_TRY(e->upload(tsrc, S.tsrc));
+    EMT_TRY(e->upload(lent, S.lent));
     EMT_TRY(e->upload(bcol, S.bcol));
     EMT_TRY(e->upload(bsrc, S.bsrc));
     EMT_TRY(e->upload(brow_len, d));

@@ -60,6 +60,8 @@ struct SysPlan {
     double* bval;            // W x stream_len: the lane's stream values (rebuilt at launch start and after each factorisation)
     double* work;            // lane-major working arena when W > 1 (W == 1 runs on the arena itself)
     double* frcp;            // W x dim: pivot reciprocals 1/U(c,c) of the lane's current factors
+    const int4* lent;        // l_nnz: (column c, U row begin, U row end, -) of every L entry (factorisation)
+    int fact_threads;        // threads taking part in an elimination step: 32 x ceil(longest U row / 32)
     int smem_xs;             // byte offsets in dynamic shared memory
     int smem_tile;
     int smem_ring_v;
@@ -151,6 +153,19 @@ __device__ __forceinline__ void sys_build_stream(const DevPlan& P, const SysPlan
     }
 }
 
+__device__ __forceinline__ void sys_cp_async(void* dst, const void* src, int bytes) {
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sys_smem_addr(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sys_smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void sys_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void sys_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+constexpr int kSysFD = 4;  // factorisation: elimination steps whose operands are in flight (cp.async)
+static_assert(kSysFD * kSysThreads <= kSysRing * kSysChunk, "factorisation pipeline must fit the TMA ring");
+
 // FactorizeSystem for one lane on the whole block (exec.cpp:175-204 + lu_factor,
 // sparse.cpp:79-145): the reference's up-looking rows, one row at a time; within a
 // row the eliminations run in ascending column order, each one's update of the
@@ -183,30 +198,75 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
     double* Lv = A + P.l;
     double* Uv = A + P.u;
     double* R = S.frcp + static_cast<size_t>(lane) * static_cast<size_t>(P.dim > 0 ? P.dim : 1);
+    double* fuv = reinterpret_cast<double*>(sm + S.smem_ring_v);  // [kSysFD][1024] (the TMA ring is idle here)
+    int* fuc = reinterpret_cast<int*>(sm + S.smem_ring_c);
+    double* fdr = reinterpret_cast<double*>(sm + S.smem_desc);    // [kSysFD][2]
+    long long tf = clock64();
     for (int i = 0; i < P.dim; ++i) {
         const int lb = __ldg(&P.l_row_ptr[i]), le = __ldg(&P.l_row_ptr[i + 1]);
         const int ub = __ldg(&P.u_row_ptr[i]), ue = __ldg(&P.u_row_ptr[i + 1]);
+        // operands of the row's first eliminations in flight (cp.async into the idle TMA
+        // ring): each thread's U entry and column, thread 0 the pivot and its reciprocal
+        const int n = le - lb;
+        auto issue = [&](int k, int slot) {
+            const int4 e4 = __ldg(&S.lent[k]);  // c, U row [cb, ce)
+            const int j = e4.y + 1 + tid;
+            if (j < e4.z) {
+                sys_cp_async(fuv + slot * kSysThreads + tid, Uv + j, 8);
+                sys_cp_async(fuc + slot * kSysThreads + tid, P.u_col + j, 4);
+            }
+            if (tid == 0) {
+                sys_cp_async(fdr + 2 * slot, Uv + e4.y, 8);
+                sys_cp_async(fdr + 2 * slot + 1, R + e4.x, 8);
+            }
+        };
+        const int nft = S.fact_threads;  // the other warps skip the eliminations (nothing to update)
+        if (tid < nft)
+            for (int q = 0; q < kSysFD - 1; ++q) {
+                if (q < n) issue(lb + q, q);
+                sys_cp_commit();
+            }
         // scatter row i of A over the union pattern, fill positions zero (sparse.cpp:94-110)
         for (int q = lb + tid; q < le; q += kSysThreads) Sx[__ldg(&P.l_col[q])] = 0.0;
         for (int q = ub + tid; q < ue; q += kSysThreads) Sx[__ldg(&P.u_col[q])] = 0.0;
         __syncthreads();
         for (int q = __ldg(&P.row_ptr[i]) + tid; q < __ldg(&P.row_ptr[i + 1]); q += kSysThreads)
             Sx[__ldg(&P.col_idx[q])] = G[q];
+        sys_cp_wait<kSysFD - 2>();
         __syncthreads();
-        // eliminate with the settled rows, ascending columns (sparse.cpp:112-124)
-        for (int k = lb; k < le; ++k) {
-            const int c = __ldg(&P.l_col[k]);
-            const int cb = __ldg(&P.u_row_ptr[c]), ce = __ldg(&P.u_row_ptr[c + 1]);
-            const double x = Sx[c], d = Uv[cb], r = R[c];
+        sys_mark(S, tf, 12);  // factorisation: row set-up
+        // eliminate with the settled rows, ascending columns (sparse.cpp:112-124); the
+        // participating warps synchronise on named barrier 1 only
+        if (tid < nft)
+        for (int sidx = 0; sidx < n; ++sidx) {
+            const int k = lb + sidx, slot = sidx % kSysFD;
+            if (sidx + kSysFD - 1 < n) issue(k + kSysFD - 1, (sidx + kSysFD - 1) % kSysFD);
+            sys_cp_commit();
+            const int4 e4 = __ldg(&S.lent[k]);
+            const double x = Sx[e4.x], d = fdr[2 * slot], r = fdr[2 * slot + 1];
+            // x / d: Markstein while |x r| is in range; a zero x (three in four L entries of the
+            // gen_scale_case factors are exact zeros) gives x r = the signed zero x / d whenever
+            // 1/d is in range (not NaN); anything else takes the IEEE division
             const double q0 = x * r;
-            const double lik = (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900) ? __fma_rn(__fma_rn(-d, q0, x), r, q0) : x / d;
+            const double lik = (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900) ? __fma_rn(__fma_rn(-d, q0, x), r, q0)
+                               : (x == 0.0 && r == r)                          ? q0
+                                                                               : x / d;
             if (tid == 0) Lv[k] = lik;
-            for (int j = cb + 1 + tid; j < ce; j += kSysThreads) {
-                const int cj = __ldg(&P.u_col[j]);
-                Sx[cj] = Sx[cj] - lik * Uv[j];
+            const int j = e4.y + 1 + tid;
+            if (j < e4.z) {
+                const int cj = fuc[slot * kSysThreads + tid];
+                Sx[cj] = Sx[cj] - lik * fuv[slot * kSysThreads + tid];
             }
-            __syncthreads();
+            for (int jj = j + kSysThreads; jj < e4.z; jj += kSysThreads) {  // U rows longer than the block
+                const int cj = __ldg(&P.u_col[jj]);
+                Sx[cj] = Sx[cj] - lik * Uv[jj];
+            }
+            sys_cp_wait<kSysFD - 2>();
+            asm volatile("bar.sync 1, %0;\n" ::"r"(nft) : "memory");
         }
+        __syncthreads();
+        sys_mark(S, tf, 13);  // factorisation: eliminations
+        if (S.prof != nullptr && tid == 0) S.prof[15] += n;
         for (int q = ub + tid; q < ue; q += kSysThreads) Uv[q] = Sx[__ldg(&P.u_col[q])];
         const double piv = Sx[i];  // U(i, i), first in its row (sparse.cpp:126-131)
         if (tid == 0) R[i] = sys_rcp(piv);
@@ -215,6 +275,7 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
             return 1;
         }
         __syncthreads();
+        sys_mark(S, tf, 14);  // factorisation: U row, pivot
     }
     // the scratch row's final contents (every column is some row's diagonal, so all are written)
     double* scr = A + P.scratch;
@@ -455,6 +516,8 @@ __device__ int sys_solve(const DevPlan& P, const SysPlan& S, double* __restrict_
             const double q0 = x * rcp;
             if (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900)
                 x = __fma_rn(__fma_rn(-d, q0, x), rcp, q0);
+            else if (x == 0.0 && rcp == rcp)  // signed zero quotient (1/d in range)
+                x = q0;
             else
                 x = x / d;
             last = x;

@@ -14,6 +14,10 @@ for k in [int(a) for a in sys.argv[1:]] or [32, 128]:
     n = 200 if k <= 128 else 50
     eng.reserve(3 * n + 1)
     t0 = time.time(); eng.advance(1, sync=True); t_first = time.time() - t0
+    if os.environ.get("EMTB200_CG_PROF"):
+        pf = eng.profile()[0]
+        print(json.dumps({"k": k, "factor_setup": int(pf[12]), "factor_elim": int(pf[13]), "factor_urow": int(pf[14]),
+                          "elim_steps": int(pf[15]), "cycles_per_step": float(pf[13]) / max(1, int(pf[15]))}), flush=True)
     eng.advance(n, sync=True)
     prof0 = eng.profile()[0, :12].copy() if os.environ.get("EMTB200_CG_PROF") else None
     t0 = time.time(); eng.advance(n, sync=True); dt = (time.time() - t0) / n
