@@ -324,3 +324,31 @@ def test_async_jit_runs_generic_then_switches_bitwise(tmp_path, monkeypatch):
     assert np.array_equal(eng.events(), ref.events())
     assert eng.stats().factor_count == ref.stats().factor_count
     assert bitwise_equal(eng.state(), ref.state())
+
+
+def test_async_jit_engine_closed_while_compiling_and_serving_paths(tmp_path, monkeypatch):
+    """Destroying an engine whose JIT is still compiling waits for the host thread; the
+    staged-batch serving path (stage / commit / run_async) across the switch stays bitwise."""
+    import bench
+    monkeypatch.setenv("EMTB200_CACHE", str(tmp_path))
+    batch, _ = bench.build_batch(40)
+    e = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, async_jit=True)
+    e.close()  # compile still in flight: the destructor joins it
+    ref = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width)
+    ref.reserve(600)
+    ref.advance(600)
+    want = ref.waves().values
+    e = engine.Engine(batch.schedule, batch.initial, const_table=batch.const_table, width=batch.width, async_jit=True)
+    outs = []
+    for k in range(3):
+        e.stage(batch.initial, batch.const_table)
+        e.commit()
+        out = np.zeros((600, e.channels * e.lanes))
+        e.run_async(600, out, chunk=100)
+        e.wait()
+        outs.append(out)
+        if k == 0:
+            e.wait_jit()
+    assert e.kernel == engine.KERNEL_SPECIALISED
+    for out in outs:
+        assert bitwise_equal(out, want)
