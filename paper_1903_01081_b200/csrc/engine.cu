@@ -1482,7 +1482,9 @@ emt_status emt_engine_stage(emt_engine* e, const double* initial, int64_t initia
                                                      " x width " + std::to_string(e->width));
     if (e->staged) return set_error(EMT_NON_POSITIVE_INPUT, "a staged batch is waiting for emt_engine_commit");
     const size_t W = static_cast<size_t>(e->W), width = static_cast<size_t>(e->width), lb = static_cast<size_t>(e->lane_begin);
-    if (const_table != nullptr && (e->kernel_mode == EMT_KERNEL_SPECIALISED || e->kernel_mode == EMT_KERNEL_TSIMT)) {
+    // (also while an async JIT is in flight: its kernel compiles the same constants in)
+    if (const_table != nullptr &&
+        (e->kernel_mode == EMT_KERNEL_SPECIALISED || e->kernel_mode == EMT_KERNEL_TSIMT || e->pending != nullptr)) {
         // constants compiled in as immediates must keep their values (an isomorphic batch)
         for (size_t q = 0; q < e->inv_slots.size(); ++q) {
             const double* row = const_table + static_cast<size_t>(e->inv_slots[q]) * width + lb;
