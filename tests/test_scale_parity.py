@@ -133,10 +133,10 @@ def test_single_scenario_20000_steps_vs_reference(case, kernel):
 
 def test_c4_120_copies_vs_oracle():
     """C4: 120 IEEE-39 copies coupled by Bergeron lines (one system), persistent
-    line-coupled launches, against the C oracle (the reference has no line model)."""
+    line-coupled launches, 20,000 passes, against the C oracle (the reference has no line model)."""
     import bench
     batch, info = bench.build_batch(120, workload="c4")
-    steps = 4000
+    steps = STEPS  # the full 1 s (the C oracle runs it in a few seconds)
     eng = _device_run(batch, steps)
     want = oracle.Schedule(batch.text()).interpret(batch.initial, steps)
     rep = parity.merge([parity.compare(eng.waves(0, steps).values, want.waves)])

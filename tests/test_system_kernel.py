@@ -21,7 +21,7 @@ def _case(k):
     return s, st
 
 
-@pytest.mark.parametrize("k,steps", [(32, 2000), (128, 300)])
+@pytest.mark.parametrize("k,steps", [(32, 4000), (128, 1500)])
 def test_scale_case_bitwise_vs_reference(k, steps):
     s, st = _case(k)
     eng = engine.Engine(s, st)
