@@ -492,14 +492,16 @@ __device__ int sys_solve(const DevPlan& P, const SysPlan& S, double* __restrict_
             if (tl == 0) flags[0] = i + 1;
             const long long c1 = S.prof ? clock64() : 0;
             const double* pb = pbuf + buf * S.pmax;
+            const double u1 = desc[buf * 4 + 0], d = desc[buf * 4 + 1], rcp = desc[buf * 4 + 2];
             int t = 0;
             if (adj) {
-                x = x - desc[buf * 4 + 0] * last;
+                x = x - u1 * last;
                 t = 1;
             }
             if (len > t) {  // groups of eight (zero-padded), the next group's loads in flight
                 double q0 = pb[t], q1 = pb[t + 1], q2 = pb[t + 2], q3 = pb[t + 3];
                 double q4 = pb[t + 4], q5 = pb[t + 5], q6 = pb[t + 6], q7 = pb[t + 7];
+#pragma unroll 2
                 for (t += 8; t < len; t += 8) {
                     const double n0 = pb[t], n1 = pb[t + 1], n2 = pb[t + 2], n3 = pb[t + 3];
                     const double n4 = pb[t + 4], n5 = pb[t + 5], n6 = pb[t + 6], n7 = pb[t + 7];
@@ -510,12 +512,12 @@ __device__ int sys_solve(const DevPlan& P, const SysPlan& S, double* __restrict_
                 x = x - q0; x = x - q1; x = x - q2; x = x - q3;
                 x = x - q4; x = x - q5; x = x - q6; x = x - q7;
             }
-            const double d = desc[buf * 4 + 1], rcp = desc[buf * 4 + 2];
             // x / d: Markstein's correction of x * (1/d) is the IEEE quotient while
             // 1/d is in range (else NaN) and |q0| stays in [2^-900, 2^900]
             const double q0 = x * rcp;
-            if (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900)
-                x = __fma_rn(__fma_rn(-d, q0, x), rcp, q0);
+            const double mk = __fma_rn(__fma_rn(-d, q0, x), rcp, q0);
+            if (__builtin_expect(fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900, 1))
+                x = mk;
             else if (x == 0.0 && rcp == rcp)  // signed zero quotient (1/d in range)
                 x = q0;
             else
