@@ -568,7 +568,7 @@ __device__ int sys_solve(const DevPlan& P, const SysPlan& S, double* __restrict_
 __global__ void __launch_bounds__(kSysThreads, 1)
 emt_system_kernel(const DevPlan P, const SysPlan S, const int step0, const int nsteps, const int row0) {
     extern __shared__ __align__(128) unsigned char sys_smem[];
-    const int tid = threadIdx.x, wid = tid >> 5, tl = tid & 31;
+    const int tid = threadIdx.x;
     const int lane = blockIdx.x;
     if (P.lane_err[lane].code != 0) return;  // lane already failed: frozen
     double* A;
