@@ -933,8 +933,8 @@ struct Sched {
 // first). A barrier is inserted when no warp has visible work, or when the
 // earliest-idle warp starves while enough work waits behind the barrier.
 Sched schedule_region(const std::vector<Task>& tasks, const std::vector<int>& ids,
-                      const std::vector<std::vector<int>>& deps, int G, double* makespan) {
-    const long kBarrier = knob("EMTB200_CG_BARRIER", knob("EMTB200_CG_COSTV2", 1) ? 100 : 200);
+                      const std::vector<std::vector<int>>& deps, int G, double* makespan, long barrier_cost = 100) {
+    const long kBarrier = knob("EMTB200_CG_BARRIER", knob("EMTB200_CG_COSTV2", 1) ? barrier_cost : 200);
     Sched out;
     const size_t n = ids.size();
     if (n == 0) {
@@ -1639,7 +1639,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     const int G = std::max(1, std::min(opt.warps, 32));
     double span_a = 0, span_b = 0;
-    Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a);
+    // a single lane (solo form) pays a barrier more than a 32-lane group does relative to
+    // its tasks: fewer, fuller phases (barrier cost 100 -> 400: C2 2.63 -> 2.55 us; the
+    // same setting costs C3 1%, so 32-lane groups keep 100)
+    const long bar_cost = solo ? 400 : 100;
+    Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a, bar_cost);
     if (sa.phases.size() == 1 && knob("EMTB200_CG_AFFINITY", 1) != 0) {
         // region A is one phase of independent tasks: regroup them so that tasks reading
         // the same node voltages share a warp (the compiler then loads each voltage once
@@ -1676,9 +1680,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
             sa.phases[0] = parts;
         }
     }
-    Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b);
+    Sched sb = schedule_region(g.tasks, ids_b, deps, G, &span_b, bar_cost);
     double span_c = 0;
-    Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c);
+    Sched sc3 = schedule_region(g.tasks, ids_c, deps, G, &span_c, bar_cost);
     {
         // filler tasks go where a warp idles longest before a barrier of the last region
         Sched& host = g.dmma ? sc3 : sb;
