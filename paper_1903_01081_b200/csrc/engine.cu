@@ -1192,15 +1192,23 @@ emt_status emt_engine_create(const char* schedule_text, const double* const_tabl
         const std::vector<double>* ct = &e->host_ctab;
         const int W = e->W, dev = e->device;
         p->done = std::async(std::launch::async, [p, sc, ct, W, dev, opt]() {
-            cudaSetDevice(dev);
-            const auto t0 = std::chrono::steady_clock::now();
-            p->ok = generate_kernel(*sc, *ct, W, opt, p->gen, p->fail);
-            p->gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (p->ok) p->ok = jit_load(p->gen.source, p->gen.name, dev, p->jit, p->log);
-            if (p->ok && driver()->FuncSetAttribute(p->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                                                    static_cast<int>(p->gen.smem_bytes)) != CUDA_SUCCESS) {
+            try {  // nothing may escape the thread: get() would rethrow it across the C ABI
+                cudaSetDevice(dev);
+                const auto t0 = std::chrono::steady_clock::now();
+                p->ok = generate_kernel(*sc, *ct, W, opt, p->gen, p->fail);
+                p->gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                if (p->ok) p->ok = jit_load(p->gen.source, p->gen.name, dev, p->jit, p->log);
+                if (p->ok && driver()->FuncSetAttribute(p->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                                        static_cast<int>(p->gen.smem_bytes)) != CUDA_SUCCESS) {
+                    p->ok = false;
+                    p->log = "cuFuncSetAttribute(max dynamic smem) failed";
+                }
+            } catch (const std::exception& ex) {
                 p->ok = false;
-                p->log = "cuFuncSetAttribute(max dynamic smem) failed";
+                p->log = std::string("async JIT failed: ") + ex.what();
+            } catch (...) {
+                p->ok = false;
+                p->log = "async JIT failed";
             }
         });
         e->summary += " (async JIT of the specialised kernel in flight)";
