@@ -1099,9 +1099,26 @@ const char* emt_version(void) {
 #endif
 }
 
+static emt_status engine_create(const char* schedule_text, const double* const_table, int32_t width,
+                                const double* initial, int64_t initial_len, const emt_config* cfg, emt_engine** out);
+
+// C ABI entry points doing host-side work (parsing, planning, code generation) turn any
+// C++ exception (e.g. std::bad_alloc) into a status instead of unwinding into C callers.
 emt_status emt_engine_create(const char* schedule_text, const double* const_table, int32_t width,
                              const double* initial, int64_t initial_len, const emt_config* cfg,
                              emt_engine** out) {
+    try {
+        return engine_create(schedule_text, const_table, width, initial, initial_len, cfg, out);
+    } catch (const std::exception& ex) {
+        return set_error(EMT_CUDA_ERROR, std::string("internal error: ") + ex.what());
+    } catch (...) {
+        return set_error(EMT_CUDA_ERROR, "internal error");
+    }
+}
+
+static emt_status engine_create(const char* schedule_text, const double* const_table, int32_t width,
+                                const double* initial, int64_t initial_len, const emt_config* cfg,
+                                emt_engine** out) {
     if (out == nullptr || schedule_text == nullptr) return set_error(EMT_INVALID_HANDLE, "null argument");
     *out = nullptr;
     auto e = std::make_unique<emt_engine>();
@@ -1872,9 +1889,25 @@ static emt_status interpret_once(const char* schedule_text, const double* initia
                                  const emt_exec_options* options, emt_config c, double* waves, double* time,
                                  emt_exec_stats* stats);
 
+static emt_status interpret_retry(const char* schedule_text, const double* initial, int64_t initial_len,
+                                  int32_t steps, const emt_exec_options* options, const emt_config* cfg,
+                                  double* waves, double* time, emt_exec_stats* stats);
+
 emt_status emt_interpret(const char* schedule_text, const double* initial, int64_t initial_len, int32_t steps,
                          const emt_exec_options* options, const emt_config* cfg, double* waves, double* time,
                          emt_exec_stats* stats) {
+    try {
+        return interpret_retry(schedule_text, initial, initial_len, steps, options, cfg, waves, time, stats);
+    } catch (const std::exception& ex) {
+        return set_error(EMT_CUDA_ERROR, std::string("internal error: ") + ex.what());
+    } catch (...) {
+        return set_error(EMT_CUDA_ERROR, "internal error");
+    }
+}
+
+static emt_status interpret_retry(const char* schedule_text, const double* initial, int64_t initial_len,
+                                  int32_t steps, const emt_exec_options* options, const emt_config* cfg,
+                                  double* waves, double* time, emt_exec_stats* stats) {
     if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
     emt_config c{};
     if (cfg) c = *cfg;
