@@ -884,8 +884,8 @@ emt_status build_system_plan(emt_engine* e) {
         } while (i0 < sv.size());  // every block has >= 1 (possibly empty) round: it stages the next tile
         rnd_ptr.push_back(static_cast<int>(rnd.size()));
     }
-    if (fsrc.empty()) {
-        fsrc.push_back(0);
+    if (fsrc.empty()) {  // one placeholder entry (never read as an L value)
+        fsrc.push_back(-1);
         fcol.push_back(0);
         fdst.push_back(0);
     }

@@ -146,7 +146,10 @@ __device__ __forceinline__ void sys_build_stream(const DevPlan& P, const SysPlan
         const int s = __ldg(&S.bsrc[e]);
         bv[e] = s >= 0 ? Uv[s] : (s == INT_MIN ? 0.0 : sys_rcp(Uv[-1 - s]));
     }
-    for (long long e = threadIdx.x; e < S.fstream_len; e += kSysThreads) fv[e] = Lv[__ldg(&S.fsrc[e])];
+    for (long long e = threadIdx.x; e < S.fstream_len; e += kSysThreads) {
+        const int k = __ldg(&S.fsrc[e]);
+        fv[e] = k >= 0 ? Lv[k] : 0.0;  // -1: the placeholder entry of an empty stream
+    }
     for (long long q = threadIdx.x; q < static_cast<long long>(S.nblk) * 1024; q += kSysThreads) {
         const int s = __ldg(&S.tsrc[q]);
         tv[q] = s >= 0 ? Lv[s] : 0.0;
