@@ -144,3 +144,72 @@ def subnormal_decay(dt=1e-4, duration=0.6):
         comp("r23", "resistor", {"resistance": 0.5}, "2", "3"),
         comp("r3", "resistor", {"resistance": 0.2}, "3", "0"),
     ], ["v:1", "v:2", "v:3"], dt, duration)
+
+
+def fuzz(seed: int):
+    """Seeded random document exercising every electrical kind, switches with several
+    toggles, AC/DC sources and a random control chain fed by meters and driving an
+    actuator: the property-style parity set (tests/golden/fuzz/, tools/make_fuzz_fixtures.py)."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(4, 24))
+    nodes = [str(k) for k in range(1, n + 1)]
+    comps = []
+    u = lambda lo, hi: float(rng.uniform(lo, hi))
+
+    def add(kind, params, a, b):
+        comps.append(comp(f"c{len(comps):03d}", kind, params, a, b))
+
+    add("resistor", {"resistance": u(0.5, 5.0)}, "1", "0")  # ground path
+    for k in range(2, n + 1):  # spanning tree of mixed branches
+        a = str(int(rng.integers(1, k)))
+        kind = int(rng.integers(0, 4))
+        if kind == 0:
+            add("resistor", {"resistance": u(0.2, 5.0)}, a, str(k))
+        elif kind == 1:
+            add("series_rl", {"resistance": u(0.05, 1.0), "inductance": 1e-3 * u(0.2, 3.0)}, a, str(k))
+        elif kind == 2:
+            add("inductor", {"inductance": 1e-3 * u(0.2, 3.0)}, a, str(k))
+        else:
+            add("resistor", {"resistance": u(0.2, 5.0)}, a, str(k))
+        if rng.random() < 0.5:  # shunt to ground
+            if rng.random() < 0.5:
+                add("capacitor", {"capacitance": 1e-5 * u(0.3, 3.0)}, str(k), "0")
+            else:
+                add("resistor", {"resistance": u(5.0, 50.0)}, str(k), "0")
+    for _ in range(int(rng.integers(0, 6))):  # meshing branches
+        a, b = (str(int(x)) for x in rng.integers(1, n + 1, size=2))
+        if a != b:
+            add("resistor", {"resistance": u(0.5, 10.0)}, a, b)
+    for _ in range(int(rng.integers(1, 4))):  # breakers, possibly several toggles
+        a, b = (str(int(x)) for x in rng.integers(1, n + 1, size=2))
+        if a == b:
+            b = "0"
+        times = sorted(float(t) for t in rng.uniform(1e-4, 4e-3, size=int(rng.integers(1, 4))))
+        add("switch", {"state": "closed" if rng.random() < 0.5 else "open", "toggle_times": times}, a, b)
+    for _ in range(int(rng.integers(1, 3))):  # sources: AC or DC
+        a = str(int(rng.integers(1, n + 1)))
+        f = 0.0 if rng.random() < 0.3 else u(40.0, 400.0)
+        if rng.random() < 0.5:
+            add("voltage_source", {"magnitude": u(1.0, 100.0), "frequency": f, "phase": u(-3.0, 3.0),
+                                   "rs": u(0.05, 1.0)}, a, "0")
+        else:
+            add("current_source", {"magnitude": u(0.1, 5.0), "frequency": f, "phase": u(-3.0, 3.0)}, a, "0")
+    meter_node = str(int(rng.integers(1, n + 1)))
+    act = str(int(rng.integers(1, n + 1)))
+    comps.append(comp("act", "controlled_current_source", {"gain": u(-0.05, 0.05)}, act, "0"))
+    control = [
+        {"id": "k1", "kind": "gain", "params": {"k": u(-0.5, 0.5)}, "inputs": ["vm"]},
+        {"id": "lag", "kind": "first_order_lag", "params": {"T": u(1e-4, 1e-2)}, "inputs": ["k1"]},
+        {"id": "itg", "kind": "integrator", "params": {}, "inputs": ["lag"]},
+        {"id": "pi", "kind": "pi_controller", "params": {"kp": u(0.0, 0.5), "ki": u(0.0, 5.0)}, "inputs": ["lag"]},
+        {"id": "sum", "kind": "sum", "params": {}, "inputs": ["pi", "-itg", "one"]},
+        {"id": "one", "kind": "constant", "params": {"value": u(-1.0, 1.0)}, "inputs": []},
+        {"id": "lim", "kind": "limiter", "params": {"min": -u(0.5, 5.0), "max": u(0.5, 5.0)}, "inputs": ["sum"]},
+        {"id": "cmp", "kind": "comparator", "params": {}, "inputs": ["lim", "k1"]},
+        {"id": "dly", "kind": "delay", "params": {}, "inputs": ["cmp"]},
+    ]
+    couplings = [{"direction": "meter", "electrical_ref": meter_node, "signal_ref": "vm"},
+                 {"direction": "actuator", "electrical_ref": "act", "signal_ref": "lim"}]
+    sw = [c["id"] for c in comps if c["kind"] == "switch"]
+    channels = [f"v:{nodes[0]}", f"v:{nodes[-1]}", f"i:{sw[0]}", "s:lim", "s:dly"]
+    return _doc(nodes, comps, channels, 1e-5, float(rng.choice([2e-3, 5e-3])), control=control, couplings=couplings)
