@@ -45,5 +45,36 @@ def main(count):
             print(f"fuzz_{seed}: error {e.code} {e.msg[:60]}")
 
 
+def batched(count):
+    """Vectorised variants (the reference's own `vectorize`, compile_task with override
+    rows): per lane, other resistances, source magnitudes and controlled-source gain."""
+    rng = np.random.default_rng(77)
+    for seed in range(count):
+        doc = docs.fuzz(100 + seed)
+        d = json.loads(doc)
+        res = [c["id"] for c in d["components"] if c["kind"] == "resistor"][:3]
+        src = [c for c in d["components"] if c["kind"] in ("voltage_source", "current_source")][:1]
+        W = int(rng.integers(3, 9))
+        rows = []
+        for _ in range(W):
+            row = [{"component": r, "param": "resistance", "value": float(rng.uniform(0.3, 6.0))} for r in res]
+            row += [{"component": c["id"], "param": "magnitude", "value": float(rng.uniform(0.5, 50.0))} for c in src]
+            row.append({"component": "act", "param": "gain", "value": float(rng.uniform(-0.05, 0.05))})
+            rows.append(row)
+        c = ref.compile_document(doc, rows=rows)
+        steps = int(round(d["task"]["duration"] / d["task"]["dt"]))
+        name = f"fuzzw_{seed}"
+        for ext, text in (("cgmsched", c.schedule), ("state", c.state)):
+            with gzip.open(os.path.join(OUT, f"{name}.{ext}.gz"), "wt", compresslevel=9) as f:
+                f.write(text)
+        init = ref.parse_state(c.state)
+        r = ref.execute(c.schedule, init, steps)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), waves=r.waves, time=r.time,
+                            factor_count=r.factor_count, error_code=0,
+                            meta=json.dumps({"steps": steps, "note": f"docs.fuzz({100 + seed}) x {W} lanes"}))
+        print(f"{name}: W={W} {r.waves.shape} factor_count={r.factor_count}")
+
+
 if __name__ == "__main__":
     main(int(sys.argv[1]) if len(sys.argv) > 1 else 24)
+    batched(8)
