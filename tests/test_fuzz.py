@@ -3,7 +3,9 @@ electrical kind, meshed topologies, breakers toggling several times, AC and DC
 sources, a meter -> control chain -> actuator loop through all control kinds)
 compiled and run by the REAL reference (tools/make_fuzz_fixtures.py). The C oracle
 (CPU) and every device kernel (GPU) must reproduce the reference's waveforms bit for
-bit and its refactorisation count."""
+bit and its refactorisation count. `fuzzw_*` are vectorised by the reference's own
+override rows; `fuzzl_*` add `transmission_line` components (no reference line
+model: their stored waves are the C oracle's, so they pin the device kernels)."""
 import gzip
 import json
 import os
@@ -27,7 +29,7 @@ def load(name):
 
 
 def test_fuzz_set_present():
-    assert len(CASES) >= 24
+    assert len(CASES) >= 38
 
 
 @pytest.mark.parametrize("name", CASES)

@@ -75,6 +75,39 @@ def batched(count):
         print(f"{name}: W={W} {r.waves.shape} factor_count={r.factor_count}")
 
 
+def with_lines(count):
+    """Random documents plus 1-3 `transmission_line` components (the document kind,
+    lines.document_batch). The reference has no line model: these are checked
+    device == C oracle, and the stored waves are the oracle's."""
+    from oracle import oracle
+    from paper_1903_01081_b200 import lines
+    from paper_1903_01081_b200 import schedule as sch
+    rng = np.random.default_rng(99)
+    for seed in range(count):
+        d = json.loads(docs.fuzz(200 + seed))
+        nodes = d["nodes"]
+        for q in range(int(rng.integers(1, 4))):
+            a, b = rng.choice(len(nodes), size=2, replace=False)
+            d["components"].append({"id": f"tl{q}", "kind": "transmission_line", "terminals": [nodes[a], nodes[b]],
+                                    "params": {"surge_impedance": float(rng.uniform(50.0, 500.0)),
+                                               "travel_time": float(rng.uniform(2.0, 9.0)) * d["task"]["dt"]}})
+        doc = json.dumps(d)
+        batch = lines.document_batch(doc, lambda x: (lambda c: (c.schedule, ref.parse_state(c.state)))(ref.compile_document(x)))
+        steps = int(round(d["task"]["duration"] / d["task"]["dt"]))
+        name = f"fuzzl_{seed}"
+        ext_n = batch.initial.size // batch.width
+        with gzip.open(os.path.join(OUT, f"{name}.cgmsched.gz"), "wt", compresslevel=9) as f:
+            f.write(batch.text())
+        with gzip.open(os.path.join(OUT, f"{name}.state.gz"), "wt", compresslevel=9) as f:
+            f.write(sch.format_state(batch.initial, ext_n, batch.width))
+        r = oracle.Schedule(batch.text()).interpret(batch.initial, steps)
+        np.savez_compressed(os.path.join(OUT, f"{name}.npz"), waves=r.waves,
+                            time=(np.arange(steps) + 1) * d["task"]["dt"], factor_count=r.factor_count, error_code=0,
+                            meta=json.dumps({"steps": steps, "note": f"docs.fuzz({200 + seed}) + lines (C oracle)"}))
+        print(f"{name}: {r.waves.shape} factor_count={r.factor_count}")
+
+
 if __name__ == "__main__":
     main(int(sys.argv[1]) if len(sys.argv) > 1 else 24)
     batched(8)
+    with_lines(6)
