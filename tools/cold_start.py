@@ -33,7 +33,8 @@ def main():
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     ct, init = pin(batch.const_table), pin(batch.initial)
     mode = sys.argv[5] if len(sys.argv) > 5 else "sync"
-    os.environ["EMTB200_CACHE"] = tempfile.mkdtemp()
+    cache = tempfile.TemporaryDirectory()  # empty on-disk cubin cache, removed at exit
+    os.environ["EMTB200_CACHE"] = cache.name
     out = torch.empty((S, len(info.channels) * batch.width), dtype=torch.float64, pin_memory=True).numpy()
     t0 = time.perf_counter()
     eng = engine.Engine(batch.schedule, init, const_table=ct, width=batch.width, device=dev, async_jit=mode == "async")
@@ -47,7 +48,9 @@ def main():
     import hashlib
     res = {"mode": mode, "total_s": t2 - t0, "create_s": t1 - t0, "run_s": t2 - t1, "jit_s": jit,
            "kernel_during_run": ran[:90], "digest": hashlib.sha1(out.tobytes()).hexdigest()}
+    eng.close()
     print(json.dumps(res))
+    cache.cleanup()
 
 
 if __name__ == "__main__":
