@@ -137,6 +137,27 @@ emt_status emt_interpret(const char* schedule_text, const double* initial, int64
                          int32_t steps, const emt_exec_options* options, const emt_config* cfg,
                          double* waves, double* time, emt_exec_stats* stats);
 
+/* ---- multi-device executor (SURVEY §8(b) emt_create / emt_run) ----------- */
+
+/* One engine over `ndev` devices: the batch's `width` lanes are split into
+ * contiguous shards, one lane-shard engine per listed device (a device may be
+ * listed twice), all run concurrently from the calling thread. `initial` holds
+ * extent*width doubles (the reference arena); the schedule text carries the
+ * batch's constant table. The engine is confined to one host thread at a time. */
+typedef struct emt_multi emt_multi;
+typedef emt_exec_stats emt_stats;
+emt_status emt_create(const char* cgmsched_text, const double* initial, int64_t extent, int32_t width,
+                      const int32_t* devices, int32_t ndev, emt_multi** out);
+/* `steps` passes from the initial arena (`warmup` of them outside measured_seconds);
+ * waves: steps x (channels * width), the WaveformSet row layout (may be NULL).
+ * factor_count counts a pass once when any lane refactorises (exec.cpp:200-201);
+ * measured_seconds is the slowest device's. On error the lowest-lane shard that
+ * failed reports. */
+emt_status emt_run(emt_multi* engine, int32_t steps, int32_t warmup, double* waves, emt_stats* out);
+/* "<where>: <message>" of the engine's last failing call. */
+const char* emt_error_detail(const emt_multi* engine);
+void emt_destroy(emt_multi* engine);
+
 /* Thread-local detail of the last failing call on this thread. */
 const char* emt_last_error(void);
 

@@ -24,6 +24,7 @@
 #include <cstring>
 #include <future>
 #include <memory>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -1870,6 +1871,122 @@ emt_status emt_engine_read_refactor_steps(emt_engine* e, int32_t* steps, int32_t
     if (count) *count = n;
     return EMT_OK;
 }
+
+// ---- multi-device engine: the executor call of SURVEY §8(b) (emt_create / emt_run)
+// over one lane-shard engine per listed device, run concurrently from one host thread.
+struct emt_multi {
+    std::vector<emt_engine*> shards;
+    std::vector<int> lo, hi;  // lane range of each shard
+    int width = 1, channels = 0;
+    std::string detail;
+    ~emt_multi() {
+        for (emt_engine* e : shards) emt_engine_destroy(e);
+    }
+};
+
+emt_status emt_create(const char* cgmsched_text, const double* initial, int64_t extent, int32_t width,
+                      const int32_t* devices, int32_t ndev, emt_multi** out) {
+    if (out == nullptr || cgmsched_text == nullptr || initial == nullptr)
+        return set_error(EMT_INVALID_HANDLE, "null argument");
+    *out = nullptr;
+    if (width < 1 || extent < 0) return set_error(EMT_NON_POSITIVE_INPUT, "width must be >= 1");
+    const int n = std::max(1, std::min<int>(ndev > 0 ? ndev : 1, width));
+    auto m = std::make_unique<emt_multi>();
+    m->width = width;
+    for (int d = 0; d < n; ++d) {  // contiguous lane shards (sharding.shard_bounds)
+        const int lo = static_cast<int>(static_cast<long long>(width) * d / n);
+        const int hi = static_cast<int>(static_cast<long long>(width) * (d + 1) / n);
+        emt_config c{};
+        c.device = devices != nullptr && ndev > 0 ? devices[d] : 0;
+        c.lane_begin = lo;
+        c.lane_count = hi - lo;
+        emt_engine* e = nullptr;
+        EMT_TRY(emt_engine_create(cgmsched_text, nullptr, width, initial, extent * width, &c, &e));
+        m->shards.push_back(e);
+        m->lo.push_back(lo);
+        m->hi.push_back(hi);
+    }
+    m->channels = static_cast<int>(m->shards[0]->sched.channel_slot.size());
+    *out = m.release();
+    return EMT_OK;
+}
+
+emt_status emt_run(emt_multi* m, int32_t steps, int32_t warmup, double* waves, emt_exec_stats* stats) {
+    if (m == nullptr) return set_error(EMT_INVALID_HANDLE, "null engine");
+    if (steps < 0) return set_error(EMT_NON_POSITIVE_INPUT, "negative step count");
+    const int warm = std::max(0, std::min(warmup, steps));
+    struct Ev {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int dev = 0;
+        ~Ev() {
+            cudaSetDevice(dev);
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    };
+    std::vector<Ev> ev(m->shards.size());
+    auto fail = [m](emt_status st) {
+        m->detail = g_last_error;
+        return st;
+    };
+    for (size_t k = 0; k < m->shards.size(); ++k) {  // enqueue every shard, then wait
+        emt_engine* e = m->shards[k];
+        ev[k].dev = e->device;
+        if (emt_status st = emt_engine_reserve(e, steps)) return fail(st);
+        CUDA_TRY(cudaSetDevice(e->device));
+        CUDA_TRY(cudaEventCreate(&ev[k].a));
+        CUDA_TRY(cudaEventCreate(&ev[k].b));
+        if (emt_status st = emt_engine_advance(e, warm, 0)) return fail(st);
+        CUDA_TRY(cudaEventRecord(ev[k].a, e->stream));
+        if (emt_status st = emt_engine_advance(e, steps - warm, 0)) return fail(st);
+        CUDA_TRY(cudaEventRecord(ev[k].b, e->stream));
+    }
+    // the first shard (lowest lanes) that failed reports, as the reference reports its lowest lane
+    for (emt_engine* e : m->shards)
+        if (emt_status st = emt_engine_sync(e)) return fail(st);
+    float worst = 0.f;
+    std::set<int> refac;
+    emt_exec_stats sum{};
+    std::vector<double> rows;
+    for (size_t k = 0; k < m->shards.size(); ++k) {
+        emt_engine* e = m->shards[k];
+        float ms = 0.f;
+        CUDA_TRY(cudaSetDevice(e->device));
+        cudaEventElapsedTime(&ms, ev[k].a, ev[k].b);
+        worst = std::max(worst, ms);
+        if (waves != nullptr && steps > 0) {  // shard rows (rows x channels x W) into the batch layout
+            const int W = m->hi[k] - m->lo[k];
+            rows.resize(static_cast<size_t>(steps) * m->channels * W);
+            if (emt_status st = emt_engine_read_waves(e, 0, steps, rows.data(), nullptr)) return fail(st);
+            for (int r = 0; r < steps; ++r)
+                for (int c = 0; c < m->channels; ++c)
+                    std::memcpy(waves + (static_cast<size_t>(r) * m->channels + c) * m->width + m->lo[k],
+                                rows.data() + (static_cast<size_t>(r) * m->channels + c) * W, sizeof(double) * W);
+        }
+        std::vector<int32_t> rs(static_cast<size_t>(std::max(1, steps)));
+        int32_t cnt = 0;
+        if (emt_status st = emt_engine_read_refactor_steps(e, rs.data(), static_cast<int32_t>(rs.size()), &cnt)) return fail(st);
+        for (int q = 0; q < std::min<int>(cnt, static_cast<int>(rs.size())); ++q) refac.insert(rs[static_cast<size_t>(q)]);
+        emt_exec_stats st{};
+        if (emt_status s2 = emt_engine_stats(e, &st)) return fail(s2);
+        sum.kernel_launches += st.kernel_launches;
+        sum.switch_events += st.switch_events;
+        if (k == 0) sum.factor_count = st.factor_count - static_cast<int>(refac.size());  // the base count
+    }
+    if (stats) {
+        // a refactorisation pass of ANY lane counts once (exec.cpp:200-201): the union over shards
+        stats->factor_count = sum.factor_count + static_cast<int>(refac.size());
+        stats->measured_steps = steps - warm;
+        stats->measured_seconds = static_cast<double>(worst) * 1e-3;  // slowest device
+        stats->kernel_launches = sum.kernel_launches;
+        stats->switch_events = sum.switch_events;
+    }
+    return EMT_OK;
+}
+
+const char* emt_error_detail(const emt_multi* m) { return m ? m->detail.c_str() : ""; }
+
+void emt_destroy(emt_multi* m) { delete m; }
 
 int32_t emt_engine_kernel(const emt_engine* e) { return e ? e->kernel_mode : 0; }
 

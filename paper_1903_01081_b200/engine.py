@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes
 import os
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -97,6 +97,12 @@ def lib():
         L.emt_interpret.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32,
                                     ctypes.POINTER(_Options), ctypes.POINTER(_Config), dp, dp,
                                     ctypes.POINTER(_Stats)]
+        L.emt_create.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32,
+                                 ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.POINTER(vp)]
+        L.emt_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp, ctypes.POINTER(_Stats)]
+        L.emt_error_detail.argtypes = [vp]
+        L.emt_error_detail.restype = ctypes.c_char_p
+        L.emt_destroy.argtypes = [vp]
         L.emt_engine_create.argtypes = [ctypes.c_char_p, dp, ctypes.c_int32, dp, ctypes.c_int64,
                                         ctypes.POINTER(_Config), ctypes.POINTER(vp)]
         L.emt_engine_destroy.argtypes = [vp]
@@ -192,6 +198,14 @@ def channel_names(schedule: str) -> List[str]:
     return [ln.split()[1] for ln in schedule.splitlines() if ln.startswith("CHANNEL ")]
 
 
+def schedule_dt(schedule: str) -> float:
+    """dt of the META record (%.17g, so the parsed double is the reference's)."""
+    for ln in schedule.splitlines():
+        if ln.startswith("META "):
+            return float(next(f for f in ln.split() if f.startswith("dt=")).split("=")[1])
+    raise ValueError("schedule has no META record")
+
+
 def schedule_width(schedule: str) -> int:
     head = schedule.split("\n", 1)[0].split()
     return int(next(t for t in head if t.startswith("width=")).split("=")[1])
@@ -285,6 +299,31 @@ def codegen(schedule: str, const_table: Optional[np.ndarray] = None, width: int 
     _check(L.emt_codegen(schedule.encode(), _dp(ct) if ct is not None else None, int(width), int(warps),
                          1 if compile else 0, arch.encode(), ctypes.byref(src), ctypes.byref(summ)))
     return src.value.decode(), summ.value.decode()
+
+
+def run_devices(schedule: str, initial: np.ndarray, steps: int, devices: Sequence[int] = (0,), warmup: int = 0):
+    """The multi-device executor (emt_create / emt_run): the batch's lanes in
+    contiguous shards over `devices`, run concurrently; returns (WaveformSet, ExecStats)."""
+    L = lib()
+    init = np.ascontiguousarray(initial, dtype=np.float64)
+    width = schedule_width(schedule)
+    extent = init.size // width
+    h = ctypes.c_void_p()
+    devs = (ctypes.c_int32 * len(devices))(*devices)
+    _check(L.emt_create(schedule.encode(), _dp(init), extent, width, devs, len(devices), ctypes.byref(h)))
+    try:
+        nch = len(channel_names(schedule))
+        waves = np.zeros((steps, nch * width))
+        st = _Stats()
+        rc = L.emt_run(h, steps, warmup, _dp(waves), ctypes.byref(st))
+        if rc != 0:
+            raise EmtError(rc, L.emt_error_detail(h).decode(errors="replace"))
+    finally:
+        L.emt_destroy(h)
+    dt = schedule_dt(schedule)
+    time = (np.arange(steps, dtype=np.float64) + 1.0) * dt
+    return (WaveformSet(channel_names(schedule), width, time, waves),
+            ExecStats(st.factor_count, st.measured_seconds, st.measured_steps, st.kernel_launches, st.switch_events))
 
 
 def interpret(schedule: str, initial: np.ndarray, steps: int, options: Optional[ExecOptions] = None,

@@ -352,3 +352,23 @@ def test_async_jit_engine_closed_while_compiling_and_serving_paths(tmp_path, mon
     assert e.kernel == engine.KERNEL_SPECIALISED
     for out in outs:
         assert bitwise_equal(out, want)
+
+
+@pytest.mark.parametrize("name,devices", [("ieee39_n1_w8", (0, 0, 0)), ("feeder_w4", (0, 0)), ("switched_dc_w3", (0,))])
+def test_multi_device_executor_equals_interpret(name, devices):
+    """emt_create / emt_run: lane shards over the listed devices (one
+    device listed several times here), waves in the batch layout and the batch's
+    factor_count (a pass counts once when any lane refactorises), bitwise."""
+    g = load_golden(name)
+    w, st = engine.run_devices(g.schedule, g.initial, g.steps, devices=devices, warmup=10)
+    assert bitwise_equal(w.values, g.waves)
+    assert bitwise_equal(w.time, g.time)
+    assert st.factor_count == g.factor_count
+    assert st.measured_steps == g.steps - 10
+
+
+def test_multi_device_executor_reports_errors():
+    g = load_golden("singular_islands")
+    with pytest.raises(engine.EmtError) as ei:
+        engine.run_devices(g.schedule, g.initial, g.steps, devices=(0, 0))
+    assert ei.value.status == g.error_code
