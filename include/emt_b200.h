@@ -158,6 +158,12 @@ emt_status emt_run(emt_multi* engine, int32_t steps, int32_t warmup, double* wav
 const char* emt_error_detail(const emt_multi* engine);
 void emt_destroy(emt_multi* engine);
 
+/* Twin of execute_parallel (proj/include/emtgrid/exec.hpp:35-37): the same
+ * results as emt_interpret; workers < 1 fails with NonPositiveInput as there. */
+emt_status emt_execute_parallel(const char* schedule_text, const double* initial, int64_t initial_len,
+                                int32_t workers, int32_t steps, const emt_exec_options* options,
+                                const emt_config* cfg, double* waves, double* time, emt_exec_stats* stats);
+
 /* Thread-local detail of the last failing call on this thread. */
 const char* emt_last_error(void);
 

@@ -2022,6 +2022,15 @@ emt_status emt_interpret(const char* schedule_text, const double* initial, int64
     }
 }
 
+emt_status emt_execute_parallel(const char* schedule_text, const double* initial, int64_t initial_len,
+                                int32_t workers, int32_t steps, const emt_exec_options* options,
+                                const emt_config* cfg, double* waves, double* time, emt_exec_stats* stats) {
+    // execute_parallel (proj/src/exec.cpp:385-389): same contract and results as
+    // interpret; the worker count is validated as there, the device does the work
+    if (workers < 1) return set_error(EMT_NON_POSITIVE_INPUT, "worker count must be at least 1");
+    return emt_interpret(schedule_text, initial, initial_len, steps, options, cfg, waves, time, stats);
+}
+
 static emt_status interpret_retry(const char* schedule_text, const double* initial, int64_t initial_len,
                                   int32_t steps, const emt_exec_options* options, const emt_config* cfg,
                                   double* waves, double* time, emt_exec_stats* stats) {

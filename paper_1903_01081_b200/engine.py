@@ -97,6 +97,9 @@ def lib():
         L.emt_interpret.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32,
                                     ctypes.POINTER(_Options), ctypes.POINTER(_Config), dp, dp,
                                     ctypes.POINTER(_Stats)]
+        L.emt_execute_parallel.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(_Options), ctypes.POINTER(_Config), dp, dp,
+                                           ctypes.POINTER(_Stats)]
         L.emt_create.argtypes = [ctypes.c_char_p, dp, ctypes.c_int64, ctypes.c_int32,
                                  ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, ctypes.POINTER(vp)]
         L.emt_run.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, dp, ctypes.POINTER(_Stats)]

@@ -92,3 +92,19 @@ def test_environment_knobs_are_inert_in_product_build(monkeypatch):
     src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=8, compile=False)
     assert src == base_src
     assert "knobs=" not in summary and "devbuild" not in summary
+
+
+def test_execute_parallel_rejects_nonpositive_workers_without_a_gpu():
+    """emt_execute_parallel validates the worker count before any device work, as
+    execute_parallel does (proj/src/exec.cpp:387-389)."""
+    import ctypes
+    import numpy as np
+    from conftest import load_golden
+    from paper_1903_01081_b200 import engine
+    L = engine.lib()
+    g = load_golden("rc_discharge")
+    init = np.ascontiguousarray(g.initial)
+    rc = L.emt_execute_parallel(g.schedule.encode(), init.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), init.size,
+                                0, 10, None, None, None, None, None)
+    assert rc == 1 + 19  # 1 + ErrorCode::NonPositiveInput (common.hpp:11-33)
+    assert b"worker count" in L.emt_last_error()

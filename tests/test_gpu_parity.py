@@ -372,3 +372,21 @@ def test_multi_device_executor_reports_errors():
     with pytest.raises(engine.EmtError) as ei:
         engine.run_devices(g.schedule, g.initial, g.steps, devices=(0, 0))
     assert ei.value.status == g.error_code
+
+
+def test_execute_parallel_twin_equals_golden():
+    """emt_execute_parallel: execute_parallel's contract (the reference's layer-parallel
+    executor is bit-identical to interpret, exec.cpp:385); the device runs it."""
+    import ctypes
+    g = load_golden("ieee39_n1_w8")
+    L = engine.lib()
+    init = np.ascontiguousarray(g.initial)
+    nch = len(engine.channel_names(g.schedule))
+    waves = np.zeros((g.steps, nch * g.width))
+    time = np.zeros(g.steps)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = L.emt_execute_parallel(g.schedule.encode(), init.ctypes.data_as(dp), init.size, 4, g.steps, None, None,
+                                waves.ctypes.data_as(dp), time.ctypes.data_as(dp), None)
+    assert rc == 0, L.emt_last_error()
+    assert bitwise_equal(waves, g.waves)
+    assert bitwise_equal(time, g.time)
