@@ -849,6 +849,17 @@ emt_status build_system_plan(emt_engine* e) {
         if (mask[static_cast<size_t>(r)] == 0u) kin[static_cast<size_t>(r)] = ke;
         blk[static_cast<size_t>(b)] |= mask[static_cast<size_t>(r)];
     }
+    // shared memory left for a forward round's products once everything else is laid
+    // out (below): bigger rounds mean fewer round barriers per forward block
+    int dev_smem_q = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem_q, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
+    int max_u_off = 1;
+    for (int r = 0; r < dim; ++r)
+        max_u_off = std::max(max_u_off, s.u_row_ptr[static_cast<size_t>(r) + 1] - s.u_row_ptr[static_cast<size_t>(r)] - 1);
+    const long long fixed = static_cast<long long>(kSysRing) * kSysChunk * 12 + 8 * kSysRing + 16 + 2 * 4 * 8 +
+                            2LL * (max_u_off + 8) * 8 + 32 * 33 * 8 + 8LL * std::max(1, dim) + 1024;
+    const int fcap = static_cast<int>(std::max(1024LL, std::min(16384LL, (dev_smem_q - fixed) / 8 / 1024 * 1024)));
+    S.fcap = fcap;
     // forward rounds: each block's trailing segments (one row's terms in the block's
     // columns, <= 32) packed into rounds whose products fit the shared buffer in a
     // transposed layout: term j of the round's piece p sits at j * P' + p (P' = pieces
@@ -864,7 +875,7 @@ emt_status build_system_plan(emt_engine* e) {
             while (i1 < sv.size()) {
                 const int len = sv[i1].z - sv[i1].y;
                 const int np = (static_cast<int>(i1 - i0) + 1) | 1;
-                if (i1 > i0 && np * std::max(maxlen, len) > kSysFcap) break;
+                if (i1 > i0 && np * std::max(maxlen, len) > fcap) break;
                 maxlen = std::max(maxlen, len);
                 ++i1;
             }
@@ -971,7 +982,7 @@ emt_status build_system_plan(emt_engine* e) {
     S.pmax += 8;  // room for the zero padding to a multiple of eight terms
     off += 2 * static_cast<size_t>(S.pmax) * sizeof(double);
     S.smem_fp = static_cast<int>(off);
-    off += static_cast<size_t>(kSysFcap) * sizeof(double);
+    off += static_cast<size_t>(S.fcap) * sizeof(double);
     S.smem_tile = static_cast<int>(off);
     off += 32 * 33 * sizeof(double);
     S.smem_xs = static_cast<int>(off);
@@ -1158,7 +1169,7 @@ static emt_status engine_create(const char* schedule_text, const double* const_t
         e->kernel_mode = EMT_KERNEL_SYSTEM;
         e->summary = "system kernel: one " + std::to_string(kSysThreads) + "-thread CTA per lane, grid=" +
                      std::to_string(e->W) + " fwd_blocks=" + std::to_string(e->sys.nblk) +
-                     " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " smem=" + std::to_string(e->sys_smem);
+                     " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " fcap=" + std::to_string(e->sys.fcap) + " smem=" + std::to_string(e->sys_smem);
         *out = e.release();
         return EMT_OK;
     }
@@ -1288,7 +1299,7 @@ static emt_status engine_create(const char* schedule_text, const double* const_t
             e->kernel_mode = EMT_KERNEL_SYSTEM;
             e->summary = "system kernel: one " + std::to_string(kSysThreads) + "-thread CTA per lane, grid=" +
                          std::to_string(e->W) + " fwd_blocks=" + std::to_string(e->sys.nblk) +
-                         " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " smem=" + std::to_string(e->sys_smem) +
+                         " stream_chunks=" + std::to_string(e->sys.stream_chunks) + " fcap=" + std::to_string(e->sys.fcap) + " smem=" + std::to_string(e->sys_smem) +
                          " (specialised kernel unavailable: " + (gf.message.empty() ? log.substr(0, 300) : gf.message) + ")";
         } else {
             e->summary += " (specialised kernel unavailable: " + (gf.message.empty() ? log.substr(0, 300) : gf.message) + ")";

@@ -35,7 +35,6 @@ constexpr int kSysThreads = 1024;
 constexpr int kSysChunkLog = 10;
 constexpr int kSysChunk = 1 << kSysChunkLog;  // backward-stream entries per TMA bulk copy
 constexpr int kSysRing = 4;      // chunks in flight
-constexpr int kSysFcap = 4096;   // forward-round products staged in shared memory
 
 struct SysPlan {
     int nblk;                // forward column blocks of 32
@@ -43,7 +42,7 @@ struct SysPlan {
     const unsigned* fwd_mask;  // dim: bit c = row r has an L entry in column 32*(r/32)+c
     const unsigned* blk_cols;  // nblk: OR of the block's row masks
     const int* rnd_ptr;      // nblk+1: rounds of each block's trailing update
-    const int4* rnd;         // (entry begin, entry end, piece begin, piece end): <= kSysFcap entries per round
+    const int4* rnd;         // (entry begin, entry end, piece begin, piece end): <= fcap entries per round
     const int4* piece;       // (row, p, count, P'): a row's terms of one round, ascending column, at fp[j * P' + p]
     const int* fsrc;         // forward stream: L index of each entry (block, then row, then column order)
     const int* fcol;         //                 its column
@@ -70,7 +69,8 @@ struct SysPlan {
     int smem_flags;          // frontier + two row-ready words (backward producer / consumer)
     int smem_desc;           // [2][4] u_{r,r+1}, diagonal, reciprocal
     int smem_pbuf;           // [2][pmax] products of the rows in flight
-    int smem_fp;             // [kSysFcap] products of a forward round
+    int smem_fp;             // [fcap] products of a forward round
+    int fcap;                // forward-round capacity (the shared memory left, 1024..16384 entries)
     int pmax;                // longest U row past the diagonal
     long long* prof;         // developer phase profile (EMTB200_CG_PROF=1): cycles per phase, else null
 };
