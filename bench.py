@@ -206,6 +206,20 @@ def dist_env():
     return rank, world, local
 
 
+def bench_config(args, W, per_gpu, world, info):
+    """The workload description both arms print (`config`): identical for the device arm
+    and the reference arm, so the two lines describe the same workload."""
+    return {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": per_gpu,
+            "emt_steps_per_bench_step": args.emt_steps if args.impl == "ours" else
+            (args.cpu_emt_steps_per_step or args.emt_steps),
+            "dt": info.dt, "nodes": info.nodes, "components": info.comps, "case": WORKLOADS[args.workload][1],
+            "parallelism": (f"{W} line-coupled copies split over {world} GPU(s)" if args.workload == "c4"
+                            else f"one k={args.scenarios} system per GPU (replicas only: the shared root "
+                                 "node couples every copy into one LU)" if args.workload == "scale"
+                            else f"{W} scenario lanes in contiguous shards over {world} GPU(s), no per-step traffic"),
+            "l2": "flushed (256 MiB write) between timed launches"}
+
+
 def flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
@@ -431,14 +445,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": wl_name, "scenarios": W, "scenarios_per_gpu": hi - lo,
-                       "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
-                       "components": info.comps, "case": WORKLOADS[args.workload][1],
-                       "parallelism": (f"{W} line-coupled copies split over {world} GPU(s)" if args.workload == "c4"
-                                       else f"one k={args.scenarios} system per GPU (replicas only: the shared root "
-                                            "node couples every copy into one LU)" if args.workload == "scale"
-                                       else f"{W} scenario lanes in contiguous shards over {world} GPU(s), no per-step traffic"),
-                       "l2": "flushed (256 MiB write) between timed launches"},
+            "config": bench_config(args, W, hi - lo, world, info),
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "matches_device_run": e2e_digest_ok,
                     "note": "per step: the batch's H2D from pinned host (Engine.stage, overlapping the previous "
@@ -583,10 +590,7 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": hib,
         "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.workload][0], "scenarios": W, "scenarios_per_gpu": W // world,
-                   "emt_steps_per_bench_step": S, "dt": info.dt, "nodes": info.nodes,
-                   "components": info.comps, "case": WORKLOADS[args.workload][1],
-                   "parallelism": f"{procs} host processes over contiguous lane shards"},
+        "config": bench_config(args, W, W // world if args.workload not in ("scale",) else W, world, info),
         "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": kind,
                          "sample": f"{W} {'copies' if kind == 'port' else 'scenarios'} x {S} EMT steps per bench "
                                    f"step ({args.warmup} warm-up + {args.steps} timed, the passes our arm times), "
