@@ -2048,7 +2048,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     o << "struct KArgs { double* arena; const double* ctab; double* waves; unsigned char* refac; int* lane_err;\n"
       << "  int* events; int* n_events; int max_events; int step0; int nsteps; int row0; double div_limit;\n"
       << "  double* ring; long long ring_lo; long long ring_cols; unsigned int* progress; int min_k; int nblocks; long long* prof; const double* srctab;\n"
-      << "  int prog_off; int sys_scope; };\n";
+      << "  int prog_off; int sys_scope; int* pick; };\n";
     auto carr_i = [&](const char* qual, const char* name, const std::vector<int>& v) {
         o << qual << " int " << name << "[" << std::max<size_t>(1, v.size()) << "] = {";
         for (size_t q = 0; q < v.size(); ++q) o << (q ? "," : "") << v[q];
@@ -2100,10 +2100,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // warps reach their phase barriers at different instructions: the non-.aligned
     // barrier form is the one the PTX ISA allows there (compute-sanitizer synccheck clean)
     o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
-    o << "#define PROF(id) do { if (a.prof && blockIdx.x == 0 && lane == 0) { const long long c_ = clock64(); "
+    o << "#define PROF(id) do { if (a.prof && BID_ == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
-    o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + a.prog_off + blockIdx.x, 0x3fffffffu); } while (0)\n";
+    o << "#define FAILPUB() do { if (a.progress != nullptr && threadIdx.x == 0) atomicExch(a.progress + a.prog_off + BID_, 0x3fffffffu); } while (0)\n";
     o << "#define LD(o) (*(const double*)(Sb + (o)))\n"
       << "#define ST(o, v) (*(double*)(Sb + (o)) = (v))\n"
       << "#define SGN(x, n) ((n) ? -(x) : (x))\n";
@@ -2116,6 +2116,46 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     else
         o << "#define LU(x) (A[(size_t)(x) * W_])\n";
 
+    // Full-chip launch (a.pick != null, engine.cu: setup_claim): the engine launches
+    // one CTA per SM and the CTA on SM s < groups takes lane group s. A launch of
+    // fewer CTAs than SMs runs up to 13% slower on some B200s (an issue throttle of
+    // low-grid launches), and lane groups spread over more TPCs than SMs 0..n-1 run
+    // slower still (profiles/ab/placement_r2.log). Correct whatever the placement:
+    // a group is taken by compare-and-swap on its flag (a.pick[1 + g]); a CTA that
+    // gets none (a spare SM, or its SM's group already taken) waits until every CTA
+    // of the launch has started -- or 20 us have passed, e.g. while another kernel
+    // holds SMs -- and then takes any group still free. Spares >= free groups, since
+    // the grid is >= the group count.
+    const std::string NG = "((W_ + " + std::to_string(LPC) + " - 1) / " + std::to_string(LPC) + ")";
+    const std::string bid_code =
+        "  int BID_ = blockIdx.x;\n"
+        "  if (a.pick != nullptr) {\n"
+        "    __shared__ int s_bid_;\n"
+        "    if (threadIdx.x == 0) {\n"
+        "      unsigned smid_; asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid_));\n"
+        "      int b_ = -1;\n"
+        "      if ((long long)smid_ < " + NG + " && atomicCAS(a.pick + 1 + smid_, 0, 1) == 0) b_ = (int)smid_;\n"
+        "      __threadfence();\n"
+        "      atomicAdd(a.pick, 1);\n"
+        "      if (b_ < 0) {\n"
+        "        unsigned long long t0_, t_;\n"
+        "        asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t0_));\n"
+        "        for (;;) {\n"
+        "          if (*(volatile int*)a.pick >= (int)gridDim.x) break;\n"
+        "          asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_));\n"
+        "          if (t_ - t0_ > 20000ull) break;\n"
+        "          __nanosleep(100);\n"
+        "        }\n"
+        "        __threadfence();\n"
+        "        for (int g_ = 0; g_ < " + NG + " && b_ < 0; ++g_)\n"
+        "          if (*(volatile int*)(a.pick + 1 + g_) == 0 && atomicCAS(a.pick + 1 + g_, 0, 1) == 0) b_ = g_;\n"
+        "      }\n"
+        "      s_bid_ = b_;\n"
+        "    }\n"
+        "    __syncthreads();\n"
+        "    BID_ = s_bid_;\n"
+        "    if (BID_ < 0) return;\n"
+        "  }\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * G << ", 1) emt_cg_kernel(const KArgs a) {\n"
       << "  extern __shared__ double sm[];\n"
       << "  const int lane = threadIdx.x & 31; const int warp = threadIdx.x >> 5;\n"
@@ -2125,7 +2165,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
                                              "; q += blockDim.x) sm[q] = __longlong_as_double(0x7ff4000000000badLL);\n  __syncthreads();\n"
                                        : std::string())
       << "  const int slane = lane < " << LPC << " ? lane : 0;  // shadow threads mirror lane 0\n"
-      << "  const int graw = blockIdx.x * " << LPC << " + slane; const bool live = lane < " << LPC << " && graw < W_;\n"
+      << bid_code
+      << "  const int graw = BID_ * " << LPC << " + slane; const bool live = lane < " << LPC << " && graw < W_;\n"
       << "  const int gl = graw < W_ ? graw : (int)(W_ - 1);\n"
       << "  double* __restrict__ S = sm + slane;\n"
       << "  char* __restrict__ Sb = (char*)S;\n"
@@ -2189,7 +2230,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     if (g.lu_shared) {
         // the factors of the CTA's first lane (every lane holds the same); reciprocals
         // from the same arena values
-        const std::string base = "(size_t)blockIdx.x * " + std::to_string(LPC);
+        const std::string base = "(size_t)BID_ * " + std::to_string(LPC);
         std::vector<std::pair<std::string, std::string>> it;
         const size_t nl = s.l_col.size(), nu = s.u_col.size();
         for (size_t q = 0; q < nl; ++q)
@@ -2264,9 +2305,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // thread's store in causality order). Releasing right after region A (C4 3.35 ->
     // 4.60 us) or one pass late (neutral) measured no better; not kept.
     auto rel_stmt = [](const std::string& val) {
-        return std::string("      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(") +
+        return std::string("      if (a.sys_scope) { __threadfence_system(); asm volatile(\"st.release.sys.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + BID_), \"r\"((unsigned int)(") +
                val + ")) : \"memory\"); }\n" +
-               "      else asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + blockIdx.x), \"r\"((unsigned int)(" +
+               "      else asm volatile(\"st.release.gpu.global.u32 [%0], %1;\" :: \"l\"(a.progress + a.prog_off + BID_), \"r\"((unsigned int)(" +
                val + ")) : \"memory\");\n";
     };
     // the release waits for the CTA's outstanding stores: issue it from the warp with

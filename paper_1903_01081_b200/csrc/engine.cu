@@ -74,6 +74,7 @@ struct CgArgs {
     const double* srctab;    // this launch's AC source values [pass][source] (emt_src_kernel)
     int prog_off;            // this engine's first CTA in the (possibly shared) progress array
     int sys_scope;           // 1: peers on other GPUs (system-scope acquire/release, uncached ring reads)
+    int* pick;               // full-chip launch: lane-group claim counter (else null, see launch_ctas)
 };
 
 struct DevPlan {
@@ -556,6 +557,9 @@ struct emt_engine {
     int base_factor_count = 0;           // global lane 0's initial fcount (ExecStats, exec.cpp:376)
 
     std::unique_ptr<PendingJit> pending;  // async JIT in flight (EMT_FLAG_ASYNC_JIT)
+    int claim_grid = 0;                   // full-chip launch of the specialised kernel: CTAs (= SMs), else 0
+    size_t claim_smem = 0;                // its dynamic shared memory (forces one CTA per SM)
+    int* d_pick = nullptr;                // [0] CTAs started, [1 + g] lane group g taken (codegen.cpp bid_code)
     int switched_at = -1;                 // pass at which the engine moved to the specialised kernel
 
     ~emt_engine() {
@@ -569,6 +573,7 @@ struct emt_engine {
         if (d_prof) cudaFree(d_prof);
         if (d_srctab) cudaFree(d_srctab);
         if (d_waves) cudaFree(d_waves);
+        if (d_pick) cudaFree(d_pick);
         if (d_refactored) cudaFree(d_refactored);
         for (cudaEvent_t ev : chunk_done) cudaEventDestroy(ev);
         if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -1006,6 +1011,33 @@ emt_status build_system_plan(emt_engine* e) {
     return EMT_OK;
 }
 
+/// Full-chip launch of the specialised kernel (generated prologue: `bid_code`,
+/// codegen.cpp): one CTA per SM, the CTAs on SMs 0..groups-1 claim the lane groups.
+/// A launch of fewer CTAs than SMs runs up to 13% slower on some B200s, the same
+/// groups spread over more TPCs slower still (profiles/ab/placement_r2.log). Needs one
+/// CTA per SM (the dynamic shared memory is raised above half an SM's when smaller)
+/// and at most one lane group per SM; otherwise, and for engines whose progress words
+/// are shared with peer engines (emt_engine_attach_lines), the launch stays one CTA
+/// per group.
+void setup_claim(emt_engine* e) {
+    e->claim_grid = 0;
+    if (e->kernel_mode != EMT_KERNEL_SPECIALISED || dev_env("EMTB200_NOCLAIM")) return;
+    int sms = 0, per_sm = 0, optin = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device) != cudaSuccess)
+        return;
+    if (cta_count(e) > sms) return;
+    const size_t need = std::max<size_t>(e->gen.smem_bytes, static_cast<size_t>(per_sm) / 2 + 1024);
+    if (need > static_cast<size_t>(optin)) return;
+    if (driver()->FuncSetAttribute(e->jit.function, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                                   static_cast<int>(need)) != CUDA_SUCCESS)
+        return;
+    if (e->d_pick == nullptr && cudaMalloc(&e->d_pick, sizeof(int) * (1 + static_cast<size_t>(sms))) != cudaSuccess) return;
+    e->claim_grid = sms;
+    e->claim_smem = need;
+}
+
 /// Adopts the asynchronously compiled specialised kernel once it is ready (or, with
 /// `block`, waits for it). Launches stay stream-ordered, so switching between two
 /// launches needs no synchronisation; both kernels produce the same bits.
@@ -1025,6 +1057,8 @@ void adopt_pending(emt_engine* e, bool block) {
         std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s (async JIT: generic kernel for passes 0..%d)", p.gen_s,
                       e->jit.compile_seconds, e->jit.cached ? " (cached)" : "", e->step - 1);
         e->summary = "specialised kernel: " + e->gen.summary + b;
+        setup_claim(e);
+        if (e->claim_grid > 0) e->summary += " launch=full-chip(" + std::to_string(e->claim_grid) + ")";
     } else {
         e->summary += " (specialised kernel unavailable: " + (p.fail.message.empty() ? p.log.substr(0, 300) : p.fail.message) + ")";
     }
@@ -1291,6 +1325,8 @@ static emt_status engine_create(const char* schedule_text, const double* const_t
             std::snprintf(b, sizeof b, " codegen=%.3fs jit=%.3fs%s", gen_s, e->jit.compile_seconds,
                           e->jit.cached ? " (cached)" : "");
             e->summary = "specialised kernel: " + e->gen.summary + b;
+            setup_claim(e.get());
+            if (e->claim_grid > 0) e->summary += " launch=full-chip(" + std::to_string(e->claim_grid) + ")";
         } else if (c.kernel == EMT_KERNEL_SPECIALISED) {
             return set_error(gf.code ? gf.code : EMT_CUDA_ERROR,
                              "specialised kernel unavailable: " + (gf.message.empty() ? log : gf.message));
@@ -1381,7 +1417,7 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
                  e->plan.ring, e->plan.ring_lo, e->plan.ring_cols,
                  e->persistent_lines ? e->d_progress : nullptr, e->min_k,
                  e->prog_total > 0 ? e->prog_total : static_cast<int>(cta_count(e)), e->d_prof, e->d_srctab,
-                 e->prog_off, e->sys_scope};
+                 e->prog_off, e->sys_scope, nullptr};
         if (e->gen.nsrc > 0 && e->jit.function2 != nullptr) {  // the launch's source value table first
             const size_t need = static_cast<size_t>(steps) * e->gen.nsrc;
             if (need > e->srctab_cap) {
@@ -1402,10 +1438,16 @@ emt_status emt_engine_advance(emt_engine* e, int32_t steps, int32_t sync) {
         }
         void* params[] = {&a};
         const bool ts = e->kernel_mode == EMT_KERNEL_TSIMT;
-        const unsigned grid = static_cast<unsigned>(ts ? e->W : cta_count(e));
+        unsigned grid = static_cast<unsigned>(ts ? e->W : cta_count(e));
+        unsigned smem = static_cast<unsigned>(e->gen.smem_bytes);
+        if (!ts && e->claim_grid > 0 && e->progress_owned) {  // full-chip launch: CTAs on SMs 0..groups-1 claim the lane groups
+            CUDA_TRY(cudaMemsetAsync(e->d_pick, 0, sizeof(int) * (1 + static_cast<size_t>(cta_count(e))), e->stream));
+            a.pick = e->d_pick;
+            grid = static_cast<unsigned>(e->claim_grid);
+            smem = static_cast<unsigned>(e->claim_smem);
+        }
         const CUresult r = driver()->LaunchKernel(e->jit.function, grid, 1, 1, static_cast<unsigned>(32 * e->gen.warps), 1, 1,
-                                          static_cast<unsigned>(e->gen.smem_bytes), reinterpret_cast<CUstream>(e->stream),
-                                          params, nullptr);
+                                          smem, reinterpret_cast<CUstream>(e->stream), params, nullptr);
         if (r != CUDA_SUCCESS) {
             const char* msg = nullptr;
             driver()->GetErrorString(r, &msg);
