@@ -1499,6 +1499,7 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // read and write; every access is a single-thread one (C2)
     const bool solo = LPC == 1 && knob("EMTB200_CG_SOLO", 1) != 0 && knob("EMTB200_CG_SLCOPY", 1) != 0 &&
                       knob("EMTB200_CG_WARPMAJOR", 1) != 0 && knob("EMTB200_CG_STRAIGHT", 1) != 0 && opt.mode != 2;
+    const int srcl1 = knob("EMTB200_CG_SRCL1", solo ? 0 : 4);  // passes ahead the source row is prefetched into L1
     g.presrc = knob("EMTB200_CG_PRESRC", 0) != 0;
     g.srctab = !g.presrc && knob("EMTB200_CG_SRCTAB", 1) != 0;
     g.rcp = knob("EMTB200_CG_RCP", 1) != 0 && opt.mode != 2 && knob("EMTB200_CG_STRAIGHT", 1) != 0;
@@ -2258,6 +2259,14 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
       << "    const int step = a.step0 + it;\n"
       << "    const double t = (double)(step + 1) * " << lit(s.dt) << ";\n"
       << "    const double tn = (double)(step + 2) * " << lit(s.dt) << "; (void)tn;\n"
+      // the source-table row of pass it+4 into L1 (rows are 8*NSRC_ bytes, so a pass
+      // whose row starts a new line would otherwise wait on L2 in the Norton region;
+      // C3 -1.3%, profiles/ab/srcl1_r2.log; not in the solo form, where it measured +0.9%,
+      // nor with lane-varying source columns (C4 +1%: the row is mostly other CTAs' lanes)
+      << (srcl1 > 0 && !g.tab_ck.empty() && g.tab_shared() == static_cast<int>(g.tab_ck.size())
+              ? "    if (threadIdx.x == 0 && it + " + std::to_string(srcl1) + " < a.nsteps) asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"(a.srctab + (size_t)(it + " +
+                    std::to_string(srcl1) + ") * NSRC_));\n"
+              : std::string())
       << "    int wflag = 0; int bad = 0x7fffffff; int srow = -1; unsigned long long swbits = 0ull; bool dok = true;\n"
       << "    (void)t; (void)bad; (void)srow; (void)step; (void)swbits; (void)dok;\n"
       ;
