@@ -390,3 +390,28 @@ def test_execute_parallel_twin_equals_golden():
     assert rc == 0, L.emt_last_error()
     assert bitwise_equal(waves, g.waves)
     assert bitwise_equal(time, g.time)
+
+
+def test_full_chip_launch_concurrent_engines_claim_every_lane_group():
+    """Full-chip launch (one CTA per SM, lane group s taken on SM s; codegen.cpp bid_code):
+    three engines launched concurrently on their own streams compete for the same SMs,
+    so CTAs land on SMs whose group another CTA already holds or never gets; every lane
+    group must still run exactly once (CAS claims, spares take the free groups)."""
+    import bench
+    b, _ = bench.build_batch(96)  # three 32-lane groups of the C3 sweep (faults 0.10 s on)
+    steps = 2400
+    ref = engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width)
+    assert "launch=full-chip" in ref.summary, ref.summary
+    ref.reserve(steps)
+    ref.advance(steps, sync=True)
+    want = ref.waves().values
+    engs = [engine.Engine(b.schedule, b.initial, const_table=b.const_table, width=b.width) for _ in range(3)]
+    for e in engs:
+        e.reserve(steps)
+    for _ in range(steps // 200):  # interleaved launches of 200 passes on three streams
+        for e in engs:
+            e.advance(200)
+    for e in engs:
+        e.sync()
+        assert bitwise_equal(e.waves().values, want)
+        assert len(e.events()) == len(ref.events())
