@@ -129,6 +129,11 @@ __device__ __forceinline__ void sys_wait_chunk(const SysPlan& S, unsigned char* 
     }
 }
 
+// IEEE division out of line: an inline `x / d` in one arm of the guarded-Markstein
+// selection is if-converted by the compiler, i.e. evaluated (slow path included) for
+// every quotient, also when the fast arm is taken
+__device__ __noinline__ double sys_div_ieee(double x, double d) { return x / d; }
+
 // Pivot reciprocal with the Markstein range of codegen.cpp (EMT_RCP): NaN outside [2^-60, 2^960].
 __device__ __forceinline__ double sys_rcp(double u) {
     return (fabs(u) >= 0x1p-60 && fabs(u) <= 0x1p960) ? 1.0 / u : __longlong_as_double(0x7ff8000000000000LL);
@@ -204,6 +209,7 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
     double* fuv = reinterpret_cast<double*>(sm + S.smem_ring_v);  // [kSysFD][1024] (the TMA ring is idle here)
     int* fuc = reinterpret_cast<int*>(sm + S.smem_ring_c);
     double* fdr = reinterpret_cast<double*>(sm + S.smem_desc);    // [kSysFD][2]
+    int4* fde = reinterpret_cast<int4*>(sm + S.smem_pbuf);        // [kSysFD] lent entries (pbuf idle here)
     long long tf = clock64();
     for (int i = 0; i < P.dim; ++i) {
         const int lb = __ldg(&P.l_row_ptr[i]), le = __ldg(&P.l_row_ptr[i + 1]);
@@ -211,8 +217,9 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
         // operands of the row's first eliminations in flight (cp.async into the idle TMA
         // ring): each thread's U entry and column, thread 0 the pivot and its reciprocal
         const int n = le - lb;
-        auto issue = [&](int k, int slot) {
-            const int4 e4 = __ldg(&S.lent[k]);  // c, U row [cb, ce)
+        // e4 = lent[k] (c, U row [cb, ce)), loaded one elimination before its issue so
+        // that no step waits on it; thread 0 keeps it in shared memory for the step
+        auto issue = [&](const int4 e4, int slot) {
             const int j = e4.y + 1 + tid;
             if (j < e4.z) {
                 sys_cp_async(fuv + slot * kSysThreads + tid, Uv + j, 8);
@@ -221,14 +228,18 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
             if (tid == 0) {
                 sys_cp_async(fdr + 2 * slot, Uv + e4.y, 8);
                 sys_cp_async(fdr + 2 * slot + 1, R + e4.x, 8);
+                fde[slot] = e4;
             }
         };
         const int nft = S.fact_threads;  // the other warps skip the eliminations (nothing to update)
-        if (tid < nft)
+        int4 e_nx = make_int4(0, 0, 0, 0);
+        if (tid < nft) {
             for (int q = 0; q < kSysFD - 1; ++q) {
-                if (q < n) issue(lb + q, q);
+                if (q < n) issue(__ldg(&S.lent[lb + q]), q);
                 sys_cp_commit();
             }
+            if (kSysFD - 1 < n) e_nx = __ldg(&S.lent[lb + kSysFD - 1]);
+        }
         // scatter row i of A over the union pattern, fill positions zero (sparse.cpp:94-110)
         for (int q = lb + tid; q < le; q += kSysThreads) Sx[__ldg(&P.l_col[q])] = 0.0;
         for (int q = ub + tid; q < ue; q += kSysThreads) Sx[__ldg(&P.u_col[q])] = 0.0;
@@ -243,9 +254,10 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
         if (tid < nft)
         for (int sidx = 0; sidx < n; ++sidx) {
             const int k = lb + sidx, slot = sidx % kSysFD;
-            if (sidx + kSysFD - 1 < n) issue(k + kSysFD - 1, (sidx + kSysFD - 1) % kSysFD);
+            if (sidx + kSysFD - 1 < n) issue(e_nx, (sidx + kSysFD - 1) % kSysFD);
             sys_cp_commit();
-            const int4 e4 = __ldg(&S.lent[k]);
+            if (sidx + kSysFD < n) e_nx = __ldg(&S.lent[k + kSysFD]);
+            const int4 e4 = fde[slot];
             const double x = Sx[e4.x], d = fdr[2 * slot], r = fdr[2 * slot + 1];
             // x / d: Markstein while |x r| is in range; a zero x (three in four L entries of the
             // gen_scale_case factors are exact zeros) gives x r = the signed zero x / d whenever
@@ -253,7 +265,7 @@ __device__ int sys_factorize(const DevPlan& P, const SysPlan& S, double* __restr
             const double q0 = x * r;
             const double lik = (fabs(q0) >= 0x1p-900 && fabs(q0) <= 0x1p900) ? __fma_rn(__fma_rn(-d, q0, x), r, q0)
                                : (x == 0.0 && r == r)                          ? q0
-                                                                               : x / d;
+                                                                               : sys_div_ieee(x, d);
             if (tid == 0) Lv[k] = lik;
             const int j = e4.y + 1 + tid;
             if (j < e4.z) {
@@ -524,7 +536,7 @@ __device__ int sys_solve(const DevPlan& P, const SysPlan& S, double* __restrict_
             else if (x == 0.0 && rcp == rcp)  // signed zero quotient (1/d in range)
                 x = q0;
             else
-                x = x / d;
+                x = sys_div_ieee(x, d);
             last = x;
             if (tl == 0) xs[i] = x;
             if (S.prof) {
