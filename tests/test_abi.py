@@ -108,3 +108,21 @@ def test_execute_parallel_rejects_nonpositive_workers_without_a_gpu():
                                 0, 10, None, None, None, None, None)
     assert rc == 1 + 19  # 1 + ErrorCode::NonPositiveInput (common.hpp:11-33)
     assert b"worker count" in L.emt_last_error()
+
+
+def test_codegen_full_chip_claim_and_source_prefetch():
+    """Generated launch prologue (codegen.cpp bid_code): lane groups are taken by CAS on
+    their flag, spares wait for every CTA or 20 us; the source-table row is prefetched
+    into L1 only when every source column is lane-invariant (C3), not for per-lane
+    columns (C4) nor in the solo form (C2). NVRTC compiles the C3 kernel for sm_100a."""
+    import bench
+    b, _ = bench.build_batch(96)
+    src, summary = engine.codegen(b.schedule, b.const_table, b.width, warps=8, compile=True)
+    assert "atomicCAS(a.pick + 1 + smid_, 0, 1)" in src and "%%globaltimer" in src and "cubin=" in summary
+    assert "prefetch.global.L1" in src
+    b4, _ = bench.build_batch(64, workload="c4")
+    src4, _ = engine.codegen(b4.schedule, b4.const_table, b4.width, warps=8)
+    assert "emt_src_kernel" in src4 and "prefetch.global.L1" not in src4
+    b2, _ = bench.build_batch(1, workload="c2")
+    src2, _ = engine.codegen(b2.schedule, b2.const_table, b2.width, warps=8)
+    assert "prefetch.global.L1" not in src2 and "atomicCAS(a.pick" in src2
