@@ -65,6 +65,26 @@ int knob(const char* name, int dflt) {
 int knob(const char*, int dflt) { return dflt; }
 #endif
 
+/// Per-warp bodies of a warp-major region ("    switch (warp) {" + one
+/// "    case w: {" ... "    } break;" per warp + "    }"), false if the text differs.
+bool split_warp_cases(const std::string& code, int G, std::vector<std::string>& bodies) {
+    const std::string head = "    switch (warp) {\n", brk = "    } break;\n";
+    if (code.compare(0, head.size(), head) != 0) return false;
+    bodies.assign(static_cast<size_t>(G), std::string());
+    size_t pos = head.size();
+    for (int w = 0; w < G; ++w) {
+        const std::string ch = "    case " + std::to_string(w) + ": {\n";
+        if (code.compare(pos, ch.size(), ch) != 0) return false;
+        pos += ch.size();
+        const std::string nxt = brk + (w + 1 < G ? "    case " + std::to_string(w + 1) + ": {\n" : std::string("    }\n"));
+        const size_t e = code.find(nxt, pos);
+        if (e == std::string::npos) return false;
+        bodies[static_cast<size_t>(w)] = code.substr(pos, e - pos);
+        pos = e + brk.size();
+    }
+    return code.compare(pos, std::string::npos, "    }\n") == 0;
+}
+
 std::string dev_knob_note() {
 #ifdef EMTB200_DEV_KNOBS
     return " devbuild" + (g_knobs_used.empty() ? std::string() : " knobs=" + g_knobs_used);
@@ -1947,8 +1967,10 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     };
     in_region_a = true;
     std::string code_a = region_code(sa, false);
+    const std::string code_a0 = code_a;
+    std::string code_af;
     if (!g.fused.empty()) {  // the launch's first pass reads i_prev from the arena; later passes recompute it
-        const std::string code_af = region_code(sa, true);
+        code_af = region_code(sa, true);
         code_a = "    if (__builtin_expect(it != 0, 1)) {\n" + code_af + "    } else {\n" + code_a + "    }\n";
     }
     in_region_a = false;
@@ -2101,6 +2123,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     // warps reach their phase barriers at different instructions: the non-.aligned
     // barrier form is the one the PTX ISA allows there (compute-sanitizer synccheck clean)
     o << "#define BAR() asm volatile(\"barrier.sync 0;\" ::: \"memory\")\n";
+    // non-aligned barrier reduction (warps arrive from different code): __syncthreads_or
+    o << "__device__ __forceinline__ bool emt_bar_or(bool p) { unsigned r_; asm volatile(\"{ .reg .pred pi_, po_; setp.ne.u32 pi_, %1, 0; "
+         "barrier.red.or.pred po_, 0, pi_; selp.u32 %0, 1, 0, po_; }\" : \"=r\"(r_) : \"r\"((unsigned)p) : \"memory\"); return r_ != 0; }\n";
     o << "#define PROF(id) do { if (a.prof && BID_ == 0 && lane == 0) { const long long c_ = clock64(); "
          "atomicAdd((unsigned long long*)(a.prof + warp * 64 + (id)), (unsigned long long)(c_ - prof_t)); prof_t = c_; } } while (0)\n";
     // a failing CTA leaves the step loop: release CTAs waiting on its progress word
@@ -2297,18 +2322,40 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     for (int x : s.watch)
         if (x >= 0 && !written_a.count(x)) o << "wflag |= (" << g.R(x) << " != 0.0); ";
     o << "}\n";
-    o << code_a;
-    o << "    if (__syncthreads_or(wflag)) {\n"
-      << (solo ? "      if (warp == 0 && lane == 0) {\n" : "      if (warp == 0) {\n")
-      << g.emit_refactor()
-      << "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
-      << "      }\n"
-      << "      if (__syncthreads_or(srow >= 0 && live)) {\n"
-      << "        if (warp == 0 && live && srow >= 0) { a.lane_err[4*gl] = 8; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = srow; a.lane_err[4*gl+3] = "
-      << g.fact_layer << "; }\n"
-      << "        FAILPUB(); return;\n"
-      << "      }\n"
-      << "    }\n";
+    const std::string refactor_block =
+        std::string(solo ? "      if (warp == 0 && lane == 0) {\n" : "      if (warp == 0) {\n") + g.emit_refactor() +
+        "        if (lane == 0) a.refac[a.row0 + it] = 1;\n"
+        "      }\n"
+        "      if (__syncthreads_or(srow >= 0 && live)) {\n"
+        "        if (warp == 0 && live && srow >= 0) { a.lane_err[4*gl] = 8; a.lane_err[4*gl+1] = step; a.lane_err[4*gl+2] = srow; a.lane_err[4*gl+3] = " +
+        std::to_string(g.fact_layer) + "; }\n"
+        "        FAILPUB(); return;\n"
+        "      }\n";
+    // one dispatch per pass: each warp's region A and region B code in one case, the A/B
+    // boundary a non-aligned barrier reduction inside the case; the rare refactorisation
+    // leaves the switch and re-enters the case after it. C3 -1.2%, C2 -1.6%, C4 -1.7%;
+    // not for shared factors (C5 +5.3%), profiles/ab/mergeab_r2.log
+    std::vector<std::string> ba0, baf, bb;
+    const bool merge_ab = knob("EMTB200_CG_MERGEAB", g.lu_shared ? 0 : 1) != 0 && straight && warp_major && !g.dmma && code_c.empty() &&
+                          split_warp_cases(code_a0, G, ba0) && (code_af.empty() || split_warp_cases(code_af, G, baf)) &&
+                          split_warp_cases(code_b, G, bb);
+    if (merge_ab) {
+        o << "    switch (warp) {\n";
+        for (int w = 0; w < G; ++w) {
+            o << "    case " << w << ": {\n";
+            if (!code_af.empty())
+                o << "    if (__builtin_expect(it != 0, 1)) {\n" << baf[static_cast<size_t>(w)] << "    } else {\n" << ba0[static_cast<size_t>(w)] << "    }\n";
+            else
+                o << ba0[static_cast<size_t>(w)];
+            o << "      if (emt_bar_or(wflag)) goto cold_ab_;\n    resume_ab_" << w << ":;\n" << bb[static_cast<size_t>(w)] << "    } break;\n";
+        }
+        o << "    }\n    if (false) {\n    cold_ab_:;\n" << refactor_block << "      switch (warp) {";
+        for (int w = 0; w < G; ++w) o << " case " << w << ": goto resume_ab_" << w << ";";
+        o << " default: break; }\n    }\n";
+    } else {
+        o << code_a;
+        o << "    if (__syncthreads_or(wflag)) {\n" << refactor_block << "    }\n";
+    }
     // progress release at the pass end: st.release after bar.sync orders the whole CTA's
     // earlier stores (PTX memory model: the barrier puts them before the releasing
     // thread's store in causality order). Releasing right after region A (C4 3.35 ->
@@ -2335,7 +2382,8 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     const std::string release =
         std::string("    if (a.progress != nullptr && threadIdx.x == ") + std::to_string(32 * rel_warp) + ") {\n" +
         rel_stmt("step + 1") + "    }\n";
-    o << code_b << dmma_block << code_c;
+    if (!merge_ab) o << code_b;
+    o << dmma_block << code_c;
     if (dok_mode) {
         // divergence (exec.cpp:229-237): rows only AND a NaN-safe predicate; the
         // failing node index (the lowest) is found in the cold path
