@@ -1660,10 +1660,11 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
     }
     const int G = std::max(1, std::min(opt.warps, 32));
     double span_a = 0, span_b = 0;
-    // a single lane (solo form) pays a barrier more than a 32-lane group does relative to
-    // its tasks: fewer, fuller phases (barrier cost 100 -> 400: C2 2.63 -> 2.55 us; the
-    // same setting costs C3 1%, so 32-lane groups keep 100)
-    const long bar_cost = solo ? 400 : 100;
+    // barrier cost in the list scheduler's model (cycles): fewer, fuller phases pay off
+    // up to ~250 with one warp dispatch per pass (C3 -1.9%, C4 -0.4%, C2 -0.5% against
+    // 100 / 400 for the solo form; 60, 150, 350, 500, 700 measured worse or mixed,
+    // profiles/ab/barrier_r2.log); the shared-factor kernel keeps 100 (250: C5 +3.7%)
+    const long bar_cost = g.lu_shared ? 100 : 250;
     Sched sa = schedule_region(g.tasks, ids_a, deps, G, &span_a, bar_cost);
     if (sa.phases.size() == 1 && knob("EMTB200_CG_AFFINITY", 1) != 0) {
         // region A is one phase of independent tasks: regroup them so that tasks reading
