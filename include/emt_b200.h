@@ -266,8 +266,10 @@ emt_status emt_engine_profile(emt_engine* engine, int64_t* cycles, int32_t n);
 emt_status emt_engine_attach_lines(emt_engine* engine, void* mirror, void* progress, int32_t cta_offset,
                                    int32_t total_ctas, int32_t system_scope);
 
-/* CTAs of this engine's launches and lanes per CTA (0 for the generic kernel):
- * the progress-array span emt_engine_attach_lines expects from this engine. */
+/* Lane groups of this engine (one CTA each; with the full-chip launch of the
+ * specialised kernel the group of SM s runs on SM s and the other CTAs exit) and
+ * lanes per group (0 for the generic kernel): the progress-array span
+ * emt_engine_attach_lines expects from this engine. */
 emt_status emt_engine_ctas(const emt_engine* engine, int32_t* ctas, int32_t* lanes_per_cta);
 /* CUDA IPC helpers for the shared mirror / progress arrays: `handle` is 64 bytes. */
 emt_status emt_ipc_alloc(int32_t device, int64_t bytes, void** ptr, void* handle);
