@@ -1658,7 +1658,9 @@ bool generate_kernel(const Schedule& s, const std::vector<double>& ctab, int lan
         }
         (g.tasks[i].region == 0 ? ids_a : g.tasks[i].region == 1 ? ids_b : ids_c).push_back(static_cast<int>(i));
     }
-    const int G = std::max(1, std::min(opt.warps, 32));
+    // the shared-factor kernel (C5) runs its chain-bound pass best on 6 warps
+    // (5.86 vs 5.99 ms at 8, 4 and 12 worse; profiles/ab/warps_r2.log)
+    const int G = std::max(1, std::min(opt.auto_warps && g.lu_shared && !g.dmma ? 6 : opt.warps, 32));
     double span_a = 0, span_b = 0;
     // barrier cost in the list scheduler's model (cycles): fewer, fuller phases pay off
     // up to ~250 with one warp dispatch per pass (C3 -1.9%, C4 -0.4%, C2 -0.5% against

@@ -18,6 +18,7 @@ namespace emtb200 {
 
 struct CodegenOptions {
     int warps = 4;                  // warps per CTA (work partitions of one 32-lane group)
+    bool auto_warps = false;        // warps chosen by the engine: the generator may pick its own count
     size_t smem_budget = 227 * 1024;  // bytes of dynamic shared memory per CTA
     bool lu_in_smem = true;         // keep L/U factors on chip when they fit
     int mode = 0;                   // 0 auto, 1 straight-line tasks, 2 compact per-type loops

@@ -1244,6 +1244,7 @@ static emt_status engine_create(const char* schedule_text, const double* const_t
         // host thread and switch to it at the first launch after it is ready
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
+        opt.auto_warps = c.warps_per_group <= 0;
         opt.exact_division = (c.flags & EMT_FLAG_EXACT_DIVISION) != 0;
         int dev_smem = 0;
         CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device));
@@ -1281,6 +1282,7 @@ static emt_status engine_create(const char* schedule_text, const double* const_t
     if (c.kernel != EMT_KERNEL_GENERIC) {
         CodegenOptions opt;
         opt.warps = c.warps_per_group > 0 ? c.warps_per_group : 8;
+        opt.auto_warps = c.warps_per_group <= 0;
         opt.tensor_solve = (c.flags & EMT_FLAG_TENSOR_SOLVE) != 0;
         opt.exact_division = (c.flags & EMT_FLAG_EXACT_DIVISION) != 0;
         int dev_smem = 0;
