@@ -36,8 +36,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
+FLAVOUR = LIB + ".flavour"  # "dev" or "product": the build the library was made as
+
+
+def stale(dev: bool = False) -> bool:
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(FLAVOUR) as f:
+            if f.read().strip() != ("dev" if dev else "product"):
+                return True  # a product build after a dev build (or the reverse) recompiles
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
@@ -46,13 +55,15 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
     """dev=True: a developer build whose generator reads EMTB200_CG_* A/B knobs from the
     environment (the product build ignores the environment; bench.py refuses a dev build)."""
-    if not force and not stale():
+    if not force and not stale(dev):
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, *(["-DEMTB200_DEV_KNOBS"] if dev else []), "-o", LIB, *SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
+    with open(FLAVOUR, "w") as f:
+        f.write("dev" if dev else "product")
     return LIB
 
 
