@@ -1,4 +1,4 @@
-"""Property-style parity: 24 seeded random documents (tests/golden/docs.py:fuzz — every
+"""Property-style parity: 64 seeded random documents (tests/golden/docs.py:fuzz — every
 electrical kind, meshed topologies, breakers toggling several times, AC and DC
 sources, a meter -> control chain -> actuator loop through all control kinds)
 compiled and run by the REAL reference (tools/make_fuzz_fixtures.py). The C oracle
@@ -29,7 +29,7 @@ def load(name):
 
 
 def test_fuzz_set_present():
-    assert len(CASES) >= 38
+    assert len(CASES) >= 78
 
 
 @pytest.mark.parametrize("name", CASES)

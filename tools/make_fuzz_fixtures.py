@@ -4,6 +4,7 @@ tests/golden/fuzz/fuzz_<seed>.{cgmsched.gz,state.gz,npz} (waves, time,
 factor_count, or the reference's error code and message).
 
     make -C oracle ref && python tools/make_fuzz_fixtures.py [count]
+    python -c "import tools.make_fuzz_fixtures as m; m.main(64, start=24)"   # add seeds 24..63 only
 """
 import gzip
 import json
@@ -22,9 +23,9 @@ import docs  # noqa: E402
 OUT = os.path.join(ROOT, "tests", "golden", "fuzz")
 
 
-def main(count):
+def main(count, start=0):
     os.makedirs(OUT, exist_ok=True)
-    for seed in range(count):
+    for seed in range(start, count):
         doc = docs.fuzz(seed)
         c = ref.compile_document(doc)
         steps = json.loads(doc)["task"]["duration"] / json.loads(doc)["task"]["dt"]
